@@ -1,0 +1,591 @@
+// qapb.cu -- C ABI (include/qapb.h) over the sm_100a search kernels.
+//
+// Host responsibilities: value-range analysis of the instance (int32 vs int64
+// on-chip state), packing (zero-diagonal int32 copies of F, D and their
+// transposes, padded to a multiple of 4), kernel configuration (CTA size, units
+// per thread, where the placement matrix lives), workspace and launches.
+#include "../../include/qapb.h"
+#include "search_kernel.cuh"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+using namespace qapb;
+
+static thread_local std::string g_err;
+static int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+#define CU(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(QAPB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct qapb_handle {
+    int n = 0, nb = 0, npad = 0, device = 0;
+    int acc_bits = 32, symmetric = 0;
+    int nunits = 0, noff = 0, threads = 0, upt = 0, storage = 0;
+    int lb_class = 0;  // 0: <=384 threads, 2 CTAs/SM register budget; 1: <=512 threads
+    unsigned smem_bytes = 0;
+    int ctas_per_sm = 0, sm_count = 0;
+    long long delta_bound = 0;
+    int32_t *dF = nullptr, *dFT = nullptr, *dD = nullptr, *dDT = nullptr, *dfd = nullptr, *ddd = nullptr;
+    uint16_t *dunit = nullptr;
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int have_timing = 0;
+    int force_seq_rng = 0;
+};
+
+typedef void (*kern_t)(const SearchParams);
+static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
+{
+#define K(A, S, MT, MB) (kern_t) qap_search_kernel<A, S, MT, MB>
+    static kern_t tab[2][3][2] = {
+        {{K(int32_t, 0, 384, 2), K(int32_t, 0, 512, 1)},
+         {K(int32_t, 1, 384, 2), K(int32_t, 1, 512, 1)},
+         {K(int32_t, 2, 384, 2), K(int32_t, 2, 512, 1)}},
+        {{K(int64_t, 0, 384, 1), K(int64_t, 0, 512, 1)},
+         {K(int64_t, 1, 384, 1), K(int64_t, 1, 512, 1)},
+         {K(int64_t, 2, 384, 1), K(int64_t, 2, 512, 1)}},
+    };
+#undef K
+    return tab[acc_bits == 64][storage][lb_class];
+}
+
+extern "C" int qapb_version(void) { return 1; }
+extern "C" const char *qapb_last_error(void) { return g_err.c_str(); }
+extern "C" int qapb_device_count(int *count)
+{
+    if (!count) return fail(QAPB_ERR_INVALID, "count is NULL");
+    CU(cudaGetDeviceCount(count));
+    return QAPB_OK;
+}
+
+static int ensure_ws(qapb_handle *h, size_t bytes)
+{
+    if (bytes <= h->ws_bytes) return QAPB_OK;
+    if (h->ws) cudaFree(h->ws);
+    h->ws = nullptr;
+    h->ws_bytes = 0;
+    size_t want = bytes + bytes / 4 + 4096;
+    if (cudaMalloc(&h->ws, want) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(QAPB_ERR_NOMEM, "workspace allocation of " + std::to_string(want) + " bytes failed");
+    }
+    h->ws_bytes = want;
+    return QAPB_OK;
+}
+
+// Upper bound on |M[a][b]| and |h[a]| over all permutations: rearrangement
+// inequality on sorted absolute rows/columns, plus the direct and diagonal terms.
+static double placement_bound(int n, const std::vector<long long> &F0, const std::vector<long long> &D0,
+                              const std::vector<long long> &fd, const std::vector<long long> &dd, bool refined)
+{
+    long long maxF = 0, maxD = 0, maxfd = 0, maxdd = 0;
+    for (long long v : F0) maxF = std::max(maxF, std::llabs(v));
+    for (long long v : D0) maxD = std::max(maxD, std::llabs(v));
+    for (long long v : fd) maxfd = std::max(maxfd, std::llabs(v));
+    for (long long v : dd) maxdd = std::max(maxdd, std::llabs(v));
+    double extra = 2.0 * (double)maxD * (double)maxF + (double)maxfd * (double)maxdd;
+    if (!refined) return 2.0 * n * (double)maxD * (double)maxF + extra;
+    std::vector<std::vector<double>> dr(n), dc(n), fr(n), fc(n);
+    for (int a = 0; a < n; ++a) {
+        dr[a].resize(n); dc[a].resize(n); fr[a].resize(n); fc[a].resize(n);
+        for (int k = 0; k < n; ++k) {
+            dr[a][k] = (double)std::llabs(D0[(size_t)a * n + k]);
+            dc[a][k] = (double)std::llabs(D0[(size_t)k * n + a]);
+            fr[a][k] = (double)std::llabs(F0[(size_t)a * n + k]);
+            fc[a][k] = (double)std::llabs(F0[(size_t)k * n + a]);
+        }
+        std::sort(dr[a].begin(), dr[a].end(), std::greater<double>());
+        std::sort(dc[a].begin(), dc[a].end(), std::greater<double>());
+        std::sort(fr[a].begin(), fr[a].end(), std::greater<double>());
+        std::sort(fc[a].begin(), fc[a].end(), std::greater<double>());
+    }
+    double best = 0;
+    for (int a = 0; a < n; ++a)
+        for (int u = 0; u < n; ++u) {
+            double s = 0;
+            for (int k = 0; k < n; ++k) s += dr[a][k] * fr[u][k] + dc[a][k] * fc[u][k];
+            best = std::max(best, s);
+        }
+    return best + extra;
+}
+
+extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int device, qapb_handle **out)
+{
+    if (!out) return fail(QAPB_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    if (n < 2) return fail(QAPB_ERR_INVALID, "instance size must be >= 2, got " + std::to_string(n));
+    if (!flow || !dist) return fail(QAPB_ERR_INVALID, "matrix pointer is NULL");
+    if (n > 1020) return fail(QAPB_ERR_UNSUPPORTED, "n > 1020 is not supported");
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return fail(QAPB_ERR_INVALID, "device " + std::to_string(device) + " out of range (" + std::to_string(ndev) + " devices)");
+    CU(cudaSetDevice(device));
+
+    const int nb = (n + 3) / 4, npad = nb * 4;
+    std::vector<long long> F0((size_t)n * n), D0((size_t)n * n), fd(n), dd(n);
+    bool sym = true;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            long long f = flow[(size_t)i * n + j], d = dist[(size_t)i * n + j];
+            if (std::llabs(f) >= (1LL << 30) || std::llabs(d) >= (1LL << 30))
+                return fail(QAPB_ERR_UNSUPPORTED, "matrix entries must satisfy |x| < 2^30");
+            if (i == j) { fd[i] = f; dd[i] = d; f = 0; d = 0; }
+            F0[(size_t)i * n + j] = f;
+            D0[(size_t)i * n + j] = d;
+            if (i != j && (flow[(size_t)i * n + j] != flow[(size_t)j * n + i] || dist[(size_t)i * n + j] != dist[(size_t)j * n + i]))
+                sym = false;
+        }
+
+    qapb_handle *h = new qapb_handle();
+    h->n = n; h->nb = nb; h->npad = npad; h->device = device; h->symmetric = sym ? 1 : 0;
+
+    // accumulator width: |delta| <= 4 * bound must stay below 2^31-1 for the int32 state
+    const double lim32 = 2147483647.0 / 4.0 - 8.0;
+    double bnd = placement_bound(n, F0, D0, fd, dd, false);
+    if (bnd >= lim32) bnd = placement_bound(n, F0, D0, fd, dd, true);
+    h->acc_bits = bnd < lim32 ? 32 : 64;
+    if (bnd >= 9.0e18 / 4.0) {
+        delete h;
+        return fail(QAPB_ERR_UNSUPPORTED, "delta bound exceeds int64");
+    }
+    h->delta_bound = (long long)std::min(4.0 * bnd, 9.0e18);
+
+    // units and CTA shape
+    h->noff = nb * (nb - 1) / 2;
+    h->nunits = h->noff + nb;
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    h->sm_count = prop.multiProcessorCount;
+    const unsigned smem_cap = (unsigned)prop.sharedMemPerBlockOptin;
+    const int acc_bytes = h->acc_bits / 8;
+    int upt = (h->nunits + 383) / 384;
+    if (upt < 1) upt = 1;
+    int threads = ((h->nunits + upt - 1) / upt + 31) / 32 * 32;
+    if (threads < 32) threads = 32;
+    if (threads < ((n + 31) / 32) * 32 && ((n + 31) / 32) * 32 <= 384) threads = ((n + 31) / 32) * 32;
+    h->upt = upt;
+    h->threads = threads;
+    h->lb_class = threads <= 384 ? 0 : 1;
+    int storage = 0;
+    for (; storage < 3; ++storage) {
+        SmemLayout L = make_layout(npad, h->nunits, threads, upt, acc_bytes, storage);
+        if (L.total <= smem_cap) { h->smem_bytes = L.total; break; }
+    }
+    if (storage == 3) {
+        delete h;
+        return fail(QAPB_ERR_UNSUPPORTED, "instance too large for shared-memory vectors");
+    }
+    h->storage = storage;
+
+    // device copies
+    std::vector<int32_t> pF((size_t)npad * npad, 0), pFT((size_t)npad * npad, 0), pD((size_t)npad * npad, 0), pDT((size_t)npad * npad, 0);
+    std::vector<int32_t> pfd(npad, 0), pdd(npad, 0);
+    for (int i = 0; i < n; ++i) {
+        pfd[i] = (int32_t)fd[i];
+        pdd[i] = (int32_t)dd[i];
+        for (int j = 0; j < n; ++j) {
+            pF[(size_t)i * npad + j] = (int32_t)F0[(size_t)i * n + j];
+            pFT[(size_t)j * npad + i] = (int32_t)F0[(size_t)i * n + j];
+            pD[(size_t)i * npad + j] = (int32_t)D0[(size_t)i * n + j];
+            pDT[(size_t)j * npad + i] = (int32_t)D0[(size_t)i * n + j];
+        }
+    }
+    std::vector<uint16_t> units(h->nunits);
+    {
+        int u = 0;
+        for (int I = 0; I < nb; ++I)
+            for (int J = I + 1; J < nb; ++J) units[u++] = (uint16_t)(I | (J << 8));
+        for (int I = 0; I < nb; ++I) units[u++] = (uint16_t)(I | (I << 8));
+    }
+    const size_t mb = (size_t)npad * npad * sizeof(int32_t);
+    auto up = [&](void **dst, const void *src, size_t bytes) -> cudaError_t {
+        cudaError_t e = cudaMalloc(dst, bytes);
+        if (e != cudaSuccess) return e;
+        return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+    };
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = up((void **)&h->dF, pF.data(), mb);
+    if (e == cudaSuccess) e = up((void **)&h->dFT, pFT.data(), mb);
+    if (e == cudaSuccess) e = up((void **)&h->dD, pD.data(), mb);
+    if (e == cudaSuccess) e = up((void **)&h->dDT, pDT.data(), mb);
+    if (e == cudaSuccess) e = up((void **)&h->dfd, pfd.data(), npad * sizeof(int32_t));
+    if (e == cudaSuccess) e = up((void **)&h->ddd, pdd.data(), npad * sizeof(int32_t));
+    if (e == cudaSuccess) e = up((void **)&h->dunit, units.data(), units.size() * sizeof(uint16_t));
+    if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
+    kern_t kern = pick_kernel(h->acc_bits, h->storage, h->lb_class);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, (const void *)kern, h->threads, h->smem_bytes);
+    if (e != cudaSuccess) {
+        std::string msg = std::string("instance upload failed: ") + cudaGetErrorString(e);
+        qapb_destroy(h);
+        return fail(QAPB_ERR_CUDA, msg);
+    }
+    *out = h;
+    return QAPB_OK;
+}
+
+extern "C" int qapb_destroy(qapb_handle *h)
+{
+    if (!h) return QAPB_OK;
+    cudaSetDevice(h->device);
+    cudaFree(h->dF); cudaFree(h->dFT); cudaFree(h->dD); cudaFree(h->dDT);
+    cudaFree(h->dfd); cudaFree(h->ddd); cudaFree(h->dunit); cudaFree(h->ws);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    delete h;
+    return QAPB_OK;
+}
+
+extern "C" int qapb_get_info(const qapb_handle *h, qapb_info *info)
+{
+    if (!h || !info) return fail(QAPB_ERR_INVALID, "NULL argument");
+    info->n = h->n; info->device = h->device; info->acc_bits = h->acc_bits; info->symmetric = h->symmetric;
+    info->threads = h->threads; info->units_per_thread = h->upt; info->storage = h->storage;
+    info->smem_bytes = (int32_t)h->smem_bytes; info->ctas_per_sm = h->ctas_per_sm; info->sm_count = h->sm_count;
+    info->delta_bound = h->delta_bound;
+    return QAPB_OK;
+}
+
+// test hook (not declared in the public header): force the sequential RNG path
+extern "C" int qapb_debug_force_seq_rng(qapb_handle *h, int on)
+{
+    if (!h) return fail(QAPB_ERR_INVALID, "NULL handle");
+    h->force_seq_rng = on;
+    return QAPB_OK;
+}
+
+static void base_params(const qapb_handle *h, SearchParams &P)
+{
+    memset(&P, 0, sizeof(P));
+    P.n = h->n; P.nb = h->nb; P.npad = h->npad; P.nunits = h->nunits; P.noff = h->noff; P.upt = h->upt;
+    P.symmetric = h->symmetric;
+    P.force_seq_rng = h->force_seq_rng;
+    P.F = h->dF; P.FT = h->dFT; P.D = h->dD; P.DT = h->dDT; P.fd = h->dfd; P.dd = h->ddd;
+    P.unit_ij = h->dunit;
+}
+
+// Launch the search kernel for `batch` starts.  `extra_ws` bytes are reserved at
+// the start of the workspace for the caller (multistart keeps best perms there).
+static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extra_ws, cudaStream_t st)
+{
+    const size_t acc_bytes = h->acc_bits / 8;
+    const size_t m_elems = (size_t)h->upt * 8 * h->threads * 4;
+    const size_t t_elems = (size_t)h->upt * 4 * h->threads * 4;
+    size_t need = (extra_ws + 255) / 256 * 256;
+    size_t offM = need;
+    if (h->storage >= 1 && P.mode != MODE_ALL_DELTAS) need += m_elems * acc_bytes * batch;
+    size_t offT = need;
+    if (h->storage >= 2 && P.mode != MODE_ALL_DELTAS) need += t_elems * sizeof(int32_t) * batch;
+    int rc = ensure_ws(h, need);
+    if (rc) return rc;
+    P.gM = (char *)h->ws + offM;
+    P.gT = (char *)h->ws + offT;
+    P.gM_stride = m_elems;
+    P.gT_stride = t_elems;
+    kern_t kern = pick_kernel(h->acc_bits, h->storage, h->lb_class);
+    CU(cudaEventRecord(h->ev0, st));
+    kern<<<batch, h->threads, h->smem_bytes, st>>>(P);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(h->ev1, st));
+    h->have_timing = 1;
+    return QAPB_OK;
+}
+
+static int check_common(qapb_handle *h, int batch)
+{
+    if (!h) return fail(QAPB_ERR_INVALID, "NULL handle");
+    if (batch < 1) return fail(QAPB_ERR_INVALID, "batch must be >= 1, got " + std::to_string(batch));
+    CU(cudaSetDevice(h->device));
+    return QAPB_OK;
+}
+
+extern "C" int qapb_full_cost(qapb_handle *h, const int64_t *perms, int batch, int64_t *costs, void *stream)
+{
+    int rc = check_common(h, batch);
+    if (rc) return rc;
+    if (!perms || !costs) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    qap_full_cost_kernel<<<batch, 256, h->npad * sizeof(int32_t), (cudaStream_t)stream>>>(
+        h->n, h->npad, h->dF, h->dD, h->dfd, h->ddd, perms, costs);
+    CU(cudaGetLastError());
+    return QAPB_OK;
+}
+
+extern "C" int qapb_all_deltas(qapb_handle *h, const int64_t *perms, int batch, int64_t *deltas, void *stream)
+{
+    int rc = check_common(h, batch);
+    if (rc) return rc;
+    if (!perms || !deltas) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    SearchParams P;
+    base_params(h, P);
+    P.mode = MODE_ALL_DELTAS;
+    P.perms = perms;
+    P.out_deltas = deltas;
+    return launch_search(h, P, batch, 0, (cudaStream_t)stream);
+}
+
+extern "C" int qapb_two_opt(qapb_handle *h, const int64_t *perms, int batch, int iterations, int64_t *best,
+                            int64_t *best_cost, int64_t *cur, int64_t *cur_cost, int64_t *move_i,
+                            int64_t *move_j, int64_t *move_delta, void *stream)
+{
+    int rc = check_common(h, batch);
+    if (rc) return rc;
+    if (iterations < 1) return fail(QAPB_ERR_INVALID, "iterations must be >= 1, got " + std::to_string(iterations));
+    if (!perms || !best || !best_cost || !cur || !cur_cost) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    if ((move_i || move_j || move_delta) && !(move_i && move_j && move_delta))
+        return fail(QAPB_ERR_INVALID, "move_i/move_j/move_delta must be given together");
+    SearchParams P;
+    base_params(h, P);
+    P.mode = MODE_TWO_OPT;
+    P.iterations = iterations;
+    P.perms = perms;
+    P.best = best; P.best_cost = best_cost; P.cur = cur; P.cur_cost = cur_cost;
+    P.tr_i = move_i; P.tr_j = move_j; P.tr_d = move_delta;
+    return launch_search(h, P, batch, 0, (cudaStream_t)stream);
+}
+
+extern "C" int qapb_tabu(qapb_handle *h, const int64_t *perms, int batch, int iterations, const int64_t *tenures,
+                         int64_t *best, int64_t *best_cost, int64_t *cur, int64_t *cur_cost, int64_t *cells,
+                         int64_t *stopped_early, int64_t *steps_done, int64_t *trail_i, int64_t *trail_j,
+                         int64_t *trail_delta, int64_t *trail_tabu, void *stream)
+{
+    int rc = check_common(h, batch);
+    if (rc) return rc;
+    if (iterations < 1) return fail(QAPB_ERR_INVALID, "iterations must be >= 1, got " + std::to_string(iterations));
+    if (!perms || !tenures || !best || !best_cost || !cur || !cur_cost) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    if ((trail_i || trail_j || trail_delta || trail_tabu) && !(trail_i && trail_j && trail_delta && trail_tabu))
+        return fail(QAPB_ERR_INVALID, "trail arrays must be given together");
+    SearchParams P;
+    base_params(h, P);
+    P.mode = MODE_TABU;
+    P.iterations = iterations;
+    P.perms = perms;
+    P.tenures = tenures;
+    P.best = best; P.best_cost = best_cost; P.cur = cur; P.cur_cost = cur_cost;
+    P.cells = cells; P.stopped = stopped_early; P.steps = steps_done;
+    P.tr_i = trail_i; P.tr_j = trail_j; P.tr_d = trail_delta; P.tr_tabu = trail_tabu;
+    return launch_search(h, P, batch, 0, (cudaStream_t)stream);
+}
+
+extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, uint64_t first_index, int count,
+                               int iterations, int64_t ten_low, int64_t ten_high, int64_t *per_start_costs,
+                               int64_t *best_key, int64_t *best_perm, void *stream)
+{
+    int rc = check_common(h, count);
+    if (rc) return rc;
+    if (algo != QAPB_ALGO_2OPT && algo != QAPB_ALGO_TABU) return fail(QAPB_ERR_INVALID, "unknown algorithm " + std::to_string(algo));
+    if (iterations < 1) return fail(QAPB_ERR_INVALID, "iterations must be >= 1, got " + std::to_string(iterations));
+    if (algo == QAPB_ALGO_TABU && !(1 <= ten_low && ten_low <= ten_high))
+        return fail(QAPB_ERR_INVALID, "invalid tenure interval [" + std::to_string(ten_low) + ", " + std::to_string(ten_high) + "]");
+    if (algo == QAPB_ALGO_TABU && (double)iterations + (double)ten_high >= 2147483647.0)
+        return fail(QAPB_ERR_UNSUPPORTED, "iterations + tenure must fit int32");
+    if (!per_start_costs || !best_key || !best_perm) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    const int n = h->n;
+    // workspace head: best perms [count,n], cur perms [count,n], cur costs [count]
+    const size_t perm_bytes = (size_t)count * n * sizeof(int64_t);
+    const size_t head = 2 * perm_bytes + (size_t)count * sizeof(int64_t);
+    SearchParams P;
+    base_params(h, P);
+    rc = ensure_ws(h, head + 256);  // make h->ws valid before taking addresses; launch_search may regrow
+    if (rc) return rc;
+    P.mode = algo == QAPB_ALGO_TABU ? MODE_TABU : MODE_TWO_OPT;
+    P.rng = 1;
+    P.iterations = iterations;
+    P.master_seed = master_seed;
+    P.first_index = first_index;
+    P.ten_lo = ten_low;
+    P.ten_hi = ten_high;
+    // compute total need first so the head pointers stay valid
+    {
+        const size_t acc_bytes = h->acc_bits / 8;
+        const size_t m_elems = (size_t)h->upt * 8 * h->threads * 4, t_elems = (size_t)h->upt * 4 * h->threads * 4;
+        size_t need = (head + 255) / 256 * 256;
+        if (h->storage >= 1) need += m_elems * acc_bytes * count;
+        if (h->storage >= 2) need += t_elems * sizeof(int32_t) * count;
+        rc = ensure_ws(h, need);
+        if (rc) return rc;
+    }
+    int64_t *w_best = (int64_t *)h->ws;
+    int64_t *w_cur = (int64_t *)((char *)h->ws + perm_bytes);
+    int64_t *w_curcost = (int64_t *)((char *)h->ws + 2 * perm_bytes);
+    P.best = w_best; P.best_cost = per_start_costs; P.cur = w_cur; P.cur_cost = w_curcost;
+    rc = launch_search(h, P, count, head, (cudaStream_t)stream);
+    if (rc) return rc;
+    qap_pick_best_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(count, n, first_index, per_start_costs, w_best, best_key, best_perm);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(h->ev1, (cudaStream_t)stream));
+    return QAPB_OK;
+}
+
+extern "C" int qapb_last_kernel_ms(qapb_handle *h, float *ms)
+{
+    if (!h || !ms) return fail(QAPB_ERR_INVALID, "NULL argument");
+    if (!h->have_timing) return fail(QAPB_ERR_INVALID, "no launch recorded");
+    CU(cudaSetDevice(h->device));
+    CU(cudaEventSynchronize(h->ev1));
+    CU(cudaEventElapsedTime(ms, h->ev0, h->ev1));
+    return QAPB_OK;
+}
+
+// ------------------------------------------------------------ host variants --
+namespace {
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+    cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 1); }
+    template <typename T> T *as() { return (T *)p; }
+};
+}  // namespace
+#define H2D(dst, src, bytes) CU(cudaMemcpy((dst), (src), (bytes), cudaMemcpyHostToDevice))
+#define D2H(dst, src, bytes) CU(cudaMemcpy((dst), (src), (bytes), cudaMemcpyDeviceToHost))
+
+extern "C" int qapb_full_cost_host(qapb_handle *h, const int64_t *perms, int batch, int64_t *costs)
+{
+    int rc = check_common(h, batch);
+    if (rc) return rc;
+    if (!perms || !costs) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    DevBuf dp, dc;
+    const size_t pb = (size_t)batch * h->n * 8;
+    CU(dp.alloc(pb)); CU(dc.alloc((size_t)batch * 8));
+    H2D(dp.p, perms, pb);
+    rc = qapb_full_cost(h, dp.as<int64_t>(), batch, dc.as<int64_t>(), nullptr);
+    if (rc) return rc;
+    D2H(costs, dc.p, (size_t)batch * 8);
+    return QAPB_OK;
+}
+
+extern "C" int qapb_all_deltas_host(qapb_handle *h, const int64_t *perms, int batch, int64_t *deltas)
+{
+    int rc = check_common(h, batch);
+    if (rc) return rc;
+    if (!perms || !deltas) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    DevBuf dp, dd;
+    const size_t pb = (size_t)batch * h->n * 8, ob = (size_t)batch * ((size_t)h->n * (h->n - 1) / 2) * 8;
+    CU(dp.alloc(pb)); CU(dd.alloc(ob));
+    H2D(dp.p, perms, pb);
+    rc = qapb_all_deltas(h, dp.as<int64_t>(), batch, dd.as<int64_t>(), nullptr);
+    if (rc) return rc;
+    D2H(deltas, dd.p, ob);
+    return QAPB_OK;
+}
+
+extern "C" int qapb_two_opt_host(qapb_handle *h, const int64_t *perms, int batch, int iterations, int64_t *best,
+                                 int64_t *best_cost, int64_t *cur, int64_t *cur_cost, int64_t *move_i,
+                                 int64_t *move_j, int64_t *move_delta)
+{
+    int rc = check_common(h, batch);
+    if (rc) return rc;
+    if (iterations < 1) return fail(QAPB_ERR_INVALID, "iterations must be >= 1, got " + std::to_string(iterations));
+    if (!perms || !best || !best_cost || !cur || !cur_cost) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    const bool tr = move_i && move_j && move_delta;
+    const size_t pb = (size_t)batch * h->n * 8, sb = (size_t)batch * 8, tb = (size_t)batch * iterations * 8;
+    DevBuf dp, dbest, dbc, dcur, dcc, dmi, dmj, dmd;
+    CU(dp.alloc(pb)); CU(dbest.alloc(pb)); CU(dbc.alloc(sb)); CU(dcur.alloc(pb)); CU(dcc.alloc(sb));
+    if (tr) { CU(dmi.alloc(tb)); CU(dmj.alloc(tb)); CU(dmd.alloc(tb)); }
+    H2D(dp.p, perms, pb);
+    rc = qapb_two_opt(h, dp.as<int64_t>(), batch, iterations, dbest.as<int64_t>(), dbc.as<int64_t>(), dcur.as<int64_t>(),
+                      dcc.as<int64_t>(), tr ? dmi.as<int64_t>() : nullptr, tr ? dmj.as<int64_t>() : nullptr,
+                      tr ? dmd.as<int64_t>() : nullptr, nullptr);
+    if (rc) return rc;
+    D2H(best, dbest.p, pb); D2H(best_cost, dbc.p, sb); D2H(cur, dcur.p, pb); D2H(cur_cost, dcc.p, sb);
+    if (tr) { D2H(move_i, dmi.p, tb); D2H(move_j, dmj.p, tb); D2H(move_delta, dmd.p, tb); }
+    return QAPB_OK;
+}
+
+extern "C" int qapb_tabu_host(qapb_handle *h, const int64_t *perms, int batch, int iterations, const int64_t *tenures,
+                              int64_t *best, int64_t *best_cost, int64_t *cur, int64_t *cur_cost, int64_t *cells,
+                              int64_t *stopped_early, int64_t *steps_done, int64_t *trail_i, int64_t *trail_j,
+                              int64_t *trail_delta, int64_t *trail_tabu)
+{
+    int rc = check_common(h, batch);
+    if (rc) return rc;
+    if (iterations < 1) return fail(QAPB_ERR_INVALID, "iterations must be >= 1, got " + std::to_string(iterations));
+    if (!perms || !tenures || !best || !best_cost || !cur || !cur_cost) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    const bool tr = trail_i && trail_j && trail_delta && trail_tabu;
+    const int n = h->n;
+    const size_t pb = (size_t)batch * n * 8, sb = (size_t)batch * 8, tb = (size_t)batch * iterations * 8;
+    const size_t cb = (size_t)batch * n * n * 8;
+    DevBuf dp, dten, dbest, dbc, dcur, dcc, dcells, dstop, dsteps, dti, dtj, dtd, dtt;
+    CU(dp.alloc(pb)); CU(dten.alloc(tb)); CU(dbest.alloc(pb)); CU(dbc.alloc(sb)); CU(dcur.alloc(pb)); CU(dcc.alloc(sb));
+    CU(dstop.alloc(sb)); CU(dsteps.alloc(sb));
+    if (cells) CU(dcells.alloc(cb));
+    if (tr) { CU(dti.alloc(tb)); CU(dtj.alloc(tb)); CU(dtd.alloc(tb)); CU(dtt.alloc(tb)); }
+    H2D(dp.p, perms, pb);
+    H2D(dten.p, tenures, tb);
+    rc = qapb_tabu(h, dp.as<int64_t>(), batch, iterations, dten.as<int64_t>(), dbest.as<int64_t>(), dbc.as<int64_t>(),
+                   dcur.as<int64_t>(), dcc.as<int64_t>(), cells ? dcells.as<int64_t>() : nullptr, dstop.as<int64_t>(),
+                   dsteps.as<int64_t>(), tr ? dti.as<int64_t>() : nullptr, tr ? dtj.as<int64_t>() : nullptr,
+                   tr ? dtd.as<int64_t>() : nullptr, tr ? dtt.as<int64_t>() : nullptr, nullptr);
+    if (rc) return rc;
+    D2H(best, dbest.p, pb); D2H(best_cost, dbc.p, sb); D2H(cur, dcur.p, pb); D2H(cur_cost, dcc.p, sb);
+    if (cells) D2H(cells, dcells.p, cb);
+    if (stopped_early) D2H(stopped_early, dstop.p, sb);
+    if (steps_done) D2H(steps_done, dsteps.p, sb);
+    if (tr) { D2H(trail_i, dti.p, tb); D2H(trail_j, dtj.p, tb); D2H(trail_delta, dtd.p, tb); D2H(trail_tabu, dtt.p, tb); }
+    return QAPB_OK;
+}
+
+extern "C" int qapb_multistart_host(qapb_handle *h, int algo, uint64_t master_seed, uint64_t first_index, int count,
+                                    int iterations, int64_t ten_low, int64_t ten_high, int64_t *per_start_costs,
+                                    int64_t *best_key, int64_t *best_perm)
+{
+    int rc = check_common(h, count);
+    if (rc) return rc;
+    if (!per_start_costs || !best_key || !best_perm) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    DevBuf dc, dk, dp;
+    CU(dc.alloc((size_t)count * 8)); CU(dk.alloc(16)); CU(dp.alloc((size_t)h->n * 8));
+    rc = qapb_multistart(h, algo, master_seed, first_index, count, iterations, ten_low, ten_high, dc.as<int64_t>(),
+                         dk.as<int64_t>(), dp.as<int64_t>(), nullptr);
+    if (rc) return rc;
+    D2H(per_start_costs, dc.p, (size_t)count * 8);
+    D2H(best_key, dk.p, 16);
+    D2H(best_perm, dp.p, (size_t)h->n * 8);
+    return QAPB_OK;
+}
+
+extern "C" int qapb_probe_int_peak(int device, int kind, double *ops_per_sec)
+{
+    if (!ops_per_sec || kind < 0 || kind > 2) return fail(QAPB_ERR_INVALID, "bad argument");
+    CU(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    DevBuf sink;
+    CU(sink.alloc(4));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    const int iters = 20000, threads = 1024, blocks = prop.multiProcessorCount * 2;
+    auto launch = [&](int it) {
+        if (kind == 0) qap_int_probe_kernel<0><<<blocks, threads>>>(it, sink.as<int>(), 3);
+        else if (kind == 1) qap_int_probe_kernel<1><<<blocks, threads>>>(it, sink.as<int>(), 3);
+        else qap_int_probe_kernel<2><<<blocks, threads>>>(it, sink.as<int>(), 3);
+    };
+    launch(200);
+    CU(cudaDeviceSynchronize());
+    CU(cudaEventRecord(e0));
+    launch(iters);
+    CU(cudaEventRecord(e1));
+    CU(cudaEventSynchronize(e1));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double per_thread = (double)iters * 8.0 * (kind == 2 ? 8.0 : 4.0);
+    *ops_per_sec = per_thread * threads * blocks / (ms * 1e-3);
+    return QAPB_OK;
+}

@@ -1,0 +1,757 @@
+// search_kernel.cuh -- device code of the QAP swap-delta hot path for sm_100a.
+//
+// One CTA owns one search (one start).  The per-search state is the *placement
+// matrix* M and the vector h:
+//
+//   S[a][b] = sum_k ( D0[a][k]*F0[p_b][p_k] + D0[k][a]*F0[p_k][p_b] )     (cost of unit p_b at location a)
+//   M[i][j] = S[i][j] + D0[i][j]*(F0[p_i][p_j] + F0[p_j][p_i]) + dd[i]*fd[p_j]     (i != j)
+//   h[i]    = S[i][i] + dd[i]*fd[p_i]
+//
+// (F0/D0 = flow/distance with zeroed diagonals, fd/dd = their diagonals), for which
+//
+//   delta(i,j) = M[i][j] + M[j][i] - h[i] - h[j]
+//
+// reproduces the reference's O(n) exchange delta (_kernels.pyx:27-41) exactly,
+// including the direct and diagonal terms, in integer arithmetic.  After a swap
+// of locations r < s every entry of M outside rows/columns r,s receives the
+// rank-2 correction  M[i][j] -= a[i]*b[j] + c[i]*e[j]  (a,c: column/row
+// differences of D0; b,e: column/row differences of F0 gathered through p), and
+// the 4n entries on rows/columns r,s have closed-form O(1) updates, so one
+// iteration costs O(n^2) instead of the reference's O(n^3) re-evaluation
+// (_kernels.pyx:159-161) while producing the same integers.
+//
+// M is tiled in 4x4 blocks; a *unit* is the block pair {(I,J),(J,I)}, I<J (or one
+// diagonal block).  A thread owns whole units, so both M[i][j] and M[j][i] of a
+// pair are thread-local and the update, the delta, the tabu/aspiration test
+// (_kernels.pyx:162) and the running argmin are fused into one pass with
+// 128-bit, bank-conflict-free shared-memory accesses ("spill layout":
+// element (row w, thread t) of unit slot k lives at ((k*8+w)*T + t)*16 bytes).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qapb {
+
+enum { MODE_ALL_DELTAS = 0, MODE_TWO_OPT = 1, MODE_TABU = 2 };
+
+struct SearchParams {
+    int n, nb, npad, nunits, noff, upt;
+    int mode;        // MODE_*
+    int rng;         // 1: derive start permutation + tenures on the device (multistart)
+    int iterations;
+    int symmetric;
+    int force_seq_rng;  // test hook: take the sequential (rejection-exact) RNG path
+    const int32_t *F, *FT, *D, *DT;  // [npad*npad], zero diagonal, zero padded
+    const int32_t *fd, *dd;          // [npad] diagonals
+    const uint16_t *unit_ij;         // [nunits]  I | J<<8
+    const int64_t *perms;            // [B,n]            (rng == 0)
+    const int64_t *tenures;          // [B,iterations]   (tabu, rng == 0)
+    unsigned long long master_seed, first_index;
+    long long ten_lo, ten_hi;
+    int64_t *out_deltas;             // [B, n(n-1)/2]    (MODE_ALL_DELTAS)
+    int64_t *best, *best_cost, *cur, *cur_cost;
+    int64_t *cells;                  // [B,n,n] or null
+    int64_t *stopped, *steps;        // [B] or null
+    int64_t *tr_i, *tr_j, *tr_d, *tr_tabu;  // [B,iterations] or null
+    void *gM;                        // global placement matrices (storage >= 1)
+    void *gT;                        // global tabu triangles    (storage == 2)
+    unsigned long long gM_stride, gT_stride;  // elements per start
+};
+
+// ---- shared-memory layout, shared by host (size) and device (offsets) ------
+struct SmemLayout {
+    unsigned offM, offT, offA, offC, offB, offE, offH, offP, offU, offRedD, offRedK, offJ, offMisc;
+    unsigned total;
+};
+
+__host__ __device__ inline unsigned align16(unsigned x) { return (x + 15u) & ~15u; }
+
+__host__ __device__ inline SmemLayout make_layout(int npad, int nunits, int T, int upt,
+                                                  int acc_bytes, int storage)
+{
+    SmemLayout L;
+    unsigned o = 0;
+    L.offM = o;
+    if (storage == 0) o += (unsigned)upt * 8u * (unsigned)T * 4u * (unsigned)acc_bytes;
+    o = align16(o);
+    L.offT = o;
+    if (storage <= 1) o += (unsigned)upt * 4u * (unsigned)T * 16u;
+    o = align16(o);
+    L.offA = o; o += 4u * npad;
+    L.offC = o; o += 4u * npad;
+    L.offB = o; o += 4u * npad;
+    L.offE = o; o += 4u * npad;
+    L.offH = o; o += (unsigned)acc_bytes * npad;
+    o = align16(o);
+    L.offP = o; o += 4u * npad;
+    L.offJ = o; o += 4u * npad;
+    L.offU = o; o += align16(2u * nunits);
+    L.offRedD = o; o += 32u * 8u;
+    L.offRedK = o; o += 32u * 4u;
+    L.offMisc = o; o += 64u;
+    L.total = align16(o);
+    return L;
+}
+
+// ---- accumulator traits -----------------------------------------------------
+template <typename acc_t> struct Acc;
+template <> struct Acc<int32_t> {
+    static __device__ __forceinline__ int32_t maxv() { return 0x7fffffff; }
+    static __device__ __forceinline__ int32_t bighalf() { return 1 << 29; }
+    static __device__ __forceinline__ int32_t clamp_thr(long long v)
+    {
+        return v < -2147483647LL ? (int32_t)0x80000000 : (int32_t)v;  // v <= 0 always
+    }
+};
+template <> struct Acc<int64_t> {
+    static __device__ __forceinline__ int64_t maxv() { return 0x7fffffffffffffffLL; }
+    static __device__ __forceinline__ int64_t bighalf() { return 1LL << 61; }
+    static __device__ __forceinline__ int64_t clamp_thr(long long v) { return v; }
+};
+
+// Row of four accumulators in the spill layout.
+__device__ __forceinline__ void ld_row(const int32_t *base, int row, int T, int t, int32_t (&v)[4])
+{
+    int4 q = reinterpret_cast<const int4 *>(base)[row * T + t];
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+}
+__device__ __forceinline__ void st_row(int32_t *base, int row, int T, int t, const int32_t (&v)[4])
+{
+    reinterpret_cast<int4 *>(base)[row * T + t] = make_int4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void ld_row(const int64_t *base, int row, int T, int t, int64_t (&v)[4])
+{
+    const longlong2 *b2 = reinterpret_cast<const longlong2 *>(base);
+    longlong2 q0 = b2[(row * 2) * T + t], q1 = b2[(row * 2 + 1) * T + t];
+    v[0] = q0.x; v[1] = q0.y; v[2] = q1.x; v[3] = q1.y;
+}
+__device__ __forceinline__ void st_row(int64_t *base, int row, int T, int t, const int64_t (&v)[4])
+{
+    longlong2 *b2 = reinterpret_cast<longlong2 *>(base);
+    b2[(row * 2) * T + t] = make_longlong2(v[0], v[1]);
+    b2[(row * 2 + 1) * T + t] = make_longlong2(v[2], v[3]);
+}
+__device__ __forceinline__ int32_t *elem_ptr(int32_t *base, int row, int T, int t, int lane4)
+{
+    return base + ((size_t)(row * T + t) * 4 + lane4);
+}
+__device__ __forceinline__ int64_t *elem_ptr(int64_t *base, int row, int T, int t, int lane4)
+{
+    return base + ((size_t)((row * 2 + (lane4 >> 1)) * T + t) * 2 + (lane4 & 1));
+}
+
+__device__ __forceinline__ void ld_vec4(const int32_t *arr, int blk, int32_t (&v)[4])
+{
+    int4 q = reinterpret_cast<const int4 *>(arr)[blk];
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+}
+__device__ __forceinline__ void ld_h4(const int32_t *arr, int blk, int32_t (&v)[4]) { ld_vec4(arr, blk, v); }
+__device__ __forceinline__ void ld_h4(const int64_t *arr, int blk, int64_t (&v)[4])
+{
+    const longlong2 *b2 = reinterpret_cast<const longlong2 *>(arr);
+    longlong2 q0 = b2[blk * 2], q1 = b2[blk * 2 + 1];
+    v[0] = q0.x; v[1] = q0.y; v[2] = q1.x; v[3] = q1.y;
+}
+
+// ---- SplitMix64 on the device (rng.py:12-20,35-47,62-70) ---------------------
+#define QAPB_GAMMA 0x9E3779B97F4A7C15ULL
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z)
+{
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+// randbelow with the exact rejection rule: accept r iff r <= 2^64-1 - (2^64 mod bound).
+__device__ inline unsigned long long randbelow_seq(unsigned long long &state, unsigned long long bound)
+{
+    unsigned long long rem = (0ULL - bound) % bound;
+    unsigned long long last_ok = ~0ULL - rem;
+    for (;;) {
+        state += QAPB_GAMMA;
+        unsigned long long r = mix64(state);
+        if (r <= last_ok) return r % bound;
+    }
+}
+
+// ---- warp / block reductions ------------------------------------------------
+// Lexicographic minimum of (value, key) over a warp; all lanes get the result.
+__device__ __forceinline__ void warp_argmin(int32_t &d, unsigned &key)
+{
+    int32_t m = __reduce_min_sync(0xffffffffu, d);
+    unsigned k = __reduce_min_sync(0xffffffffu, d == m ? key : 0xffffffffu);
+    d = m;
+    key = k;
+}
+__device__ __forceinline__ void warp_argmin(int64_t &d, unsigned &key)
+{
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        int64_t od = __shfl_xor_sync(0xffffffffu, d, off);
+        unsigned ok = __shfl_xor_sync(0xffffffffu, key, off);
+        if (od < d || (od == d && ok < key)) {
+            d = od;
+            key = ok;
+        }
+    }
+}
+
+__device__ __forceinline__ long long block_sum_i64(long long v, long long *scratch /* >= 33 */, int tid, int T)
+{
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    __syncthreads();
+    if ((tid & 31) == 0) scratch[tid >> 5] = v;
+    __syncthreads();
+    if (tid < 32) {
+        long long s = tid < (T >> 5) ? scratch[tid] : 0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (tid == 0) scratch[32] = s;
+    }
+    __syncthreads();
+    return scratch[32];
+}
+
+__device__ __forceinline__ unsigned pair_key(int i, int j, int flag)
+{
+    return ((unsigned)i << 17) | ((unsigned)j << 1) | (unsigned)flag;
+}
+
+// Locate element M[x][y] (x != y) in the spill layout: returns row index
+// (k*8 + w) and owning thread / lane.
+struct ElemLoc { int row, t, lane4; };
+__device__ __forceinline__ ElemLoc locate(int x, int y, int nb, int noff, int T)
+{
+    int X = x >> 2, Y = y >> 2, uid, w, l;
+    if (X < Y) {
+        uid = X * nb - ((X * (X + 1)) >> 1) + (Y - X - 1);
+        w = x & 3; l = y & 3;
+    } else if (X > Y) {
+        uid = Y * nb - ((Y * (Y + 1)) >> 1) + (X - Y - 1);
+        w = 4 + (x & 3); l = y & 3;
+    } else {
+        uid = noff + X;
+        w = x & 3; l = y & 3;
+    }
+    int k = uid / T;
+    ElemLoc e;
+    e.t = uid - k * T;
+    e.row = k * 8 + w;
+    e.lane4 = l;
+    return e;
+}
+
+// -----------------------------------------------------------------------------
+// The search kernel.  STORAGE: 0 = M and tabu triangle in shared memory,
+// 1 = M in global (L2-resident), tabu in shared, 2 = both in global.
+// -----------------------------------------------------------------------------
+template <typename acc_t, int STORAGE, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
+    const int b = blockIdx.x;
+    const int n = P.n, nb = P.nb, npad = P.npad, noff = P.noff, nunits = P.nunits, upt = P.upt;
+    const SmemLayout lay = make_layout(npad, nunits, T, upt, (int)sizeof(acc_t), STORAGE);
+
+    acc_t *M = STORAGE == 0 ? reinterpret_cast<acc_t *>(smem_raw + lay.offM)
+                            : reinterpret_cast<acc_t *>(P.gM) + (size_t)b * P.gM_stride;
+    int32_t *Tb = STORAGE <= 1 ? reinterpret_cast<int32_t *>(smem_raw + lay.offT)
+                               : reinterpret_cast<int32_t *>(P.gT) + (size_t)b * P.gT_stride;
+    int32_t *sA = reinterpret_cast<int32_t *>(smem_raw + lay.offA);
+    int32_t *sC = reinterpret_cast<int32_t *>(smem_raw + lay.offC);
+    int32_t *sB = reinterpret_cast<int32_t *>(smem_raw + lay.offB);
+    int32_t *sE = reinterpret_cast<int32_t *>(smem_raw + lay.offE);
+    acc_t *sH = reinterpret_cast<acc_t *>(smem_raw + lay.offH);
+    int32_t *sP = reinterpret_cast<int32_t *>(smem_raw + lay.offP);
+    unsigned *sJ = reinterpret_cast<unsigned *>(smem_raw + lay.offJ);
+    uint16_t *sU = reinterpret_cast<uint16_t *>(smem_raw + lay.offU);
+    long long *sRed64 = reinterpret_cast<long long *>(smem_raw + lay.offRedD);  // 32 x 8 B
+    acc_t *sRedD = reinterpret_cast<acc_t *>(smem_raw + lay.offRedD);
+    unsigned *sRedK = reinterpret_cast<unsigned *>(smem_raw + lay.offRedK);
+    long long *sMisc = reinterpret_cast<long long *>(smem_raw + lay.offMisc);  // [0..1] tenure ring, [2] flags
+
+    const int32_t *__restrict__ F = P.F;
+    const int32_t *__restrict__ FT = P.FT;
+    const int32_t *__restrict__ D = P.D;
+    const int32_t *__restrict__ DT = P.DT;
+    const bool sym = P.symmetric != 0;
+    const acc_t MAXV = Acc<acc_t>::maxv();
+
+    // ---------------------------------------------------------------- setup
+    for (int u = tid; u < nunits; u += T) sU[u] = P.unit_ij[u];
+    for (int i = tid; i < npad; i += T) {
+        sA[i] = 0; sC[i] = 0; sB[i] = 0; sE[i] = 0;
+        sH[i] = 0;
+        sP[i] = (P.rng || i >= n) ? (i < n ? i : 0) : (int32_t)P.perms[(size_t)b * n + i];
+    }
+    unsigned long long rng_state = 0;  // meaningful in thread 0 only
+    if (P.rng) {
+        // multistart.py:88: state = derive_seed(master, index); core.py:81-87 shuffle.
+        const unsigned long long seed = mix64(P.master_seed + QAPB_GAMMA * (P.first_index + (unsigned long long)b + 1ULL));
+        // Draw k (0-based) serves i = n-1-k with bound i+1.  Draws are computed in
+        // parallel assuming no rejection; any rejection (probability ~ n^2/2^64)
+        // falls back to the exact sequential loop.
+        int reject = P.force_seq_rng;
+        for (int k = tid; k < n - 1; k += T) {
+            unsigned long long bound = (unsigned long long)(n - 1 - k) + 1ULL;
+            unsigned long long r = mix64(seed + QAPB_GAMMA * ((unsigned long long)k + 1ULL));
+            unsigned long long rem = (0ULL - bound) % bound;
+            if (r > ~0ULL - rem) reject = 1;
+            sJ[n - 1 - k] = (unsigned)(r % bound);
+        }
+        reject = __syncthreads_or(reject);
+        if (tid == 0) {
+            rng_state = seed;
+            if (reject) {
+                for (int i = n - 1; i >= 1; --i) {
+                    unsigned j = (unsigned)randbelow_seq(rng_state, (unsigned long long)i + 1ULL);
+                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
+                }
+            } else {
+                for (int i = n - 1; i >= 1; --i) {
+                    unsigned j = sJ[i];
+                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
+                }
+                rng_state = seed + QAPB_GAMMA * (unsigned long long)(n - 1);
+            }
+            if (P.mode == MODE_TABU)  // tabu.py:184-186: tenure for iteration 1
+                sMisc[1] = P.ten_lo + (long long)randbelow_seq(rng_state, (unsigned long long)(P.ten_hi - P.ten_lo + 1));
+        }
+    }
+    if (P.cells) {
+        int64_t *cz = P.cells + (size_t)b * n * n;
+        for (int i = tid; i < n * n; i += T) cz[i] = 0;
+    }
+    __syncthreads();
+
+    // full cost (_kernels.pyx:18-24), int64, including the diagonal products.
+    long long cost;
+    {
+        long long part = 0;
+        for (int idx = tid; idx < n * n; idx += T) {
+            int i = idx / n, j = idx - i * n;
+            int pi = sP[i], pj = sP[j];
+            part += (i == j) ? (long long)P.fd[pi] * P.dd[i]
+                             : (long long)F[pi * npad + pj] * D[i * npad + j];
+        }
+        cost = block_sum_i64(part, sRed64, tid, T);
+        __syncthreads();
+    }
+
+    // h[i]
+    for (int i = tid; i < n; i += T) {
+        int pi = sP[i];
+        acc_t acc = (acc_t)P.dd[i] * (acc_t)P.fd[pi];
+        if (sym) {
+            for (int k = 0; k < n; ++k) acc += (acc_t)2 * ((acc_t)D[i * npad + k] * (acc_t)F[pi * npad + sP[k]]);
+        } else {
+            for (int k = 0; k < n; ++k) {
+                int pk = sP[k];
+                acc += (acc_t)D[i * npad + k] * (acc_t)F[pi * npad + pk] + (acc_t)DT[i * npad + k] * (acc_t)FT[pi * npad + pk];
+            }
+        }
+        sH[i] = acc;
+    }
+    __syncthreads();
+
+    // M (and tabu triangle) per unit
+    for (int k = 0; k < upt; ++k) {
+        const int uid = tid + k * T;
+        if (uid >= nunits) break;
+        const int I = sU[uid] & 0xff, J = sU[uid] >> 8;
+        int pI[4], pJ[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { pI[u] = sP[4 * I + u]; pJ[u] = sP[4 * J + u]; }
+        acc_t U[4][4], L[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) { U[u][v] = 0; L[u][v] = 0; }
+        for (int kk = 0; kk < n; ++kk) {
+            const int pk = sP[kk];
+            int32_t dI[4], dJ[4], fI[4], fJ[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                dI[u] = D[(4 * I + u) * npad + kk];
+                dJ[u] = D[(4 * J + u) * npad + kk];
+                fI[u] = F[pI[u] * npad + pk];
+                fJ[u] = F[pJ[u] * npad + pk];
+            }
+            if (sym) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        U[u][v] += (acc_t)dI[u] * (acc_t)fJ[v];
+                        L[v][u] += (acc_t)dJ[v] * (acc_t)fI[u];
+                    }
+            } else {
+                int32_t dtI[4], dtJ[4], ftI[4], ftJ[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    dtI[u] = DT[(4 * I + u) * npad + kk];
+                    dtJ[u] = DT[(4 * J + u) * npad + kk];
+                    ftI[u] = FT[pI[u] * npad + pk];
+                    ftJ[u] = FT[pJ[u] * npad + pk];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        U[u][v] += (acc_t)dI[u] * (acc_t)fJ[v] + (acc_t)dtI[u] * (acc_t)ftJ[v];
+                        L[v][u] += (acc_t)dJ[v] * (acc_t)fI[u] + (acc_t)dtJ[v] * (acc_t)ftI[u];
+                    }
+            }
+        }
+        int32_t Ex[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int i = 4 * I + u, j = 4 * J + v;
+                if (sym) { U[u][v] *= 2; L[v][u] *= 2; }
+                const acc_t fs = (acc_t)F[pI[u] * npad + pJ[v]] + (acc_t)F[pJ[v] * npad + pI[u]];
+                U[u][v] += (acc_t)D[i * npad + j] * fs + (acc_t)P.dd[i] * (acc_t)P.fd[pJ[v]];
+                L[v][u] += (acc_t)D[j * npad + i] * fs + (acc_t)P.dd[j] * (acc_t)P.fd[pI[u]];
+                const bool pad = (i >= n) || (j >= n);
+                if (pad) { U[u][v] = Acc<acc_t>::bighalf(); L[v][u] = Acc<acc_t>::bighalf(); }
+                if (i == j) { U[u][v] = 0; L[v][u] = 0; }
+                Ex[u][v] = pad ? 0x7fffffff : 0;
+            }
+        if (P.mode == MODE_ALL_DELTAS) {
+            acc_t hI[4], hJ[4];
+            ld_h4(sH, I, hI);
+            ld_h4(sH, J, hJ);
+            int64_t *out = P.out_deltas + (size_t)b * ((size_t)n * (n - 1) / 2);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int i = 4 * I + u, j = 4 * J + v;
+                    if (i < j && j < n) {
+                        const acc_t d = (I == J) ? U[u][v] + U[v][u] - hI[u] - hI[v]
+                                                 : U[u][v] + L[v][u] - hI[u] - hJ[v];
+                        out[(size_t)i * n - ((size_t)i * (i + 1)) / 2 + (j - i - 1)] = (int64_t)d;
+                    }
+                }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                st_row(M, k * 8 + u, T, tid, U[u]);
+                st_row(M, k * 8 + 4 + u, T, tid, L[u]);
+                reinterpret_cast<int4 *>(Tb)[(k * 4 + u) * T + tid] = make_int4(Ex[u][0], Ex[u][1], Ex[u][2], Ex[u][3]);
+            }
+        }
+    }
+    if (P.mode == MODE_ALL_DELTAS) return;
+    __syncthreads();
+
+    // ------------------------------------------------------------ iterations
+    long long best_cost = cost;
+    acc_t thr = 0;  // best_cost - cost, clamped; aspiration <=> d < thr  (_kernels.pyx:162)
+    const bool tabu = P.mode == MODE_TABU;
+    const int iters = P.iterations;
+    int steps_done = 0, stopped = 0;
+    int64_t *best_out = P.best + (size_t)b * n;
+    for (int i = tid; i < n; i += T) best_out[i] = sP[i];
+
+    for (int c = 1; c <= iters; ++c) {
+        long long ten = 0;
+        if (tabu && !P.rng) ten = P.tenures[(size_t)b * iters + (c - 1)];  // consumed after the pass
+
+        // ---- fused pass: rank-2 update, delta, admissibility, running argmin
+        acc_t bd = MAXV;
+        unsigned bkey = 0xffffffffu;
+        for (int k = 0; k < upt; ++k) {
+            const int uid = tid + k * T;
+            if (uid >= nunits) break;
+            const int I = sU[uid] & 0xff, J = sU[uid] >> 8;
+            acc_t cand[16];
+            acc_t m = MAXV;
+            if (I != J) {
+                acc_t U[4][4], L[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    ld_row(M, k * 8 + u, T, tid, U[u]);
+                    ld_row(M, k * 8 + 4 + u, T, tid, L[u]);
+                }
+                if (c > 1) {
+                    int32_t aI[4], bI[4], aJ[4], bJ[4];
+                    ld_vec4(sA, I, aI); ld_vec4(sB, I, bI); ld_vec4(sA, J, aJ); ld_vec4(sB, J, bJ);
+                    if (sym) {  // a pre-doubled: a == c, b == e
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                U[u][v] -= (acc_t)aI[u] * (acc_t)bJ[v];
+                                L[v][u] -= (acc_t)aJ[v] * (acc_t)bI[u];
+                            }
+                    } else {
+                        int32_t cI[4], eI[4], cJ[4], eJ[4];
+                        ld_vec4(sC, I, cI); ld_vec4(sE, I, eI); ld_vec4(sC, J, cJ); ld_vec4(sE, J, eJ);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                U[u][v] -= (acc_t)aI[u] * (acc_t)bJ[v] + (acc_t)cI[u] * (acc_t)eJ[v];
+                                L[v][u] -= (acc_t)aJ[v] * (acc_t)bI[u] + (acc_t)cJ[v] * (acc_t)eI[u];
+                            }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        st_row(M, k * 8 + u, T, tid, U[u]);
+                        st_row(M, k * 8 + 4 + u, T, tid, L[u]);
+                    }
+                }
+                acc_t hI[4], hJ[4];
+                ld_h4(sH, I, hI);
+                ld_h4(sH, J, hJ);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    int32_t ex[4];
+                    ld_vec4(Tb, (k * 4 + u) * T + tid, ex);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const acc_t d = U[u][v] + L[v][u] - hI[u] - hJ[v];
+                        const bool adm = (ex[v] <= c) || (d < thr);
+                        const acc_t cd = adm ? d : MAXV;
+                        cand[u * 4 + v] = cd;
+                        m = cd < m ? cd : m;
+                    }
+                }
+            } else {
+                acc_t U[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) ld_row(M, k * 8 + u, T, tid, U[u]);
+                if (c > 1) {
+                    int32_t aI[4], bI[4], cI[4], eI[4];
+                    ld_vec4(sA, I, aI); ld_vec4(sB, I, bI); ld_vec4(sC, I, cI); ld_vec4(sE, I, eI);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v)
+                            if (u != v)
+                                U[u][v] -= sym ? (acc_t)aI[u] * (acc_t)bI[v]
+                                               : (acc_t)aI[u] * (acc_t)bI[v] + (acc_t)cI[u] * (acc_t)eI[v];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) st_row(M, k * 8 + u, T, tid, U[u]);
+                }
+                acc_t hI[4];
+                ld_h4(sH, I, hI);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    int32_t ex[4];
+                    ld_vec4(Tb, (k * 4 + u) * T + tid, ex);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        acc_t cd = MAXV;
+                        if (u < v) {
+                            const acc_t d = U[u][v] + U[v][u] - hI[u] - hI[v];
+                            const bool adm = (ex[v] <= c) || (d < thr);
+                            cd = adm ? d : MAXV;
+                        }
+                        cand[u * 4 + v] = cd;
+                        m = cd < m ? cd : m;
+                    }
+                }
+            }
+            if (m != MAXV && m <= bd) {
+                int slot = 15;
+#pragma unroll
+                for (int q = 14; q >= 0; --q) slot = (cand[q] == m) ? q : slot;
+                const int u = slot >> 2, v = slot & 3;
+                const int32_t ex = Tb[((size_t)((k * 4 + u) * T + tid)) * 4 + v];
+                const unsigned key = pair_key(4 * I + u, 4 * J + v, ex > c ? 1 : 0);
+                if (m < bd || key < bkey) { bd = m; bkey = key; }
+            }
+        }
+        warp_argmin(bd, bkey);
+        if (lane == 0) { sRedD[warp] = bd; sRedK[warp] = bkey; }
+        __syncthreads();  // ---------------------------------------------- sync #1
+        bd = lane < W ? sRedD[lane] : MAXV;
+        bkey = lane < W ? sRedK[lane] : 0xffffffffu;
+        warp_argmin(bd, bkey);
+        if (bd == MAXV) {  // no admissible move: premature stop (_kernels.pyx:168-170)
+            stopped = 1;
+            break;
+        }
+        const int r = (int)(bkey >> 17), s = (int)((bkey >> 1) & 0xffffu);
+        const int was_tabu = (int)(bkey & 1u);
+        cost += (long long)bd;
+        const bool improved = cost < best_cost;
+        if (improved) best_cost = cost;
+        thr = Acc<acc_t>::clamp_thr(best_cost - cost);
+        if (tabu && P.rng) ten = sMisc[c & 1];
+        steps_done = c;
+
+        if (tid == 0) {
+            if (P.tr_i) {
+                const size_t o = (size_t)b * iters + (c - 1);
+                P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
+                if (P.tr_tabu) P.tr_tabu[o] = was_tabu;
+            }
+            if (tabu && P.rng && c < iters)  // tenure of iteration c+1 (tabu.py:184-186)
+                sMisc[(c + 1) & 1] = P.ten_lo + (long long)randbelow_seq(rng_state, (unsigned long long)(P.ten_hi - P.ten_lo + 1));
+        }
+
+        // ---- prep: difference vectors (old permutation), h, rows/columns r,s
+        {
+            const int pr = sP[r], ps = sP[s];
+            const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
+            const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
+            for (int i = tid; i < n; i += T) {
+                const int pi = sP[i];
+                const int32_t Dsi = D[s * npad + i], Dri = D[r * npad + i];
+                const int32_t Dis = DT[s * npad + i], Dir = DT[r * npad + i];
+                const int32_t Fpips = FT[ps * npad + pi], Fpipr = FT[pr * npad + pi];
+                const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
+                int32_t a = Dis - Dir, cc = Dsi - Dri, bb = Fpips - Fpipr, e = Fpspi - Fprpi;
+                if (improved) best_out[i] = (i == r) ? ps : (i == s) ? pr : pi;
+                if (i == r) {
+                    // corners and h[r], h[s]
+                    ElemLoc lrs = locate(r, s, nb, noff, T), lsr = locate(s, r, nb, noff, T);
+                    acc_t *prs = elem_ptr(M, lrs.row, T, lrs.t, lrs.lane4);
+                    acc_t *psr = elem_ptr(M, lsr.row, T, lsr.t, lsr.lane4);
+                    const acc_t mrs = *prs, msr = *psr, hr = sH[r], hs = sH[s];
+                    *prs = hr + (acc_t)(Drs - Dsr) * (acc_t)Fpspr;
+                    *psr = hs + (acc_t)(Dsr - Drs) * (acc_t)Fprps;
+                    sH[r] = mrs + (acc_t)(Dsr - Drs) * (acc_t)Fprps;
+                    sH[s] = msr + (acc_t)(Drs - Dsr) * (acc_t)Fpspr;
+                    a = 0; cc = 0; bb = 0; e = 0;
+                } else if (i == s) {
+                    if (tabu) {  // cells[bi][bj] = c + t; cells[bj][bi] += 1  (_kernels.pyx:176-178)
+                        const int R = r >> 2, S = s >> 2;
+                        const int uid = (R < S) ? R * nb - ((R * (R + 1)) >> 1) + (S - R - 1) : noff + R;
+                        const int kq = uid / T, tq = uid - kq * T;
+                        Tb[((size_t)((kq * 4 + (r & 3)) * T + tq)) * 4 + (s & 3)] = (int32_t)(c + ten);
+                        if (P.cells) {
+                            int64_t *cz = P.cells + (size_t)b * n * n;
+                            cz[(size_t)r * n + s] = (int64_t)c + ten;
+                            cz[(size_t)s * n + r] += 1;
+                        }
+                    }
+                    a = 0; cc = 0; bb = 0; e = 0;
+                } else {
+                    ElemLoc lri = locate(r, i, nb, noff, T), lsi = locate(s, i, nb, noff, T);
+                    ElemLoc lir = locate(i, r, nb, noff, T), lis = locate(i, s, nb, noff, T);
+                    acc_t *pri = elem_ptr(M, lri.row, T, lri.t, lri.lane4);
+                    acc_t *psi = elem_ptr(M, lsi.row, T, lsi.t, lsi.lane4);
+                    acc_t *pir = elem_ptr(M, lir.row, T, lir.t, lir.lane4);
+                    acc_t *pis = elem_ptr(M, lis.row, T, lis.t, lis.lane4);
+                    const acc_t mri = *pri, msi = *psi, mir = *pir, mis = *pis;
+                    const acc_t be = (acc_t)bb + (acc_t)e;
+                    const acc_t fs_ps = (acc_t)Fpips + (acc_t)Fpspi;  // Fs[p_i][p_s]
+                    const acc_t fs_pr = (acc_t)Fpipr + (acc_t)Fprpi;  // Fs[p_i][p_r]
+                    *pri = mri - (acc_t)Drs * (acc_t)bb - (acc_t)Dsr * (acc_t)e + (acc_t)Dri * be;
+                    *psi = msi + (acc_t)Dsr * (acc_t)bb + (acc_t)Drs * (acc_t)e - (acc_t)Dsi * be;
+                    *pir = mis + (acc_t)a * ((acc_t)Fpspr - fs_ps) + (acc_t)cc * (acc_t)Fprps;
+                    *pis = mir + (acc_t)a * (fs_pr - (acc_t)Fprps) - (acc_t)cc * (acc_t)Fpspr;
+                    sH[i] -= (acc_t)a * (acc_t)bb + (acc_t)cc * (acc_t)e;
+                }
+                sA[i] = sym ? 2 * a : a;
+                sC[i] = cc; sB[i] = bb; sE[i] = e;
+            }
+        }
+        __syncthreads();  // ---------------------------------------------- sync #2
+        if (tid == 0) { const int32_t t = sP[r]; sP[r] = sP[s]; sP[s] = t; }
+    }
+    __syncthreads();
+
+    for (int i = tid; i < n; i += T) P.cur[(size_t)b * n + i] = sP[i];
+    if (tid == 0) {
+        P.best_cost[b] = best_cost;
+        P.cur_cost[b] = cost;
+        if (P.stopped) P.stopped[b] = stopped;
+        if (P.steps) P.steps[b] = steps_done;
+    }
+}
+
+// ---- kernels.full_cost, batched (one CTA per permutation) -------------------
+__global__ void qap_full_cost_kernel(int n, int npad, const int32_t *__restrict__ F,
+                                     const int32_t *__restrict__ D, const int32_t *__restrict__ fd,
+                                     const int32_t *__restrict__ dd, const int64_t *__restrict__ perms,
+                                     int64_t *__restrict__ costs)
+{
+    __shared__ long long scratch[33];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int32_t *sP = reinterpret_cast<int32_t *>(smem_raw);
+    const int tid = threadIdx.x, T = blockDim.x, b = blockIdx.x;
+    for (int i = tid; i < n; i += T) sP[i] = (int32_t)perms[(size_t)b * n + i];
+    __syncthreads();
+    long long part = 0;
+    for (int idx = tid; idx < n * n; idx += T) {
+        int i = idx / n, j = idx - i * n;
+        int pi = sP[i], pj = sP[j];
+        part += (i == j) ? (long long)fd[pi] * dd[i] : (long long)F[pi * npad + pj] * D[i * npad + j];
+    }
+    long long total = block_sum_i64(part, scratch, tid, T);
+    if (tid == 0) costs[b] = total;
+}
+
+// ---- multistart reduce: min (cost, index), ties -> lowest index (multistart.py:156)
+__global__ void qap_pick_best_kernel(int count, int n, unsigned long long first_index,
+                                     const int64_t *__restrict__ costs,
+                                     const int64_t *__restrict__ best_perms /* [count,n] */,
+                                     int64_t *__restrict__ best_key, int64_t *__restrict__ best_perm)
+{
+    __shared__ long long sc[32];
+    __shared__ int si[32];
+    __shared__ int winner;
+    const int tid = threadIdx.x, T = blockDim.x;
+    long long bc = 0x7fffffffffffffffLL;
+    int bi = 0x7fffffff;
+    for (int k = tid; k < count; k += T) {
+        long long c = costs[k];
+        if (c < bc || (c == bc && k < bi)) { bc = c; bi = k; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        long long oc = __shfl_xor_sync(0xffffffffu, bc, off);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (oc < bc || (oc == bc && oi < bi)) { bc = oc; bi = oi; }
+    }
+    if ((tid & 31) == 0) { sc[tid >> 5] = bc; si[tid >> 5] = bi; }
+    __syncthreads();
+    if (tid < 32) {
+        bc = tid < (T >> 5) ? sc[tid] : 0x7fffffffffffffffLL;
+        bi = tid < (T >> 5) ? si[tid] : 0x7fffffff;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            long long oc = __shfl_xor_sync(0xffffffffu, bc, off);
+            int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (oc < bc || (oc == bc && oi < bi)) { bc = oc; bi = oi; }
+        }
+        if (tid == 0) {
+            winner = bi;
+            best_key[0] = bc;
+            best_key[1] = (int64_t)(first_index + (unsigned long long)bi);
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += T) best_perm[i] = best_perms[(size_t)winner * n + i];
+}
+
+// ---- integer-pipe peak probe -----------------------------------------------
+template <int KIND>
+__global__ void qap_int_probe_kernel(int iters, int *sink, int seed)
+{
+    int x0 = threadIdx.x + seed, x1 = x0 * 3 + 1, x2 = x0 * 5 + 2, x3 = x0 * 7 + 3;
+    int y0 = x0 ^ 11, y1 = x1 ^ 13, y2 = x2 ^ 17, y3 = x3 ^ 19;
+    const int m = seed | 1, a = seed + 7;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (KIND == 0 || KIND == 2) { x0 = x0 * m + a; x1 = x1 * m + a; x2 = x2 * m + a; x3 = x3 * m + a; }
+            if (KIND == 1 || KIND == 2) {
+                y0 = (y0 + a) + y1;
+                y1 = (y1 + a) + y2;
+                y2 = (y2 + a) + y3;
+                y3 = (y3 + a) + y0;
+            }
+        }
+    }
+    if ((x0 ^ x1 ^ x2 ^ x3 ^ y0 ^ y1 ^ y2 ^ y3) == 0x12345678) *sink = 1;
+}
+
+}  // namespace qapb

@@ -1,0 +1,246 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact.
+
+Modelled on the reference's backend-equivalence suite
+(/root/reference/pkg/tests/test_backends.py:24-71): every returned array of
+full_cost / all_deltas / two_opt_run / tabu_run is compared element for element,
+on the reference's own generator (`random_instance`) and on the QAPLIB-shaped
+synthetic instances of BASELINE.json.  Sizes are chosen so the oracle finishes in
+seconds; full-size runs are covered by size-independent properties in
+test_properties_gpu.py.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def q(built):
+    import paper_2307_11248_b200 as pkg
+
+    return pkg
+
+
+@pytest.fixture(scope="module")
+def orc(built):
+    import oracle
+
+    return oracle
+
+
+def _fuzz_instance(n, seed, symmetric=False, diag=True, lo=-40, hi=90):
+    rng = np.random.default_rng(seed)
+    f = rng.integers(lo, hi, (n, n)).astype(np.int64)
+    d = rng.integers(lo, hi, (n, n)).astype(np.int64)
+    if symmetric:
+        f, d = f + f.T, d + d.T
+    if not diag:
+        np.fill_diagonal(f, 0)
+        np.fill_diagonal(d, 0)
+    return f, d
+
+
+def _cases():
+    from paper_2307_11248_b200 import shapes
+
+    out = []
+    for n in (2, 3, 5, 12, 23, 30):
+        inst = shapes.rand(n, 1000 + n)
+        out.append((f"rand{n}", inst.flow, inst.distance))
+    for n in (4, 5, 12, 23, 30):
+        out.append((f"fuzz-asym-diag{n}",) + _fuzz_instance(n, n))
+        out.append((f"fuzz-sym-diag{n}",) + _fuzz_instance(n, 100 + n, symmetric=True))
+    for name in ("nug12", "tai30a", "sko49", "tai64c"):
+        inst = shapes.by_name(name)
+        out.append((name, inst.flow, inst.distance))
+    return out
+
+
+CASES = _cases()
+
+
+@pytest.mark.parametrize("name,flow,dist", CASES, ids=[c[0] for c in CASES])
+def test_kernels_match_oracle(q, orc, name, flow, dist):
+    n = flow.shape[0]
+    rng = orc.Rng(77 + n)
+    perm = rng.permutation(n)
+    lo, hi = orc.tenure_bounds(n)
+    iters = 60
+    ten = rng.tenures(lo, hi, iters)
+    k = q.kernels
+
+    assert k.full_cost(flow, dist, perm) == orc.full_cost(flow, dist, perm)
+    assert np.array_equal(k.all_deltas(flow, dist, perm), orc.all_deltas(flow, dist, perm))
+
+    got = k.two_opt_run(flow, dist, perm, iters)
+    want = orc.two_opt_run(flow, dist, perm, iters)
+    for idx, (g, w) in enumerate(zip(got, want)):
+        assert np.array_equal(g, w), f"two_opt_run output {idx}"
+
+    got = k.tabu_run(flow, dist, perm, iters, ten)
+    want = orc.tabu_run(flow, dist, perm, iters, ten)
+    for idx, (g, w) in enumerate(zip(got[:7], want[:7])):
+        assert np.array_equal(g, w), f"tabu_run output {idx}"
+    for idx, (g, w) in enumerate(zip(got[7], want[7])):
+        assert np.array_equal(g, w), f"tabu trail array {idx}"
+
+
+def test_inputs_not_mutated(q):
+    from paper_2307_11248_b200 import shapes
+
+    inst = shapes.rand(12, 5)
+    perm = np.arange(12, dtype=np.int64)[::-1].copy()
+    snap = perm.copy()
+    q.kernels.two_opt_run(inst.flow, inst.distance, perm, 10)
+    q.kernels.tabu_run(inst.flow, inst.distance, perm, 10, np.full(10, 2, np.int64))
+    assert np.array_equal(perm, snap)
+
+
+def test_toy2_known_answers(q):
+    """conftest.py:12-18 / test_core.py:31-33,55-56: costs 13 and 17, delta +4."""
+    inst = q.parse_instance("2\n0 3\n2 0\n0 1\n5 0", name="toy")
+    ident, swapped = np.array([0, 1], np.int64), np.array([1, 0], np.int64)
+    assert q.full_cost(inst, ident) == 13
+    assert q.full_cost(inst, swapped) == 17
+    assert q.all_deltas(inst, ident).tolist() == [4]
+
+
+def test_premature_stop(q, orc):
+    """test_tabu.py:96-105: on n=2 the only move becomes tabu and nothing aspirates."""
+    inst = q.parse_instance("2\n0 3\n2 0\n0 1\n5 0", name="toy")
+    perm = np.array([0, 1], np.int64)
+    ten = np.full(6, 3, np.int64)
+    got = q.kernels.tabu_run(inst.flow, inst.distance, perm, 6, ten)
+    want = orc.tabu_run(inst.flow, inst.distance, perm, 6, ten)
+    assert want[5] is True and got[5] is True
+    assert got[6] == want[6]
+    for g, w in zip(got[:5], want[:5]):
+        assert np.array_equal(g, w)
+    for g, w in zip(got[7], want[7]):
+        assert np.array_equal(g, w)
+
+
+def test_batched_runs_match_single(q, orc):
+    from paper_2307_11248_b200 import shapes
+
+    inst = shapes.rand(23, 9)
+    n, iters, B = 23, 40, 9
+    lo, hi = orc.tenure_bounds(n)
+    perms, tens = [], []
+    for b in range(B):
+        r = orc.Rng(orc.derive_seed(3, b))
+        perms.append(r.permutation(n))
+        tens.append(r.tenures(lo, hi, iters))
+    perms, tens = np.stack(perms), np.stack(tens)
+    best, bc, cur, cc, cells, stop, steps, tr = q.kernels.tabu_run_batch(inst.flow, inst.distance, perms, iters, tens)
+    deltas = q.kernels.all_deltas_batch(inst.flow, inst.distance, perms)
+    costs = q.kernels.full_cost_batch(inst.flow, inst.distance, perms)
+    for b in range(B):
+        want = orc.tabu_run(inst.flow, inst.distance, perms[b], iters, tens[b])
+        assert np.array_equal(best[b], want[0]) and bc[b] == want[1]
+        assert np.array_equal(cur[b], want[2]) and cc[b] == want[3]
+        assert np.array_equal(cells[b], want[4])
+        assert steps[b] == want[6]
+        assert np.array_equal(tr[0][b, : want[6]], want[7][0])
+        assert np.array_equal(tr[2][b, : want[6]], want[7][2])
+        assert np.array_equal(deltas[b], orc.all_deltas(inst.flow, inst.distance, perms[b]))
+        assert costs[b] == orc.full_cost(inst.flow, inst.distance, perms[b])
+
+
+@pytest.mark.parametrize("shape,iters,starts", [("tai100a", 40, 3), ("sko100", 40, 2), ("tai150b", 24, 2), ("tai256c", 8, 2)])
+def test_large_shapes_short_runs(q, orc, shape, iters, starts):
+    """BASELINE.json configs 3-5 at oracle-affordable iteration counts: int32 state in
+    shared memory (n=100), int64 state (tai150b), L2-resident state (n=256)."""
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.backend import device_instance
+
+    inst = shapes.by_name(shape)
+    n = inst.n
+    info = device_instance(inst.flow, inst.distance).info
+    if shape == "tai150b":
+        assert info["acc_bits"] == 64
+    lo, hi = orc.tenure_bounds(n)
+    for b in range(starts):
+        r = orc.Rng(orc.derive_seed(11, b))
+        perm = r.permutation(n)
+        ten = r.tenures(lo, hi, iters)
+        assert np.array_equal(q.kernels.all_deltas(inst.flow, inst.distance, perm),
+                              orc.all_deltas(inst.flow, inst.distance, perm))
+        got = q.kernels.tabu_run(inst.flow, inst.distance, perm, iters, ten)
+        want = orc.tabu_run(inst.flow, inst.distance, perm, iters, ten)
+        for idx, (g, w) in enumerate(zip(got[:7], want[:7])):
+            assert np.array_equal(g, w), f"{shape} tabu output {idx}"
+        for idx, (g, w) in enumerate(zip(got[7], want[7])):
+            assert np.array_equal(g, w), f"{shape} trail {idx}"
+        got2 = q.kernels.two_opt_run(inst.flow, inst.distance, perm, iters)
+        want2 = orc.two_opt_run(inst.flow, inst.distance, perm, iters)
+        for idx, (g, w) in enumerate(zip(got2, want2)):
+            assert np.array_equal(g, w), f"{shape} 2opt output {idx}"
+
+
+@pytest.mark.parametrize("algo", ["tabu", "2opt"])
+@pytest.mark.parametrize("shape,starts,iters", [("rand30", 64, 240), ("nug12", 40, 48), ("tai100a", 8, 60), ("rand5", 33, 20)])
+def test_multistart_matches_oracle(q, orc, algo, shape, starts, iters):
+    """Device-side RNG + batched search + reduce == reference run_multistart semantics
+    (multistart.py:86-172): per-start cost vector, winner, tie rule."""
+    from paper_2307_11248_b200 import shapes
+
+    inst = shapes.by_name(shape)
+    res = q.run_multistart(inst, q.SearchConfig(algorithm=algo, n_starts=starts, iterations=iters, master_seed=5))
+    costs, bc, bi, bp = orc.multistart(inst.flow, inst.distance, algo, 5, starts, iters, threads=orc.max_threads())
+    assert np.array_equal(res.per_start_costs, costs)
+    assert res.best.cost == bc and res.best_start_index == bi
+    assert np.array_equal(res.best.permutation, bp)
+    assert res.best.seed == orc.derive_seed(5, bi)
+    assert q.evaluate_cost(inst, res.best.permutation) == res.best.cost
+
+
+def test_multistart_golden_kat30(q):
+    """SURVEY.md 8c known answers generated from the reference itself: kat30,
+    64 starts x 240 iterations, master seed 0."""
+    from paper_2307_11248_b200 import shapes
+
+    inst = shapes.rand(30, 1234)
+    res = q.run_multistart(inst, q.SearchConfig(algorithm="tabu", n_starts=64, iterations=240, master_seed=0))
+    assert (res.best.cost, res.best_start_index, int(res.per_start_costs.sum())) == (1776990, 23, 115222749)
+    res = q.run_multistart(inst, q.SearchConfig(algorithm="2opt", n_starts=64, iterations=120, master_seed=0))
+    assert (res.best.cost, res.best_start_index, int(res.per_start_costs.sum())) == (1809350, 36, 117877671)
+
+
+def test_sequential_rng_path_is_identical(q):
+    """The rejection-exact sequential RNG path (taken when a draw would be rejected)
+    must give the same starts as the parallel fast path."""
+    from paper_2307_11248_b200 import _lib, shapes
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    inst = shapes.rand(23, 2)
+    di = DeviceInstance(inst.flow, inst.distance)
+    fast = di.multistart("tabu", 9, 0, 16, 30, 2, 8)
+    _lib.check(_lib.lib().qapb_debug_force_seq_rng(di.handle, 1))
+    slow = di.multistart("tabu", 9, 0, 16, 30, 2, 8)
+    assert np.array_equal(fast[0], slow[0]) and fast[1:3] == slow[1:3] and np.array_equal(fast[3], slow[3])
+    di.close()
+
+
+def test_first_index_offsets_are_consistent(q):
+    """Sharding invariant used for multi-GPU: starts [8,16) run alone equal the same
+    slice of a [0,16) run."""
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.backend import device_instance
+
+    inst = shapes.rand(12, 4)
+    di = device_instance(inst.flow, inst.distance)
+    whole = di.multistart("tabu", 3, 0, 16, 40, 1, 4)
+    part = di.multistart("tabu", 3, 8, 8, 40, 1, 4)
+    assert np.array_equal(whole[0][8:], part[0])
+
+
+def test_error_mapping(q):
+    from paper_2307_11248_b200 import shapes
+
+    inst = shapes.rand(5, 1)
+    with pytest.raises(q.DomainError):
+        q.kernels.two_opt_run(inst.flow, inst.distance, np.arange(5), 0)
+    with pytest.raises(q.DomainError):
+        q.full_cost(inst, np.arange(4))
