@@ -299,6 +299,8 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     P.gM_stride = m_elems;
     P.gT_stride = t_elems;
     kern_t kern = pick_kernel(h->acc_bits, h->storage, h->lb_class);
+    // several handles share one kernel instantiation: (re)assert this handle's opt-in size
+    CU(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes));
     CU(cudaEventRecord(h->ev0, st));
     kern<<<batch, h->threads, h->smem_bytes, st>>>(P);
     CU(cudaGetLastError());

@@ -1,0 +1,216 @@
+"""Host-side logic (no GPU): RNG, QAPLIB I/O, records, config digest, sharding, error
+classes, the step-wise auditors fed with oracle-produced trails, and the C-ABI surface."""
+import ctypes
+import io
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2307_11248_b200 as q
+from paper_2307_11248_b200 import _lib, multistart, shapes
+from paper_2307_11248_b200.rng import raw_stream
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOY = "2\n0 3\n2 0\n0 1\n5 0"
+
+
+def test_rng_matches_oracle(built):
+    import oracle
+
+    for seed in (0, 5, 2**64 - 3, 123456789):
+        a, b = q.SplitMix64(seed), oracle.Rng(seed)
+        assert [a.next64() for _ in range(5)] == [b.next64() for _ in range(5)]
+        assert [a.randbelow(k) for k in (1, 2, 10, 97, 2**40 + 7)] == [b.randbelow(k) for k in (1, 2, 10, 97, 2**40 + 7)]
+        assert a.state == b.state
+    assert q.derive_seed(7, 5) == 0x3FDABE86CBBEAA11 == oracle.derive_seed(7, 5)
+    assert q.derive_seed(-1, 0) == oracle.derive_seed(-1 & (2**64 - 1), 0)
+    assert np.array_equal(q.random_permutation(23, q.SplitMix64(9)), oracle.Rng(9).permutation(23))
+    with pytest.raises(ValueError):
+        q.derive_seed(1, -1)
+    assert raw_stream(5, 4).tolist() == [q.SplitMix64(5).next64() if False else x for x in
+                                         (lambda r: [r.next64() for _ in range(4)])(q.SplitMix64(5))]
+
+
+def test_random_instance_matches_oracle(built):
+    import oracle
+
+    inst = shapes.rand(12, 1234)
+    f, d = oracle.Rng(oracle.derive_seed(1234, 0)).instance(12)
+    assert np.array_equal(inst.flow, f) and np.array_equal(inst.distance, d)
+    assert inst.flow[0].tolist() == [0, 21, 93, 16, 79, 57, 99, 30, 76, 2, 56, 38]
+
+
+def test_tenure_bounds_table():
+    """test_tabu.py:13-18."""
+    for n, lo, hi in [(30, 3, 10), (100, 10, 33), (12, 1, 4), (256, 25, 85), (2, 1, 1), (150, 15, 50)]:
+        t = q.tenure_bounds(n)
+        assert (t.low, t.high) == (lo, hi)
+    with pytest.raises(q.DomainError):
+        q.tenure_bounds(1)
+    with pytest.raises(q.DomainError):
+        q.TenureInterval(0, 3)
+
+
+def test_parse_and_roundtrip():
+    inst = q.parse_instance(TOY, name="toy")
+    assert inst.n == 2 and inst.flow.tolist() == [[0, 3], [2, 0]] and inst.distance.tolist() == [[0, 1], [5, 0]]
+    assert not inst.flow.flags.writeable
+    buf = io.StringIO()
+    q.write_qaplib(inst, buf)
+    assert q.parse_instance(buf.getvalue(), name="toy") == inst
+    assert q.evaluate_cost(inst, np.array([0, 1])) == 13 and q.evaluate_cost(inst, np.array([1, 0])) == 17
+    with pytest.raises(q.MalformedInstanceError) as e:
+        q.parse_instance("2\n0 3\n2 0\n0 1\n5")
+    assert e.value.byte_offset == len("2\n0 3\n2 0\n0 1\n5")
+    with pytest.raises(q.MalformedInstanceError):
+        q.parse_instance("2 0 3 2 0 0 1 5 0 9")
+    with pytest.raises(q.TokenParseError) as e:
+        q.parse_instance("2\n0 x\n2 0\n0 1\n5 0")
+    assert e.value.byte_offset == 4
+    with pytest.raises(q.MalformedInstanceError):
+        q.parse_instance("")
+    with pytest.raises(q.DomainError):
+        q.parse_instance("1 0 0")
+
+
+def test_solution_io():
+    inst = q.parse_instance(TOY, name="toy")
+    rec = q.SolutionRecord("toy", np.array([0, 1], np.int64), 13, "tabu", 7)
+    buf = io.StringIO()
+    q.write_solution(rec, buf, inst)
+    assert buf.getvalue() == "toy\n2\n13\n1 2\n"
+    back = q.read_solution(buf.getvalue())
+    assert back.cost == 13 and back.permutation.tolist() == [0, 1] and back.instance_name == "toy"
+    with pytest.raises(q.IntegrityError):
+        q.write_solution(q.SolutionRecord("toy", np.array([0, 1]), 14), io.StringIO(), inst)
+
+
+def test_best_known_registry():
+    reg = q.load_best_known("# c\ntai30a,1818146\n\ntai100a,21052466\n")
+    assert reg.get("tai30a") == 1818146 and reg.get("nope") is None
+    with pytest.raises(q.TokenParseError):
+        q.load_best_known("a,b,c\n")
+    with pytest.raises(q.DomainError):
+        q.load_best_known("a,0\n")
+
+
+def test_search_config_and_digest():
+    cfg = q.SearchConfig()
+    assert cfg.n_starts == 6144 and cfg.resolved_iterations(30) == 240
+    assert q.SearchConfig(algorithm="2opt").resolved_iterations(30) == 120
+    for bad in (dict(algorithm="sa"), dict(n_starts=0), dict(iterations=0)):
+        with pytest.raises(q.DomainError):
+            q.SearchConfig(**bad)
+    # digest of (kat30, tabu, 64 starts, 240 iterations, master 0) from the reference
+    inst = shapes.rand(30, 1234)
+    kat = q.Instance("kat30", 30, inst.flow.copy(), inst.distance.copy())
+    cfg = q.SearchConfig(algorithm="tabu", n_starts=64, iterations=240, master_seed=0)
+    assert q.config_digest(kat, cfg) == "bd8b855cdce8c9f9"
+    g = np.load(os.path.join(ROOT, "tests", "golden", "golden_kat30_multi_tabu.npz"))
+    assert q.config_digest(inst, cfg) == str(g["digest"])
+    import dataclasses
+
+    assert q.config_digest(inst, dataclasses.replace(cfg, workers=3)) == q.config_digest(inst, cfg)
+
+
+def test_shard_bounds_partition():
+    for n_starts in (1, 7, 64, 1000, 6144):
+        for world in (1, 2, 3, 4, 8):
+            spans = [multistart.shard_bounds(n_starts, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n_starts
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_moves_and_delta_cost(built):
+    import oracle
+
+    assert q.enumerate_moves(4) == [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
+    rs = np.random.default_rng(3)
+    for n in (3, 7, 12):
+        f = rs.integers(-20, 50, (n, n)).astype(np.int64)
+        d = rs.integers(-20, 50, (n, n)).astype(np.int64)
+        inst = q.Instance("x", n, f, d)
+        p = rs.permutation(n).astype(np.int64)
+        want = oracle.all_deltas(f, d, p)
+        got = [q.delta_cost(inst, p, mv) for mv in q.enumerate_moves(n)]
+        assert got == want.tolist()
+        for mv, dl in zip(q.enumerate_moves(n), got):
+            assert q.evaluate_cost(inst, q.apply_move(p, mv)) == q.evaluate_cost(inst, p) + dl
+    with pytest.raises(q.DomainError):
+        q.apply_move(np.arange(4), (2, 1))
+    with pytest.raises(q.DomainError):
+        q.apply_move(np.arange(4), (1, 1))
+
+
+def test_admissibility_truth_table():
+    """test_tabu.py:53-71."""
+    cells = np.zeros((3, 3), np.int64)
+    cells[0, 1] = 5
+    assert q.is_admissible(cells, (0, 1), 100, 50, 5)        # expired exactly now
+    assert not q.is_admissible(cells, (0, 1), 100, 50, 4)    # tabu, no aspiration
+    assert q.is_admissible(cells, (0, 1), 49, 50, 4)         # aspirated
+    assert not q.is_admissible(cells, (0, 1), 50, 50, 4)     # equal does not aspirate
+    cells[1, 0] = 99                                         # frequency cell is never read
+    assert q.is_admissible(cells, (0, 2), 100, 50, 1)
+    with pytest.raises(q.DomainError):
+        q.is_admissible(cells, (1, 0), 1, 1, 1)
+
+
+def test_trail_csv_format():
+    tr = q.TabuTrail("t", np.array([0, 1]), q.TenureInterval(1, 2), 2, False, np.array([0]), np.array([1]),
+                     np.array([-4]), np.array([0]), np.array([0]), np.array([2]))
+    buf = io.StringIO()
+    q.write_trail(tr, buf)
+    assert buf.getvalue() == "iter,i,j,delta,tabu_flag,aspirated_flag,tenure_drawn\n1,1,2,-4,0,0,2\n"
+
+
+def test_abi_exports_every_declared_symbol(built):
+    """The library loads (no GPU needed) and exports every function include/qapb.h declares."""
+    header = open(os.path.join(ROOT, "include", "qapb.h")).read()
+    declared = set(re.findall(r"\b(qapb_[a-z0-9_]+)\s*\(", header))
+    assert declared, "no declarations found"
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"{name} declared in qapb.h but not exported"
+    assert declared == set(_lib.SIGNATURES), "ctypes table and header disagree"
+    assert _lib.lib().qapb_version() == 1
+
+
+def test_abi_argument_errors_without_gpu(built):
+    """Argument validation happens before any CUDA work and maps to DomainError."""
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    f = np.zeros((1, 1), np.int64)
+    rc = L.qapb_create(1, f.ctypes.data, f.ctypes.data, 0, ctypes.byref(h))
+    assert rc == _lib.ERR_INVALID and b"n" in L.qapb_last_error()
+    with pytest.raises(q.DomainError):
+        _lib.check(rc)
+    assert L.qapb_get_info(None, None) == _lib.ERR_INVALID
+    assert L.qapb_destroy(None) == _lib.OK
+
+
+def test_no_cpu_fallback(built):
+    """Without a CUDA device compute entries raise QapError -- nothing is computed on the host."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    inst = q.parse_instance(TOY, name="toy")
+    with pytest.raises(q.QapError):
+        q.full_cost(inst, np.array([0, 1]))
+    with pytest.raises(q.QapError):
+        q.run_multistart(inst, q.SearchConfig(n_starts=2, iterations=2))
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2307_11248_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, fn)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", text, re.M), fn
+                assert "liboracle" not in text, fn
