@@ -6,6 +6,7 @@
 // per thread, where the placement matrix lives), workspace and launches.
 #include "../../include/qapb.h"
 #include "search_kernel.cuh"
+#include "search_reg.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -35,6 +36,7 @@ struct qapb_handle {
     int acc_bits = 32, symmetric = 0;
     int nunits = 0, noff = 0, threads = 0, upt = 0, storage = 0;
     int lb_class = 0;  // 0: <=384 threads, 2 CTAs/SM register budget; 1: <=512 threads
+    int g_threads = 0, g_upt = 0, g_lb_class = 0;  // generic-kernel plan (all_deltas on register-resident handles)
     unsigned smem_bytes = 0;
     int ctas_per_sm = 0, sm_count = 0;
     long long delta_bound = 0;
@@ -61,6 +63,18 @@ static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
     };
 #undef K
     return tab[acc_bits == 64][storage][lb_class];
+}
+
+static kern_t pick_reg_kernel(int symmetric, int lb_class)
+{
+#define KR(S, MT, MB) (kern_t) qap_search_reg_kernel<S, MT, MB>
+    static kern_t tab[2][2] = {{KR(false, 352, 2), KR(false, 544, 1)}, {KR(true, 352, 2), KR(true, 544, 1)}};
+#undef KR
+    return tab[symmetric != 0][lb_class];
+}
+static kern_t handle_kernel(const qapb_handle *h)
+{
+    return h->storage == 3 ? pick_reg_kernel(h->symmetric, h->lb_class) : pick_kernel(h->acc_bits, h->storage, h->lb_class);
 }
 
 extern "C" int qapb_version(void) { return 1; }
@@ -181,14 +195,25 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     h->upt = upt;
     h->threads = threads;
     h->lb_class = threads <= 384 ? 0 : 1;
+    h->g_threads = threads; h->g_upt = upt; h->g_lb_class = h->lb_class;
     int storage = 0;
-    for (; storage < 3; ++storage) {
-        SmemLayout L = make_layout(npad, h->nunits, threads, upt, acc_bytes, storage);
-        if (L.total <= smem_cap) { h->smem_bytes = L.total; break; }
-    }
-    if (storage == 3) {
-        delete h;
-        return fail(QAPB_ERR_UNSUPPORTED, "instance too large for shared-memory vectors");
+    const char *force = getenv("QAPB_FORCE_GENERIC");
+    if (h->acc_bits == 32 && nb <= 32 && !(force && force[0] == '1')) {
+        // register-resident plan: one thread per off-diagonal unit + one warp for the diagonal blocks
+        storage = 3;
+        h->upt = 1;
+        h->threads = (h->noff + 31) / 32 * 32 + 32;
+        h->lb_class = h->threads <= 352 ? 0 : 1;
+        h->smem_bytes = make_reg_layout(npad, nb).total;
+    } else {
+        for (; storage < 3; ++storage) {
+            SmemLayout L = make_layout(npad, h->nunits, threads, upt, acc_bytes, storage);
+            if (L.total <= smem_cap) { h->smem_bytes = L.total; break; }
+        }
+        if (storage == 3) {
+            delete h;
+            return fail(QAPB_ERR_UNSUPPORTED, "instance too large for shared-memory vectors");
+        }
     }
     h->storage = storage;
 
@@ -228,7 +253,7 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     if (e == cudaSuccess) e = up((void **)&h->dunit, units.data(), units.size() * sizeof(uint16_t));
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
-    kern_t kern = pick_kernel(h->acc_bits, h->storage, h->lb_class);
+    kern_t kern = handle_kernel(h);
     if (e == cudaSuccess) e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, (const void *)kern, h->threads, h->smem_bytes);
     if (e != cudaSuccess) {
@@ -289,20 +314,29 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     const size_t t_elems = (size_t)h->upt * 4 * h->threads * 4;
     size_t need = (extra_ws + 255) / 256 * 256;
     size_t offM = need;
-    if (h->storage >= 1 && P.mode != MODE_ALL_DELTAS) need += m_elems * acc_bytes * batch;
+    if ((h->storage == 1 || h->storage == 2) && P.mode != MODE_ALL_DELTAS) need += m_elems * acc_bytes * batch;
     size_t offT = need;
-    if (h->storage >= 2 && P.mode != MODE_ALL_DELTAS) need += t_elems * sizeof(int32_t) * batch;
+    if (h->storage == 2 && P.mode != MODE_ALL_DELTAS) need += t_elems * sizeof(int32_t) * batch;
     int rc = ensure_ws(h, need);
     if (rc) return rc;
     P.gM = (char *)h->ws + offM;
     P.gT = (char *)h->ws + offT;
     P.gM_stride = m_elems;
     P.gT_stride = t_elems;
-    kern_t kern = pick_kernel(h->acc_bits, h->storage, h->lb_class);
-    // several handles share one kernel instantiation: (re)assert this handle's opt-in size
-    CU(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes));
+    kern_t kern = handle_kernel(h);
+    int threads = h->threads;
+    unsigned smem = h->smem_bytes;
+    if (h->storage == 3 && P.mode == MODE_ALL_DELTAS) {
+        // the full evaluator lives in the generic kernel; it keeps no per-search state
+        kern = pick_kernel(32, 2, h->g_lb_class);
+        threads = h->g_threads;
+        P.upt = h->g_upt;
+        smem = make_layout(h->npad, h->nunits, threads, P.upt, 4, 2).total;
+    }
+    // several handles share one kernel instantiation: (re)assert this launch's opt-in size
+    CU(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CU(cudaEventRecord(h->ev0, st));
-    kern<<<batch, h->threads, h->smem_bytes, st>>>(P);
+    kern<<<batch, threads, smem, st>>>(P);
     CU(cudaGetLastError());
     CU(cudaEventRecord(h->ev1, st));
     h->have_timing = 1;
@@ -417,8 +451,8 @@ extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, u
         const size_t acc_bytes = h->acc_bits / 8;
         const size_t m_elems = (size_t)h->upt * 8 * h->threads * 4, t_elems = (size_t)h->upt * 4 * h->threads * 4;
         size_t need = (head + 255) / 256 * 256;
-        if (h->storage >= 1) need += m_elems * acc_bytes * count;
-        if (h->storage >= 2) need += t_elems * sizeof(int32_t) * count;
+        if (h->storage == 1 || h->storage == 2) need += m_elems * acc_bytes * count;
+        if (h->storage == 2) need += t_elems * sizeof(int32_t) * count;
         rc = ensure_ws(h, need);
         if (rc) return rc;
     }

@@ -1,0 +1,513 @@
+// search_reg.cuh -- register-resident variant of the search kernel (n <= 128, int32 state).
+//
+// Same algorithm and the same integers as qap_search_kernel (search_kernel.cuh), but the
+// placement matrix M and the tabu triangle never leave the register file: thread t < noff
+// owns off-diagonal unit t = block pair {(I,J),(J,I)} as 32 + 16 registers for the whole
+// run, so the per-iteration pass is pure ALU work (rank-2 update, delta, admissibility,
+// running argmin) fed by a handful of 128-bit shared-memory vector loads.  The last warp
+// owns the nb diagonal 4x4 blocks, kept in shared memory.
+//
+// After move (r,s) the 4n entries on rows/columns r,s do not follow the rank-2 rule.  They
+// are fixed at the start of the next pass from six n-vectors published between the two
+// barriers of an iteration:
+//   colR[i] = M[i][r], colS[i] = M[i][s]     dumped by the threads that own those columns
+//   tR[i], tS[i]                             additive terms of  M'[i][r] = colS[i] + tR[i],
+//                                                               M'[i][s] = colR[i] + tS[i]
+//   xR[i], xS[i]                             additive terms of  M'[r][i] = M[r][i] + xR[i], ...
+// with the corner values M'[r][s], M'[s][r] folded into tS[r], tR[s] (colR[r] = colS[s] = 0)
+// and h[r], h[s] written by the thread that owns the winning pair.  r & 3 and s & 3 are
+// uniform across the CTA, so the register indices are selected with uniform switches.
+#pragma once
+#include "search_kernel.cuh"
+
+namespace qapb {
+
+struct RegLayout {
+    unsigned offA, offC, offB, offE, offH, offColR, offColS, offTR, offTS, offXR, offXS;
+    unsigned offP, offJ, offDM, offDT, offRedD, offRedK, offMisc, total;
+};
+
+__host__ __device__ inline RegLayout make_reg_layout(int npad, int nb)
+{
+    RegLayout L;
+    unsigned o = 0;
+    const unsigned v = 4u * (unsigned)npad;
+    L.offA = o; o += v; L.offC = o; o += v; L.offB = o; o += v; L.offE = o; o += v; L.offH = o; o += v;
+    L.offColR = o; o += v; L.offColS = o; o += v; L.offTR = o; o += v; L.offTS = o; o += v;
+    L.offXR = o; o += v; L.offXS = o; o += v;
+    L.offP = o; o += v; L.offJ = o; o += v;
+    L.offDM = o; o += 64u * (unsigned)nb;
+    L.offDT = o; o += 64u * (unsigned)nb;
+    L.offRedD = o; o += 32u * 8u;
+    L.offRedK = o; o += 32u * 4u;
+    L.offMisc = o; o += 64u;
+    L.total = align16(o);
+    return L;
+}
+
+__device__ __forceinline__ int32_t pick16(const int32_t (&A)[4][4], int slot)
+{
+    int32_t r = A[0][0];
+#pragma unroll
+    for (int q = 1; q < 16; ++q) r = (slot == q) ? A[q >> 2][q & 3] : r;
+    return r;
+}
+__device__ __forceinline__ void put16(int32_t (&A)[4][4], int slot, int32_t val)
+{
+#pragma unroll
+    for (int q = 0; q < 16; ++q) A[q >> 2][q & 3] = (slot == q) ? val : A[q >> 2][q & 3];
+}
+__device__ __forceinline__ void st_vec4(int32_t *arr, int blk, int32_t a, int32_t b, int32_t c, int32_t d)
+{
+    reinterpret_cast<int4 *>(arr)[blk] = make_int4(a, b, c, d);
+}
+
+// M entries of one unit from scratch (O(n) per entry): the full evaluator, also used by
+// kernels.all_deltas.  U[u][v] = M[4I+u][4J+v], L[v][u] = M[4J+v][4I+u].
+__device__ __forceinline__ void build_unit(const SearchParams &P, const int32_t *sP, int I, int J, bool sym,
+                                           int32_t (&U)[4][4], int32_t (&L)[4][4], int32_t (&Ex)[4][4])
+{
+    const int n = P.n, npad = P.npad;
+    const int32_t *__restrict__ F = P.F;
+    const int32_t *__restrict__ FT = P.FT;
+    const int32_t *__restrict__ D = P.D;
+    const int32_t *__restrict__ DT = P.DT;
+    int pI[4], pJ[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { pI[u] = sP[4 * I + u]; pJ[u] = sP[4 * J + u]; }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) { U[u][v] = 0; L[u][v] = 0; }
+    for (int kk = 0; kk < n; ++kk) {
+        const int pk = sP[kk];
+        int32_t dI[4], dJ[4], fI[4], fJ[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            dI[u] = D[(4 * I + u) * npad + kk];
+            dJ[u] = D[(4 * J + u) * npad + kk];
+            fI[u] = F[pI[u] * npad + pk];
+            fJ[u] = F[pJ[u] * npad + pk];
+        }
+        if (sym) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    U[u][v] += dI[u] * fJ[v];
+                    L[v][u] += dJ[v] * fI[u];
+                }
+        } else {
+            int32_t dtI[4], dtJ[4], ftI[4], ftJ[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                dtI[u] = DT[(4 * I + u) * npad + kk];
+                dtJ[u] = DT[(4 * J + u) * npad + kk];
+                ftI[u] = FT[pI[u] * npad + pk];
+                ftJ[u] = FT[pJ[u] * npad + pk];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    U[u][v] += dI[u] * fJ[v] + dtI[u] * ftJ[v];
+                    L[v][u] += dJ[v] * fI[u] + dtJ[v] * ftI[u];
+                }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int i = 4 * I + u, j = 4 * J + v;
+            if (sym) { U[u][v] *= 2; L[v][u] *= 2; }
+            const int32_t fs = F[pI[u] * npad + pJ[v]] + F[pJ[v] * npad + pI[u]];
+            U[u][v] += D[i * npad + j] * fs + P.dd[i] * P.fd[pJ[v]];
+            L[v][u] += D[j * npad + i] * fs + P.dd[j] * P.fd[pI[u]];
+            const bool pad = (i >= n) || (j >= n);
+            if (pad) { U[u][v] = 1 << 29; L[v][u] = 1 << 29; }
+            if (i == j) { U[u][v] = 0; L[v][u] = 0; }
+            Ex[u][v] = pad ? 0x7fffffff : 0;
+        }
+}
+
+#define QAPB_SWITCH4(idx, BODY)            \
+    switch (idx) {                         \
+        case 0: { constexpr int q = 0; BODY } break; \
+        case 1: { constexpr int q = 1; BODY } break; \
+        case 2: { constexpr int q = 2; BODY } break; \
+        default: { constexpr int q = 3; BODY } break; \
+    }
+
+template <bool SYM, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const SearchParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
+    const int b = blockIdx.x;
+    const int n = P.n, nb = P.nb, npad = P.npad, noff = P.noff;
+    const int Toff = T - 32;  // the last warp owns the diagonal blocks
+    const RegLayout lay = make_reg_layout(npad, nb);
+    int32_t *sA = reinterpret_cast<int32_t *>(smem_raw + lay.offA);
+    int32_t *sC = reinterpret_cast<int32_t *>(smem_raw + lay.offC);
+    int32_t *sB = reinterpret_cast<int32_t *>(smem_raw + lay.offB);
+    int32_t *sE = reinterpret_cast<int32_t *>(smem_raw + lay.offE);
+    int32_t *sH = reinterpret_cast<int32_t *>(smem_raw + lay.offH);
+    int32_t *sColR = reinterpret_cast<int32_t *>(smem_raw + lay.offColR);
+    int32_t *sColS = reinterpret_cast<int32_t *>(smem_raw + lay.offColS);
+    int32_t *sTR = reinterpret_cast<int32_t *>(smem_raw + lay.offTR);
+    int32_t *sTS = reinterpret_cast<int32_t *>(smem_raw + lay.offTS);
+    int32_t *sXR = reinterpret_cast<int32_t *>(smem_raw + lay.offXR);
+    int32_t *sXS = reinterpret_cast<int32_t *>(smem_raw + lay.offXS);
+    int32_t *sP = reinterpret_cast<int32_t *>(smem_raw + lay.offP);
+    unsigned *sJ = reinterpret_cast<unsigned *>(smem_raw + lay.offJ);
+    int32_t *sDM = reinterpret_cast<int32_t *>(smem_raw + lay.offDM);  // [nb][4][4]
+    int32_t *sDT = reinterpret_cast<int32_t *>(smem_raw + lay.offDT);  // [nb][4][4]
+    long long *sRed64 = reinterpret_cast<long long *>(smem_raw + lay.offRedD);
+    int32_t *sRedD = reinterpret_cast<int32_t *>(smem_raw + lay.offRedD);
+    unsigned *sRedK = reinterpret_cast<unsigned *>(smem_raw + lay.offRedK);
+    long long *sMisc = reinterpret_cast<long long *>(smem_raw + lay.offMisc);
+
+    const int32_t *__restrict__ F = P.F;
+    const int32_t *__restrict__ FT = P.FT;
+    const int32_t *__restrict__ D = P.D;
+    const int32_t *__restrict__ DT = P.DT;
+    const int32_t MAXV = 0x7fffffff;
+
+    // ---------------------------------------------------------------- setup
+    for (int i = tid; i < npad; i += T) {
+        sA[i] = 0; sC[i] = 0; sB[i] = 0; sE[i] = 0; sH[i] = 0;
+        sColR[i] = 0; sColS[i] = 0; sTR[i] = 0; sTS[i] = 0; sXR[i] = 0; sXS[i] = 0;
+        sP[i] = (P.rng || i >= n) ? (i < n ? i : 0) : (int32_t)P.perms[(size_t)b * n + i];
+    }
+    unsigned long long rng_state = 0;
+    if (P.rng) {
+        const unsigned long long seed = mix64(P.master_seed + QAPB_GAMMA * (P.first_index + (unsigned long long)b + 1ULL));
+        int reject = P.force_seq_rng;
+        for (int k = tid; k < n - 1; k += T) {
+            unsigned long long bound = (unsigned long long)(n - 1 - k) + 1ULL;
+            unsigned long long r = mix64(seed + QAPB_GAMMA * ((unsigned long long)k + 1ULL));
+            unsigned long long rem = (0ULL - bound) % bound;
+            if (r > ~0ULL - rem) reject = 1;
+            sJ[n - 1 - k] = (unsigned)(r % bound);
+        }
+        reject = __syncthreads_or(reject);
+        if (tid == 0) {
+            rng_state = seed;
+            if (reject) {
+                for (int i = n - 1; i >= 1; --i) {
+                    unsigned j = (unsigned)randbelow_seq(rng_state, (unsigned long long)i + 1ULL);
+                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
+                }
+            } else {
+                for (int i = n - 1; i >= 1; --i) {
+                    unsigned j = sJ[i];
+                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
+                }
+                rng_state = seed + QAPB_GAMMA * (unsigned long long)(n - 1);
+            }
+            if (P.mode == MODE_TABU)
+                sMisc[1] = P.ten_lo + (long long)randbelow_seq(rng_state, (unsigned long long)(P.ten_hi - P.ten_lo + 1));
+        }
+    }
+    if (P.cells) {
+        int64_t *cz = P.cells + (size_t)b * n * n;
+        for (int i = tid; i < n * n; i += T) cz[i] = 0;
+    }
+    __syncthreads();
+
+    long long cost;
+    {
+        long long part = 0;
+        for (int idx = tid; idx < n * n; idx += T) {
+            int i = idx / n, j = idx - i * n;
+            int pi = sP[i], pj = sP[j];
+            part += (i == j) ? (long long)P.fd[pi] * P.dd[i] : (long long)F[pi * npad + pj] * D[i * npad + j];
+        }
+        cost = block_sum_i64(part, sRed64, tid, T);
+        __syncthreads();
+    }
+    for (int i = tid; i < n; i += T) {
+        int pi = sP[i];
+        int32_t acc = P.dd[i] * P.fd[pi];
+        if (SYM) {
+            for (int k = 0; k < n; ++k) acc += 2 * (D[i * npad + k] * F[pi * npad + sP[k]]);
+        } else {
+            for (int k = 0; k < n; ++k) {
+                int pk = sP[k];
+                acc += D[i * npad + k] * F[pi * npad + pk] + DT[i * npad + k] * FT[pi * npad + pk];
+            }
+        }
+        sH[i] = acc;
+    }
+
+    const bool offd = tid < noff;
+    const int dblk = tid - Toff;  // diagonal block index for the last warp
+    const bool diag = dblk >= 0 && dblk < nb;
+    int I = 0, J = 0;
+    if (offd) { I = P.unit_ij[tid] & 0xff; J = P.unit_ij[tid] >> 8; }
+    int32_t U[4][4], L[4][4], E[4][4];
+    if (offd) {
+        build_unit(P, sP, I, J, SYM, U, L, E);
+    } else if (diag) {
+        int32_t Ud[4][4], Ld[4][4], Ed[4][4];
+        build_unit(P, sP, dblk, dblk, SYM, Ud, Ld, Ed);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                sDM[dblk * 16 + u * 4 + v] = Ud[u][v];
+                sDT[dblk * 16 + u * 4 + v] = (u < v) ? Ed[u][v] : 0x7fffffff;
+            }
+    }
+    __syncthreads();
+
+    // ------------------------------------------------------------ iterations
+    long long best_cost = cost;
+    int32_t thr = 0;
+    const bool tabu = P.mode == MODE_TABU;
+    const int iters = P.iterations;
+    int steps_done = 0, stopped = 0;
+    int64_t *best_out = P.best + (size_t)b * n;
+    for (int i = tid; i < n; i += T) best_out[i] = sP[i];
+    int R = -1, S = -1, ru = 0, su = 0;  // previous move (block and in-block indices)
+
+    for (int c = 1; c <= iters; ++c) {
+        long long ten = 0;
+        if (tabu && !P.rng) ten = P.tenures[(size_t)b * iters + (c - 1)];
+
+        int32_t my_d = MAXV;
+        int my_slot = 0, my_flag = 0;
+        unsigned my_key = 0xffffffffu;
+        if (offd) {
+            if (R >= 0) {
+                // ---- generic rank-2 update
+                int32_t aI[4], bI[4], aJ[4], bJ[4];
+                ld_vec4(sA, I, aI); ld_vec4(sB, I, bI); ld_vec4(sA, J, aJ); ld_vec4(sB, J, bJ);
+                if (SYM) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            U[u][v] -= aI[u] * bJ[v];
+                            L[v][u] -= aJ[v] * bI[u];
+                        }
+                } else {
+                    int32_t cI[4], eI[4], cJ[4], eJ[4];
+                    ld_vec4(sC, I, cI); ld_vec4(sE, I, eI); ld_vec4(sC, J, cJ); ld_vec4(sE, J, eJ);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            U[u][v] -= aI[u] * bJ[v] + cI[u] * eJ[v];
+                            L[v][u] -= aJ[v] * bI[u] + cJ[v] * eI[u];
+                        }
+                }
+                // ---- rows / columns r and s of the previous move
+                if (I == R || J == R || I == S || J == S) {
+                    if (I == R) {
+                        int32_t x[4], cs[4], t[4];
+                        ld_vec4(sXR, J, x); ld_vec4(sColS, J, cs); ld_vec4(sTR, J, t);
+                        QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+                            for (int v = 0; v < 4; ++v) { U[q][v] += x[v]; L[v][q] = cs[v] + t[v]; }
+                        })
+                    }
+                    if (J == R) {
+                        int32_t x[4], cs[4], t[4];
+                        ld_vec4(sXR, I, x); ld_vec4(sColS, I, cs); ld_vec4(sTR, I, t);
+                        QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+                            for (int u = 0; u < 4; ++u) { L[q][u] += x[u]; U[u][q] = cs[u] + t[u]; }
+                        })
+                    }
+                    if (I == S) {
+                        int32_t x[4], cr[4], t[4];
+                        ld_vec4(sXS, J, x); ld_vec4(sColR, J, cr); ld_vec4(sTS, J, t);
+                        QAPB_SWITCH4(su, {
+_Pragma("unroll")
+                            for (int v = 0; v < 4; ++v) { U[q][v] += x[v]; L[v][q] = cr[v] + t[v]; }
+                        })
+                    }
+                    if (J == S) {
+                        int32_t x[4], cr[4], t[4];
+                        ld_vec4(sXS, I, x); ld_vec4(sColR, I, cr); ld_vec4(sTS, I, t);
+                        QAPB_SWITCH4(su, {
+_Pragma("unroll")
+                            for (int u = 0; u < 4; ++u) { L[q][u] += x[u]; U[u][q] = cr[u] + t[u]; }
+                        })
+                    }
+                }
+            }
+            // ---- delta, admissibility (_kernels.pyx:162), running first-minimum
+            int32_t hI[4], hJ[4];
+            ld_vec4(sH, I, hI);
+            ld_vec4(sH, J, hJ);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int32_t d = U[u][v] + L[v][u] - hI[u] - hJ[v];
+                    const bool adm = (E[u][v] <= c) || (d < thr);
+                    if (adm && d < my_d) { my_d = d; my_slot = u * 4 + v; }
+                }
+            if (my_d != MAXV) {
+                my_flag = pick16(E, my_slot) > c ? 1 : 0;
+                my_key = pair_key(4 * I + (my_slot >> 2), 4 * J + (my_slot & 3), my_flag);
+            }
+        } else if (diag) {
+            int32_t *dm = sDM + dblk * 16;
+            if (R >= 0) {
+                // special entries first (direct shared-memory addressing), then the generic rule
+                if (dblk == R) {
+                    for (int u = 0; u < 4; ++u)
+                        if (u != ru) dm[u * 4 + ru] = sColS[4 * R + u] + sTR[4 * R + u];
+                }
+                if (dblk == S) {
+                    for (int u = 0; u < 4; ++u)
+                        if (u != su) dm[u * 4 + su] = sColR[4 * S + u] + sTS[4 * S + u];
+                }
+                if (dblk == R) {
+                    for (int v = 0; v < 4; ++v)
+                        if (v != ru) dm[ru * 4 + v] += sXR[4 * R + v];
+                }
+                if (dblk == S) {
+                    for (int v = 0; v < 4; ++v)
+                        if (v != su) dm[su * 4 + v] += sXS[4 * S + v];
+                }
+                int32_t aI[4], bI[4], cI[4], eI[4];
+                ld_vec4(sA, dblk, aI); ld_vec4(sB, dblk, bI); ld_vec4(sC, dblk, cI); ld_vec4(sE, dblk, eI);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+                        if (u != v) dm[u * 4 + v] -= SYM ? aI[u] * bI[v] : aI[u] * bI[v] + cI[u] * eI[v];
+            }
+            int32_t hI[4];
+            ld_vec4(sH, dblk, hI);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = u + 1; v < 4; ++v) {
+                    const int32_t d = dm[u * 4 + v] + dm[v * 4 + u] - hI[u] - hI[v];
+                    const int32_t ex = sDT[dblk * 16 + u * 4 + v];
+                    const bool adm = (ex <= c) || (d < thr);
+                    if (adm && d < my_d) { my_d = d; my_slot = u * 4 + v; my_flag = ex > c ? 1 : 0; }
+                }
+            if (my_d != MAXV) my_key = pair_key(4 * dblk + (my_slot >> 2), 4 * dblk + (my_slot & 3), my_flag);
+        }
+
+        int32_t bd = my_d;
+        unsigned bkey = my_key;
+        warp_argmin(bd, bkey);
+        if (lane == 0) { sRedD[warp] = bd; sRedK[warp] = bkey; }
+        __syncthreads();  // ---------------------------------------------- sync #1
+        bd = lane < W ? sRedD[lane] : MAXV;
+        bkey = lane < W ? sRedK[lane] : 0xffffffffu;
+        warp_argmin(bd, bkey);
+        if (bd == MAXV) {
+            stopped = 1;
+            break;
+        }
+        const int r = (int)(bkey >> 17), s = (int)((bkey >> 1) & 0xffffu);
+        const int was_tabu = (int)(bkey & 1u);
+        cost += (long long)bd;
+        const bool improved = cost < best_cost;
+        if (improved) best_cost = cost;
+        thr = Acc<int32_t>::clamp_thr(best_cost - cost);
+        if (tabu && P.rng) ten = sMisc[c & 1];
+        steps_done = c;
+        R = r >> 2; S = s >> 2; ru = r & 3; su = s & 3;
+
+        if (tid == 0) {
+            if (P.tr_i) {
+                const size_t o = (size_t)b * iters + (c - 1);
+                P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
+                if (P.tr_tabu) P.tr_tabu[o] = was_tabu;
+            }
+            if (tabu && P.rng && c < iters)
+                sMisc[(c + 1) & 1] = P.ten_lo + (long long)randbelow_seq(rng_state, (unsigned long long)(P.ten_hi - P.ten_lo + 1));
+        }
+
+        const int pr = sP[r], ps = sP[s];
+        const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
+        const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
+
+        // ---- the thread owning the winning pair: corners, h[r], h[s], tabu memory
+        if (my_key == bkey && my_d != MAXV) {
+            int32_t mrs, msr;
+            if (offd) {
+                mrs = pick16(U, ru * 4 + su);
+                msr = pick16(L, su * 4 + ru);
+                if (tabu) put16(E, ru * 4 + su, (int32_t)(c + ten));
+            } else {
+                mrs = sDM[R * 16 + ru * 4 + su];
+                msr = sDM[R * 16 + su * 4 + ru];
+                if (tabu) sDT[R * 16 + ru * 4 + su] = (int32_t)(c + ten);
+            }
+            const int32_t hr = sH[r], hs = sH[s];
+            sTS[r] = hr + (Drs - Dsr) * Fpspr;  // M'[r][s]
+            sTR[s] = hs + (Dsr - Drs) * Fprps;  // M'[s][r]
+            sH[r] = mrs + (Dsr - Drs) * Fprps;
+            sH[s] = msr + (Drs - Dsr) * Fpspr;
+            if (tabu && P.cells) {
+                int64_t *cz = P.cells + (size_t)b * n * n;
+                cz[(size_t)r * n + s] = (int64_t)c + ten;
+                cz[(size_t)s * n + r] += 1;
+            }
+        }
+        // ---- owners of columns r and s publish them
+        if (offd) {
+            if (J == R) { QAPB_SWITCH4(ru, { st_vec4(sColR, I, U[0][q], U[1][q], U[2][q], U[3][q]); }) }
+            if (I == R) { QAPB_SWITCH4(ru, { st_vec4(sColR, J, L[0][q], L[1][q], L[2][q], L[3][q]); }) }
+            if (J == S) { QAPB_SWITCH4(su, { st_vec4(sColS, I, U[0][q], U[1][q], U[2][q], U[3][q]); }) }
+            if (I == S) { QAPB_SWITCH4(su, { st_vec4(sColS, J, L[0][q], L[1][q], L[2][q], L[3][q]); }) }
+        } else if (diag) {
+            if (dblk == R)
+                for (int u = 0; u < 4; ++u) sColR[4 * R + u] = (u != ru) ? sDM[R * 16 + u * 4 + ru] : 0;
+            if (dblk == S)
+                for (int u = 0; u < 4; ++u) sColS[4 * S + u] = (u != su) ? sDM[S * 16 + u * 4 + su] : 0;
+        }
+        // ---- difference vectors of the move (old permutation), additive terms, h
+        for (int i = tid; i < n; i += T) {
+            const int pi = sP[i];
+            if (improved) best_out[i] = (i == r) ? ps : (i == s) ? pr : pi;
+            int32_t a = 0, cc = 0, bb = 0, e = 0, xr = 0, xs = 0, tr = 0, ts = 0;
+            if (i != r && i != s) {
+                const int32_t Dsi = D[s * npad + i], Dri = D[r * npad + i];
+                const int32_t Dis = DT[s * npad + i], Dir = DT[r * npad + i];
+                const int32_t Fpips = FT[ps * npad + pi], Fpipr = FT[pr * npad + pi];
+                const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
+                a = Dis - Dir; cc = Dsi - Dri; bb = Fpips - Fpipr; e = Fpspi - Fprpi;
+                const int32_t be = bb + e;
+                xr = -Drs * bb - Dsr * e + Dri * be;
+                xs = Dsr * bb + Drs * e - Dsi * be;
+                tr = a * (Fpspr - (Fpips + Fpspi)) + cc * Fprps;
+                ts = a * ((Fpipr + Fprpi) - Fprps) - cc * Fpspr;
+                sH[i] -= a * bb + cc * e;
+                sTR[i] = tr;
+                sTS[i] = ts;
+            } else if (i == r) {
+                sTR[i] = 0;  // tS[r] is written by the owner of the pair
+            } else {
+                sTS[i] = 0;  // tR[s] is written by the owner of the pair
+            }
+            sA[i] = SYM ? 2 * a : a;
+            sC[i] = cc; sB[i] = bb; sE[i] = e;
+            sXR[i] = xr; sXS[i] = xs;
+        }
+        __syncthreads();  // ---------------------------------------------- sync #2
+        if (tid == 0) { const int32_t t = sP[r]; sP[r] = sP[s]; sP[s] = t; }
+    }
+    __syncthreads();
+
+    for (int i = tid; i < n; i += T) P.cur[(size_t)b * n + i] = sP[i];
+    if (tid == 0) {
+        P.best_cost[b] = best_cost;
+        P.cur_cost[b] = cost;
+        if (P.stopped) P.stopped[b] = stopped;
+        if (P.steps) P.steps[b] = steps_done;
+    }
+}
+
+}  // namespace qapb
