@@ -287,6 +287,16 @@ extern "C" int qapb_get_info(const qapb_handle *h, qapb_info *info)
     return QAPB_OK;
 }
 
+// development hook (not in the public header): phase-cycle counters of CTA 0 of the next launches
+static long long *g_dbg = nullptr;
+extern "C" int qapb_debug_phase_cycles(long long *out15)
+{
+    if (!g_dbg) { if (cudaMalloc(&g_dbg, 15 * sizeof(long long)) != cudaSuccess) return QAPB_ERR_NOMEM; cudaMemset(g_dbg, 0, 15 * sizeof(long long)); return QAPB_OK; }
+    cudaDeviceSynchronize();
+    cudaMemcpy(out15, g_dbg, 15 * sizeof(long long), cudaMemcpyDeviceToHost);
+    return QAPB_OK;
+}
+
 // test hook (not declared in the public header): force the sequential RNG path
 extern "C" int qapb_debug_force_seq_rng(qapb_handle *h, int on)
 {
@@ -303,6 +313,7 @@ static void base_params(const qapb_handle *h, SearchParams &P)
     P.force_seq_rng = h->force_seq_rng;
     P.F = h->dF; P.FT = h->dFT; P.D = h->dD; P.DT = h->dDT; P.fd = h->dfd; P.dd = h->ddd;
     P.unit_ij = h->dunit;
+    P.dbg = g_dbg;
 }
 
 // Launch the search kernel for `batch` starts.  `extra_ws` bytes are reserved at
@@ -326,12 +337,15 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     kern_t kern = handle_kernel(h);
     int threads = h->threads;
     unsigned smem = h->smem_bytes;
+    if (h->storage == 3) P.rlay = make_reg_layout(h->npad, h->nb);
+    else P.lay = make_layout(h->npad, h->nunits, h->threads, h->upt, h->acc_bits / 8, h->storage);
     if (h->storage == 3 && P.mode == MODE_ALL_DELTAS) {
         // the full evaluator lives in the generic kernel; it keeps no per-search state
         kern = pick_kernel(32, 2, h->g_lb_class);
         threads = h->g_threads;
         P.upt = h->g_upt;
-        smem = make_layout(h->npad, h->nunits, threads, P.upt, 4, 2).total;
+        P.lay = make_layout(h->npad, h->nunits, threads, P.upt, 4, 2);
+        smem = P.lay.total;
     }
     // several handles share one kernel instantiation: (re)assert this launch's opt-in size
     CU(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

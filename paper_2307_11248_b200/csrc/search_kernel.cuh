@@ -33,34 +33,11 @@
 namespace qapb {
 
 enum { MODE_ALL_DELTAS = 0, MODE_TWO_OPT = 1, MODE_TABU = 2 };
-
-struct SearchParams {
-    int n, nb, npad, nunits, noff, upt;
-    int mode;        // MODE_*
-    int rng;         // 1: derive start permutation + tenures on the device (multistart)
-    int iterations;
-    int symmetric;
-    int force_seq_rng;  // test hook: take the sequential (rejection-exact) RNG path
-    const int32_t *F, *FT, *D, *DT;  // [npad*npad], zero diagonal, zero padded
-    const int32_t *fd, *dd;          // [npad] diagonals
-    const uint16_t *unit_ij;         // [nunits]  I | J<<8
-    const int64_t *perms;            // [B,n]            (rng == 0)
-    const int64_t *tenures;          // [B,iterations]   (tabu, rng == 0)
-    unsigned long long master_seed, first_index;
-    long long ten_lo, ten_hi;
-    int64_t *out_deltas;             // [B, n(n-1)/2]    (MODE_ALL_DELTAS)
-    int64_t *best, *best_cost, *cur, *cur_cost;
-    int64_t *cells;                  // [B,n,n] or null
-    int64_t *stopped, *steps;        // [B] or null
-    int64_t *tr_i, *tr_j, *tr_d, *tr_tabu;  // [B,iterations] or null
-    void *gM;                        // global placement matrices (storage >= 1)
-    void *gT;                        // global tabu triangles    (storage == 2)
-    unsigned long long gM_stride, gT_stride;  // elements per start
-};
+enum { TENURE_CHUNK = 256 };  // tenure draws precomputed per refill
 
 // ---- shared-memory layout, shared by host (size) and device (offsets) ------
 struct SmemLayout {
-    unsigned offM, offT, offA, offC, offB, offE, offH, offP, offU, offRedD, offRedK, offJ, offMisc;
+    unsigned offM, offT, offA, offC, offB, offE, offH, offP, offU, offRedD, offRedK, offJ, offMisc, offTen;
     unsigned total;
 };
 
@@ -89,9 +66,42 @@ __host__ __device__ inline SmemLayout make_layout(int npad, int nunits, int T, i
     L.offRedD = o; o += 32u * 8u;
     L.offRedK = o; o += 32u * 4u;
     L.offMisc = o; o += 64u;
+    L.offTen = o; o += 4u * TENURE_CHUNK;
     L.total = align16(o);
     return L;
 }
+
+struct RegLayout {
+    unsigned offA, offC, offB, offE, offH, offColR, offColS, offTR, offTS, offXR, offXS;
+    unsigned offP, offJ, offDM, offDT, offRedD, offRedK, offMisc, offTen, total;
+};
+
+struct SearchParams {
+    int n, nb, npad, nunits, noff, upt;
+    int mode;        // MODE_*
+    int rng;         // 1: derive start permutation + tenures on the device (multistart)
+    int iterations;
+    int symmetric;
+    int force_seq_rng;  // test hook: take the sequential (rejection-exact) RNG path
+    const int32_t *F, *FT, *D, *DT;  // [npad*npad], zero diagonal, zero padded
+    const int32_t *fd, *dd;          // [npad] diagonals
+    const uint16_t *unit_ij;         // [nunits]  I | J<<8
+    const int64_t *perms;            // [B,n]            (rng == 0)
+    const int64_t *tenures;          // [B,iterations]   (tabu, rng == 0)
+    unsigned long long master_seed, first_index;
+    long long ten_lo, ten_hi;
+    int64_t *out_deltas;             // [B, n(n-1)/2]    (MODE_ALL_DELTAS)
+    int64_t *best, *best_cost, *cur, *cur_cost;
+    int64_t *cells;                  // [B,n,n] or null
+    int64_t *stopped, *steps;        // [B] or null
+    int64_t *tr_i, *tr_j, *tr_d, *tr_tabu;  // [B,iterations] or null
+    void *gM;                        // global placement matrices (storage >= 1)
+    void *gT;                        // global tabu triangles    (storage == 2)
+    unsigned long long gM_stride, gT_stride;  // elements per start
+    long long *dbg;                  // optional phase-cycle counters (development), else null
+    SmemLayout lay;                  // generic kernel: offsets live in the constant bank
+    RegLayout rlay;                  // register-resident kernel
+};
 
 // ---- accumulator traits -----------------------------------------------------
 template <typename acc_t> struct Acc;
@@ -170,6 +180,37 @@ __device__ inline unsigned long long randbelow_seq(unsigned long long &state, un
         state += QAPB_GAMMA;
         unsigned long long r = mix64(state);
         if (r <= last_ok) return r % bound;
+    }
+}
+
+
+// Tenure stream (tabu.py:184-186), TENURE_CHUNK draws at a time: draw k of a chunk is
+// mix64(state + (k+1)*GAMMA), computed by thread k; if any draw would be rejected by
+// randbelow (probability ~ span/2^64) thread 0 replays the chunk with the exact
+// sequential rule.  Every thread keeps the stream state, so no 64-bit division sits on
+// the per-iteration critical path.  Must be called by all threads of the CTA.
+__device__ inline void fill_tenure_chunk(unsigned long long &state, long long lo, long long hi, int force_seq,
+                                         int32_t *sTen, long long *sMisc, int tid, int T)
+{
+    const unsigned long long span = (unsigned long long)(hi - lo + 1);
+    const unsigned long long last_ok = ~0ULL - (0ULL - span) % span;
+    int reject = force_seq;
+    for (int k = tid; k < TENURE_CHUNK; k += T) {
+        const unsigned long long r = mix64(state + QAPB_GAMMA * ((unsigned long long)k + 1ULL));
+        if (r > last_ok) reject = 1;
+        sTen[k] = (int32_t)(lo + (long long)(r % span));
+    }
+    reject = __syncthreads_or(reject);
+    if (reject) {
+        if (tid == 0) {
+            unsigned long long st = state;
+            for (int k = 0; k < TENURE_CHUNK; ++k) sTen[k] = (int32_t)(lo + (long long)randbelow_seq(st, span));
+            sMisc[3] = (long long)st;
+        }
+        __syncthreads();
+        state = (unsigned long long)sMisc[3];
+    } else {
+        state += QAPB_GAMMA * (unsigned long long)TENURE_CHUNK;
     }
 }
 
@@ -252,7 +293,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
     const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
     const int b = blockIdx.x;
     const int n = P.n, nb = P.nb, npad = P.npad, noff = P.noff, nunits = P.nunits, upt = P.upt;
-    const SmemLayout lay = make_layout(npad, nunits, T, upt, (int)sizeof(acc_t), STORAGE);
+    const SmemLayout &lay = P.lay;
 
     acc_t *M = STORAGE == 0 ? reinterpret_cast<acc_t *>(smem_raw + lay.offM)
                             : reinterpret_cast<acc_t *>(P.gM) + (size_t)b * P.gM_stride;
@@ -269,7 +310,8 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
     long long *sRed64 = reinterpret_cast<long long *>(smem_raw + lay.offRedD);  // 32 x 8 B
     acc_t *sRedD = reinterpret_cast<acc_t *>(smem_raw + lay.offRedD);
     unsigned *sRedK = reinterpret_cast<unsigned *>(smem_raw + lay.offRedK);
-    long long *sMisc = reinterpret_cast<long long *>(smem_raw + lay.offMisc);  // [0..1] tenure ring, [2] flags
+    long long *sMisc = reinterpret_cast<long long *>(smem_raw + lay.offMisc);
+    int32_t *sTen = reinterpret_cast<int32_t *>(smem_raw + lay.offTen);
 
     const int32_t *__restrict__ F = P.F;
     const int32_t *__restrict__ FT = P.FT;
@@ -315,8 +357,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                 }
                 rng_state = seed + QAPB_GAMMA * (unsigned long long)(n - 1);
             }
-            if (P.mode == MODE_TABU)  // tabu.py:184-186: tenure for iteration 1
-                sMisc[1] = P.ten_lo + (long long)randbelow_seq(rng_state, (unsigned long long)(P.ten_hi - P.ten_lo + 1));
+            sMisc[2] = (long long)rng_state;
         }
     }
     if (P.cells) {
@@ -324,6 +365,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
         for (int i = tid; i < n * n; i += T) cz[i] = 0;
     }
     __syncthreads();
+    if (P.rng) rng_state = (unsigned long long)sMisc[2];  // stream state after the shuffle, in every thread
 
     // full cost (_kernels.pyx:18-24), int64, including the diagonal products.
     long long cost;
@@ -458,7 +500,13 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
 
     for (int c = 1; c <= iters; ++c) {
         long long ten = 0;
-        if (tabu && !P.rng) ten = P.tenures[(size_t)b * iters + (c - 1)];  // consumed after the pass
+        if (tabu) {
+            if (!P.rng) {
+                ten = P.tenures[(size_t)b * iters + (c - 1)];  // consumed after the pass
+            } else if (((c - 1) & (TENURE_CHUNK - 1)) == 0) {
+                fill_tenure_chunk(rng_state, P.ten_lo, P.ten_hi, P.force_seq_rng, sTen, sMisc, tid, T);
+            }
+        }
 
         // ---- fused pass: rank-2 update, delta, admissibility, running argmin
         acc_t bd = MAXV;
@@ -582,7 +630,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
         const bool improved = cost < best_cost;
         if (improved) best_cost = cost;
         thr = Acc<acc_t>::clamp_thr(best_cost - cost);
-        if (tabu && P.rng) ten = sMisc[c & 1];
+        if (tabu && P.rng) ten = sTen[(c - 1) & (TENURE_CHUNK - 1)];
         steps_done = c;
 
         if (tid == 0) {
@@ -591,8 +639,6 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                 P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
                 if (P.tr_tabu) P.tr_tabu[o] = was_tabu;
             }
-            if (tabu && P.rng && c < iters)  // tenure of iteration c+1 (tabu.py:184-186)
-                sMisc[(c + 1) & 1] = P.ten_lo + (long long)randbelow_seq(rng_state, (unsigned long long)(P.ten_hi - P.ten_lo + 1));
         }
 
         // ---- prep: difference vectors (old permutation), h, rows/columns r,s

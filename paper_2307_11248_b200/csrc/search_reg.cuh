@@ -22,11 +22,6 @@
 
 namespace qapb {
 
-struct RegLayout {
-    unsigned offA, offC, offB, offE, offH, offColR, offColS, offTR, offTS, offXR, offXS;
-    unsigned offP, offJ, offDM, offDT, offRedD, offRedK, offMisc, total;
-};
-
 __host__ __device__ inline RegLayout make_reg_layout(int npad, int nb)
 {
     RegLayout L;
@@ -41,6 +36,7 @@ __host__ __device__ inline RegLayout make_reg_layout(int npad, int nb)
     L.offRedD = o; o += 32u * 8u;
     L.offRedK = o; o += 32u * 4u;
     L.offMisc = o; o += 64u;
+    L.offTen = o; o += 4u * TENURE_CHUNK;
     L.total = align16(o);
     return L;
 }
@@ -139,6 +135,14 @@ __device__ __forceinline__ void build_unit(const SearchParams &P, const int32_t 
         default: { constexpr int q = 3; BODY } break; \
     }
 
+// 16-way switch over slot = u*4+v; `qu`, `qv` are compile-time inside BODY.
+#define QAPB_SWITCH16(uu, vv, BODY)                                        \
+    QAPB_SWITCH4(uu, { constexpr int qu = q; switch (vv) {                 \
+        case 0: { constexpr int qv = 0; BODY } break;                     \
+        case 1: { constexpr int qv = 1; BODY } break;                     \
+        case 2: { constexpr int qv = 2; BODY } break;                     \
+        default: { constexpr int qv = 3; BODY } break; } })
+
 template <bool SYM, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const SearchParams P)
 {
@@ -147,7 +151,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
     const int b = blockIdx.x;
     const int n = P.n, nb = P.nb, npad = P.npad, noff = P.noff;
     const int Toff = T - 32;  // the last warp owns the diagonal blocks
-    const RegLayout lay = make_reg_layout(npad, nb);
+    const RegLayout &lay = P.rlay;
     int32_t *sA = reinterpret_cast<int32_t *>(smem_raw + lay.offA);
     int32_t *sC = reinterpret_cast<int32_t *>(smem_raw + lay.offC);
     int32_t *sB = reinterpret_cast<int32_t *>(smem_raw + lay.offB);
@@ -161,12 +165,11 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
     int32_t *sXS = reinterpret_cast<int32_t *>(smem_raw + lay.offXS);
     int32_t *sP = reinterpret_cast<int32_t *>(smem_raw + lay.offP);
     unsigned *sJ = reinterpret_cast<unsigned *>(smem_raw + lay.offJ);
-    int32_t *sDM = reinterpret_cast<int32_t *>(smem_raw + lay.offDM);  // [nb][4][4]
-    int32_t *sDT = reinterpret_cast<int32_t *>(smem_raw + lay.offDT);  // [nb][4][4]
     long long *sRed64 = reinterpret_cast<long long *>(smem_raw + lay.offRedD);
     int32_t *sRedD = reinterpret_cast<int32_t *>(smem_raw + lay.offRedD);
     unsigned *sRedK = reinterpret_cast<unsigned *>(smem_raw + lay.offRedK);
     long long *sMisc = reinterpret_cast<long long *>(smem_raw + lay.offMisc);
+    int32_t *sTen = reinterpret_cast<int32_t *>(smem_raw + lay.offTen);
 
     const int32_t *__restrict__ F = P.F;
     const int32_t *__restrict__ FT = P.FT;
@@ -206,8 +209,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
                 }
                 rng_state = seed + QAPB_GAMMA * (unsigned long long)(n - 1);
             }
-            if (P.mode == MODE_TABU)
-                sMisc[1] = P.ten_lo + (long long)randbelow_seq(rng_state, (unsigned long long)(P.ten_hi - P.ten_lo + 1));
+            sMisc[2] = (long long)rng_state;
         }
     }
     if (P.cells) {
@@ -215,6 +217,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
         for (int i = tid; i < n * n; i += T) cz[i] = 0;
     }
     __syncthreads();
+    if (P.rng) rng_state = (unsigned long long)sMisc[2];
 
     long long cost;
     {
@@ -241,24 +244,23 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
         sH[i] = acc;
     }
 
+    // Unit ownership.  Off-diagonal thread: U = block (I,J), L = block (J,I), E = tabu expiry of
+    // the 16 pairs.  Diagonal lane: I == J, U = the block itself (L unused), E valid for u < v.
     const bool offd = tid < noff;
-    const int dblk = tid - Toff;  // diagonal block index for the last warp
-    const bool diag = dblk >= 0 && dblk < nb;
+    const bool diag = tid >= Toff && (tid - Toff) < nb;
     int I = 0, J = 0;
     if (offd) { I = P.unit_ij[tid] & 0xff; J = P.unit_ij[tid] >> 8; }
+    if (diag) { I = tid - Toff; J = I; }
     int32_t U[4][4], L[4][4], E[4][4];
-    if (offd) {
+    if (offd || diag) {
         build_unit(P, sP, I, J, SYM, U, L, E);
-    } else if (diag) {
-        int32_t Ud[4][4], Ld[4][4], Ed[4][4];
-        build_unit(P, sP, dblk, dblk, SYM, Ud, Ld, Ed);
+        if (diag) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                sDM[dblk * 16 + u * 4 + v] = Ud[u][v];
-                sDT[dblk * 16 + u * 4 + v] = (u < v) ? Ed[u][v] : 0x7fffffff;
-            }
+                for (int v = 0; v < 4; ++v)
+                    if (u >= v) E[u][v] = 0x7fffffff;  // only pairs u < v exist in a diagonal block
+        }
     }
     __syncthreads();
 
@@ -272,16 +274,25 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
     for (int i = tid; i < n; i += T) best_out[i] = sP[i];
     int R = -1, S = -1, ru = 0, su = 0;  // previous move (block and in-block indices)
 
+    long long tacc[5] = {0, 0, 0, 0, 0};
+    const bool timing = P.dbg != nullptr && b == 0 && (tid == 0 || tid == 128 || tid == Toff);
     for (int c = 1; c <= iters; ++c) {
+        long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0;
+        if (timing) tA = clock64();
         long long ten = 0;
-        if (tabu && !P.rng) ten = P.tenures[(size_t)b * iters + (c - 1)];
+        if (tabu) {
+            if (!P.rng) {
+                ten = P.tenures[(size_t)b * iters + (c - 1)];
+            } else if (((c - 1) & (TENURE_CHUNK - 1)) == 0) {
+                fill_tenure_chunk(rng_state, P.ten_lo, P.ten_hi, P.force_seq_rng, sTen, sMisc, tid, T);
+            }
+        }
 
         int32_t my_d = MAXV;
-        int my_slot = 0, my_flag = 0;
-        unsigned my_key = 0xffffffffu;
+        int my_slot = 0;
         if (offd) {
             if (R >= 0) {
-                // ---- generic rank-2 update
+                // ---- generic rank-2 update (a is pre-doubled for symmetric instances)
                 int32_t aI[4], bI[4], aJ[4], bJ[4];
                 ld_vec4(sA, I, aI); ld_vec4(sB, I, bI); ld_vec4(sA, J, aJ); ld_vec4(sB, J, bJ);
                 if (SYM) {
@@ -339,69 +350,104 @@ _Pragma("unroll")
                     }
                 }
             }
-            // ---- delta, admissibility (_kernels.pyx:162), running first-minimum
+            // ---- delta, admissibility (_kernels.pyx:162), first minimum: four independent row
+            // chains (instruction-level parallelism), merged in row order so ties keep the
+            // lexicographically first pair.
             int32_t hI[4], hJ[4];
             ld_vec4(sH, I, hI);
             ld_vec4(sH, J, hJ);
+            int32_t rd[4];
+            int rs[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < 4; ++u) {
+                rd[u] = MAXV;
+                rs[u] = u * 4;
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
                     const int32_t d = U[u][v] + L[v][u] - hI[u] - hJ[v];
                     const bool adm = (E[u][v] <= c) || (d < thr);
-                    if (adm && d < my_d) { my_d = d; my_slot = u * 4 + v; }
+                    if (adm && d < rd[u]) { rd[u] = d; rs[u] = u * 4 + v; }
                 }
-            if (my_d != MAXV) {
-                my_flag = pick16(E, my_slot) > c ? 1 : 0;
-                my_key = pair_key(4 * I + (my_slot >> 2), 4 * J + (my_slot & 3), my_flag);
             }
+            if (rd[1] < rd[0]) { rd[0] = rd[1]; rs[0] = rs[1]; }
+            if (rd[3] < rd[2]) { rd[2] = rd[3]; rs[2] = rs[3]; }
+            if (rd[2] < rd[0]) { rd[0] = rd[2]; rs[0] = rs[2]; }
+            my_d = rd[0];
+            my_slot = rs[0];
         } else if (diag) {
-            int32_t *dm = sDM + dblk * 16;
             if (R >= 0) {
-                // special entries first (direct shared-memory addressing), then the generic rule
-                if (dblk == R) {
-                    for (int u = 0; u < 4; ++u)
-                        if (u != ru) dm[u * 4 + ru] = sColS[4 * R + u] + sTR[4 * R + u];
-                }
-                if (dblk == S) {
-                    for (int u = 0; u < 4; ++u)
-                        if (u != su) dm[u * 4 + su] = sColR[4 * S + u] + sTS[4 * S + u];
-                }
-                if (dblk == R) {
-                    for (int v = 0; v < 4; ++v)
-                        if (v != ru) dm[ru * 4 + v] += sXR[4 * R + v];
-                }
-                if (dblk == S) {
-                    for (int v = 0; v < 4; ++v)
-                        if (v != su) dm[su * 4 + v] += sXS[4 * S + v];
-                }
-                int32_t aI[4], bI[4], cI[4], eI[4];
-                ld_vec4(sA, dblk, aI); ld_vec4(sB, dblk, bI); ld_vec4(sC, dblk, cI); ld_vec4(sE, dblk, eI);
+                int32_t aI[4], bI[4];
+                ld_vec4(sA, I, aI); ld_vec4(sB, I, bI);
+                if (SYM) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                    for (int u = 0; u < 4; ++u)
 #pragma unroll
-                    for (int v = 0; v < 4; ++v)
-                        if (u != v) dm[u * 4 + v] -= SYM ? aI[u] * bI[v] : aI[u] * bI[v] + cI[u] * eI[v];
+                        for (int v = 0; v < 4; ++v)
+                            if (u != v) U[u][v] -= aI[u] * bI[v];
+                } else {
+                    int32_t cI[4], eI[4];
+                    ld_vec4(sC, I, cI); ld_vec4(sE, I, eI);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v)
+                            if (u != v) U[u][v] -= aI[u] * bI[v] + cI[u] * eI[v];
+                }
+                // rows / columns r and s inside this diagonal block: column assignments first,
+                // then the row increments (x is 0 at the corner positions)
+                if (I == R) {
+                    int32_t cs[4], t[4];
+                    ld_vec4(sColS, I, cs); ld_vec4(sTR, I, t);
+                    QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+                        for (int u = 0; u < 4; ++u) if (u != q) U[u][q] = cs[u] + t[u];
+                    })
+                }
+                if (I == S) {
+                    int32_t cr[4], t[4];
+                    ld_vec4(sColR, I, cr); ld_vec4(sTS, I, t);
+                    QAPB_SWITCH4(su, {
+_Pragma("unroll")
+                        for (int u = 0; u < 4; ++u) if (u != q) U[u][q] = cr[u] + t[u];
+                    })
+                }
+                if (I == R) {
+                    int32_t x[4];
+                    ld_vec4(sXR, I, x);
+                    QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+                        for (int v = 0; v < 4; ++v) if (v != q) U[q][v] += x[v];
+                    })
+                }
+                if (I == S) {
+                    int32_t x[4];
+                    ld_vec4(sXS, I, x);
+                    QAPB_SWITCH4(su, {
+_Pragma("unroll")
+                        for (int v = 0; v < 4; ++v) if (v != q) U[q][v] += x[v];
+                    })
+                }
             }
             int32_t hI[4];
-            ld_vec4(sH, dblk, hI);
+            ld_vec4(sH, I, hI);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
                 for (int v = u + 1; v < 4; ++v) {
-                    const int32_t d = dm[u * 4 + v] + dm[v * 4 + u] - hI[u] - hI[v];
-                    const int32_t ex = sDT[dblk * 16 + u * 4 + v];
-                    const bool adm = (ex <= c) || (d < thr);
-                    if (adm && d < my_d) { my_d = d; my_slot = u * 4 + v; my_flag = ex > c ? 1 : 0; }
+                    const int32_t d = U[u][v] + U[v][u] - hI[u] - hI[v];
+                    const bool adm = (E[u][v] <= c) || (d < thr);
+                    if (adm && d < my_d) { my_d = d; my_slot = u * 4 + v; }
                 }
-            if (my_d != MAXV) my_key = pair_key(4 * dblk + (my_slot >> 2), 4 * dblk + (my_slot & 3), my_flag);
         }
+        const unsigned my_key = (my_d != MAXV) ? pair_key(4 * I + (my_slot >> 2), 4 * J + (my_slot & 3), 0) : 0xffffffffu;
 
+        if (timing) tB = clock64();
         int32_t bd = my_d;
         unsigned bkey = my_key;
         warp_argmin(bd, bkey);
         if (lane == 0) { sRedD[warp] = bd; sRedK[warp] = bkey; }
         __syncthreads();  // ---------------------------------------------- sync #1
+        if (timing) tC = clock64();
         bd = lane < W ? sRedD[lane] : MAXV;
         bkey = lane < W ? sRedK[lane] : 0xffffffffu;
         warp_argmin(bd, bkey);
@@ -410,94 +456,104 @@ _Pragma("unroll")
             break;
         }
         const int r = (int)(bkey >> 17), s = (int)((bkey >> 1) & 0xffffu);
-        const int was_tabu = (int)(bkey & 1u);
         cost += (long long)bd;
         const bool improved = cost < best_cost;
         if (improved) best_cost = cost;
         thr = Acc<int32_t>::clamp_thr(best_cost - cost);
-        if (tabu && P.rng) ten = sMisc[c & 1];
+        if (tabu && P.rng) ten = sTen[(c - 1) & (TENURE_CHUNK - 1)];
         steps_done = c;
         R = r >> 2; S = s >> 2; ru = r & 3; su = s & 3;
-
-        if (tid == 0) {
-            if (P.tr_i) {
-                const size_t o = (size_t)b * iters + (c - 1);
-                P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
-                if (P.tr_tabu) P.tr_tabu[o] = was_tabu;
-            }
-            if (tabu && P.rng && c < iters)
-                sMisc[(c + 1) & 1] = P.ten_lo + (long long)randbelow_seq(rng_state, (unsigned long long)(P.ten_hi - P.ten_lo + 1));
-        }
-
         const int pr = sP[r], ps = sP[s];
-        const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
-        const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
+        if (timing) tD = clock64();
 
-        // ---- the thread owning the winning pair: corners, h[r], h[s], tabu memory
-        if (my_key == bkey && my_d != MAXV) {
-            int32_t mrs, msr;
-            if (offd) {
-                mrs = pick16(U, ru * 4 + su);
-                msr = pick16(L, su * 4 + ru);
-                if (tabu) put16(E, ru * 4 + su, (int32_t)(c + ten));
+        // ---- difference vectors of the move (old permutation), additive terms, h: thread i < n
+        if (tid < n) {
+            const int i = tid;
+            const int pi = sP[i];
+            const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
+            const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
+            const int32_t Dsi = D[s * npad + i], Dri = D[r * npad + i];
+            const int32_t Dis = DT[s * npad + i], Dir = DT[r * npad + i];
+            const int32_t Fpips = FT[ps * npad + pi], Fpipr = FT[pr * npad + pi];
+            const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
+            if (improved) best_out[i] = (i == r) ? ps : (i == s) ? pr : pi;
+            const bool mid = (i != r) && (i != s);
+            const int32_t a = mid ? Dis - Dir : 0, cc = mid ? Dsi - Dri : 0;
+            const int32_t bb = mid ? Fpips - Fpipr : 0, e = mid ? Fpspi - Fprpi : 0;
+            const int32_t be = bb + e;
+            sA[i] = SYM ? 2 * a : a;
+            sB[i] = bb;
+            if (!SYM) { sC[i] = cc; sE[i] = e; }
+            sXR[i] = -Drs * bb - Dsr * e + (mid ? Dri : 0) * be;
+            sXS[i] = Dsr * bb + Drs * e - (mid ? Dsi : 0) * be;
+            if (mid) {
+                sH[i] -= a * bb + cc * e;
+                sTR[i] = a * (Fpspr - (Fpips + Fpspi)) + cc * Fprps;
+                sTS[i] = a * ((Fpipr + Fprpi) - Fprps) - cc * Fpspr;
+            } else if (i == r) {
+                sTR[i] = 0;  // tS[r] is written by the owner of the pair
             } else {
-                mrs = sDM[R * 16 + ru * 4 + su];
-                msr = sDM[R * 16 + su * 4 + ru];
-                if (tabu) sDT[R * 16 + ru * 4 + su] = (int32_t)(c + ten);
+                sTS[i] = 0;  // tR[s] is written by the owner of the pair
+            }
+        }
+        // ---- the thread owning the winning pair: corners, h[r], h[s], tabu memory, trail
+        if (my_key == bkey) {
+            const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
+            const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
+            int32_t mrs = 0, msr = 0, old_exp = 0;
+            const int32_t new_exp = (int32_t)(c + ten);
+            if (offd) {
+                QAPB_SWITCH16(ru, su, {
+                    mrs = U[qu][qv]; msr = L[qv][qu]; old_exp = E[qu][qv];
+                    if (tabu) E[qu][qv] = new_exp;
+                })
+            } else {
+                QAPB_SWITCH16(ru, su, {
+                    mrs = U[qu][qv]; msr = U[qv][qu]; old_exp = E[qu][qv];
+                    if (tabu) E[qu][qv] = new_exp;
+                })
             }
             const int32_t hr = sH[r], hs = sH[s];
             sTS[r] = hr + (Drs - Dsr) * Fpspr;  // M'[r][s]
             sTR[s] = hs + (Dsr - Drs) * Fprps;  // M'[s][r]
             sH[r] = mrs + (Dsr - Drs) * Fprps;
             sH[s] = msr + (Drs - Dsr) * Fpspr;
+            if (P.tr_i) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
+                const size_t o = (size_t)b * iters + (c - 1);
+                P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
+                if (P.tr_tabu) P.tr_tabu[o] = old_exp > c ? 1 : 0;
+            }
             if (tabu && P.cells) {
                 int64_t *cz = P.cells + (size_t)b * n * n;
                 cz[(size_t)r * n + s] = (int64_t)c + ten;
                 cz[(size_t)s * n + r] += 1;
             }
         }
-        // ---- owners of columns r and s publish them
+        // ---- owners of columns r and s publish them (colR[r] = colS[s] = 0 by the diagonal lanes)
         if (offd) {
             if (J == R) { QAPB_SWITCH4(ru, { st_vec4(sColR, I, U[0][q], U[1][q], U[2][q], U[3][q]); }) }
             if (I == R) { QAPB_SWITCH4(ru, { st_vec4(sColR, J, L[0][q], L[1][q], L[2][q], L[3][q]); }) }
             if (J == S) { QAPB_SWITCH4(su, { st_vec4(sColS, I, U[0][q], U[1][q], U[2][q], U[3][q]); }) }
             if (I == S) { QAPB_SWITCH4(su, { st_vec4(sColS, J, L[0][q], L[1][q], L[2][q], L[3][q]); }) }
         } else if (diag) {
-            if (dblk == R)
-                for (int u = 0; u < 4; ++u) sColR[4 * R + u] = (u != ru) ? sDM[R * 16 + u * 4 + ru] : 0;
-            if (dblk == S)
-                for (int u = 0; u < 4; ++u) sColS[4 * S + u] = (u != su) ? sDM[S * 16 + u * 4 + su] : 0;
-        }
-        // ---- difference vectors of the move (old permutation), additive terms, h
-        for (int i = tid; i < n; i += T) {
-            const int pi = sP[i];
-            if (improved) best_out[i] = (i == r) ? ps : (i == s) ? pr : pi;
-            int32_t a = 0, cc = 0, bb = 0, e = 0, xr = 0, xs = 0, tr = 0, ts = 0;
-            if (i != r && i != s) {
-                const int32_t Dsi = D[s * npad + i], Dri = D[r * npad + i];
-                const int32_t Dis = DT[s * npad + i], Dir = DT[r * npad + i];
-                const int32_t Fpips = FT[ps * npad + pi], Fpipr = FT[pr * npad + pi];
-                const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
-                a = Dis - Dir; cc = Dsi - Dri; bb = Fpips - Fpipr; e = Fpspi - Fprpi;
-                const int32_t be = bb + e;
-                xr = -Drs * bb - Dsr * e + Dri * be;
-                xs = Dsr * bb + Drs * e - Dsi * be;
-                tr = a * (Fpspr - (Fpips + Fpspi)) + cc * Fprps;
-                ts = a * ((Fpipr + Fprpi) - Fprps) - cc * Fpspr;
-                sH[i] -= a * bb + cc * e;
-                sTR[i] = tr;
-                sTS[i] = ts;
-            } else if (i == r) {
-                sTR[i] = 0;  // tS[r] is written by the owner of the pair
-            } else {
-                sTS[i] = 0;  // tR[s] is written by the owner of the pair
+            if (I == R) {
+                QAPB_SWITCH4(ru, { st_vec4(sColR, I, q == 0 ? 0 : U[0][q], q == 1 ? 0 : U[1][q], q == 2 ? 0 : U[2][q], q == 3 ? 0 : U[3][q]); })
             }
-            sA[i] = SYM ? 2 * a : a;
-            sC[i] = cc; sB[i] = bb; sE[i] = e;
-            sXR[i] = xr; sXS[i] = xs;
+            if (I == S) {
+                QAPB_SWITCH4(su, { st_vec4(sColS, I, q == 0 ? 0 : U[0][q], q == 1 ? 0 : U[1][q], q == 2 ? 0 : U[2][q], q == 3 ? 0 : U[3][q]); })
+            }
         }
+        if (timing) tE = clock64();
         __syncthreads();  // ---------------------------------------------- sync #2
-        if (tid == 0) { const int32_t t = sP[r]; sP[r] = sP[s]; sP[s] = t; }
+        if (timing) {
+            const long long tF = clock64();
+            tacc[0] += tB - tA; tacc[1] += tC - tB; tacc[2] += tD - tC; tacc[3] += tE - tD; tacc[4] += tF - tE;
+        }
+        if (tid == 0) { sP[r] = ps; sP[s] = pr; }
+    }
+    if (timing) {
+        const int slot = tid == 0 ? 0 : (tid == 128 ? 1 : 2);
+        for (int q = 0; q < 5; ++q) P.dbg[slot * 5 + q] = tacc[q];
     }
     __syncthreads();
 

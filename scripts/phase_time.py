@@ -1,0 +1,27 @@
+"""Per-phase cycle counters of CTA 0 (development aid)."""
+import ctypes, sys
+sys.path.insert(0, ".")
+import numpy as np
+import paper_2307_11248_b200 as q
+from paper_2307_11248_b200 import shapes, _lib
+from paper_2307_11248_b200.backend import device_instance
+shape = sys.argv[1] if len(sys.argv) > 1 else "tai100a"
+starts = int(sys.argv[2]) if len(sys.argv) > 2 else 296
+iters = int(sys.argv[3]) if len(sys.argv) > 3 else 400
+algo = sys.argv[4] if len(sys.argv) > 4 else "tabu"
+inst = shapes.by_name(shape)
+di = device_instance(inst.flow, inst.distance)
+t = q.tenure_bounds(inst.n)
+L = _lib.lib()
+L.qapb_debug_phase_cycles.argtypes = [ctypes.c_void_p]
+buf = np.zeros(15, np.int64)
+di.multistart(algo, 0, 0, starts, iters, t.low, t.high)
+L.qapb_debug_phase_cycles(buf.ctypes.data)   # enable
+di.multistart(algo, 1, 0, starts, iters, t.low, t.high)
+ms = di.last_kernel_ms()
+L.qapb_debug_phase_cycles(buf.ctypes.data)   # read
+names = ["pass", "wait1", "reduce+book", "winner/publish/vector", "wait2"]
+print(f"{shape} starts={starts} iters={iters} {algo}: {ms:.3f} ms  ({ms*1e3/iters:.2f} us/iter)")
+for slot, who in enumerate(["thread0 (owner+vector)", "thread128 (owner)", "diag lane0"]):
+    v = buf[slot*5:(slot+1)*5] / iters
+    print(f"  {who:24s} " + "  ".join(f"{n}={x:7.0f}" for n, x in zip(names, v)) + f"   total={v.sum():.0f} clk/iter")
