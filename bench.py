@@ -23,7 +23,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -51,35 +50,45 @@ def executed_ops_per_eval(n: int, symmetric: bool) -> float:
 
 
 class ClockSampler(threading.Thread):
-    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled through NVML every ~2 ms during the timed region
+    (nvidia-smi itself takes tens of ms per query -- too coarse for a ~100 ms region)."""
 
     def __init__(self, index: int):
         super().__init__(daemon=True)
         self.index, self.samples, self._halt = index, [], threading.Event()
 
     def run(self):
-        while not self._halt.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
-                parts = [p.strip() for p in out.strip().split(",")]
-                if len(parts) >= 6:
-                    self.samples.append(parts)
-            except Exception:
-                pass
-            self._halt.wait(0.1)
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            while not self._halt.is_set():
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)))
+                self._halt.wait(0.002)
+        except Exception as exc:  # pragma: no cover
+            self.error = repr(exc)
 
     def stop(self) -> dict:
         self._halt.set()
         self.join(timeout=6)
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled: " + getattr(self, "error", "no samples")]}
+        import pynvml as nv
+
         sm = sorted(float(s[0]) for s in self.samples)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = [nm for k, nm in enumerate(names) if any(s[2 + k].lower().startswith("active") for s in self.samples)]
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.samples[0][1]), "reasons": reasons,
-                "samples": len(self.samples)}
+        bits = 0
+        for _, r in self.samples:
+            bits |= int(r)
+        names = {"hw_slowdown": nv.nvmlClocksThrottleReasonHwSlowdown,
+                 "hw_thermal_slowdown": nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+                 "sw_thermal_slowdown": nv.nvmlClocksThrottleReasonSwThermalSlowdown,
+                 "sw_power_cap": nv.nvmlClocksThrottleReasonSwPowerCap}
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": getattr(self, "max_mhz", None),
+                "reasons": [k for k, v in names.items() if bits & v], "samples": len(self.samples),
+                "how": "NVML, every ~2 ms over the timed region"}
 
 
 def _instance():
@@ -273,7 +282,7 @@ def run_ours(args) -> None:
         pk = _peaks()
         dram_bytes = _profile_traffic()
         roofline = {
-            "bound": "int_alu", "kernel": "qap_search_kernel",
+            "bound": "int_alu", "kernel": "qap_search_reg_kernel" if info["storage"] == 3 else "qap_search_kernel",
             "achieved": achieved / 1e12, "peak": int_peak / 1e12, "unit": "Tint-op/s",
             "frac": achieved / int_peak, "traffic": dram_bytes,
             "ops_per_eval": ops_survey, "ops_per_eval_source": "SURVEY.md 8(d) incremental evaluator",

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -42,6 +43,8 @@ struct qapb_handle {
     long long delta_bound = 0;
     int32_t *dF = nullptr, *dFT = nullptr, *dD = nullptr, *dDT = nullptr, *dfd = nullptr, *ddd = nullptr;
     uint16_t *dunit = nullptr;
+    void *arena = nullptr;  // one block holding all of the above
+    size_t arena_bytes = 0;
     void *ws = nullptr;
     size_t ws_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -86,18 +89,78 @@ extern "C" int qapb_device_count(int *count)
     return QAPB_OK;
 }
 
+// ---- process-wide device block cache --------------------------------------------------
+// cudaMalloc/cudaFree cost far more than a whole search launch on small instances, so
+// blocks released by qapb_destroy are kept (per device, bounded) and handed out again.
+namespace {
+struct Block { void *p; size_t bytes; int device; };
+std::mutex g_pool_mu;
+std::vector<Block> g_pool;
+size_t g_pool_bytes = 0;
+const size_t POOL_MAX_BYTES = (size_t)4 << 30;
+const size_t POOL_MAX_BLOCKS = 64;
+
+void *pool_alloc(int device, size_t need, size_t *got)
+{
+    need = (need + 65535) / 65536 * 65536;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        int best = -1;
+        for (int k = 0; k < (int)g_pool.size(); ++k)
+            if (g_pool[k].device == device && g_pool[k].bytes >= need && g_pool[k].bytes <= 2 * need + 65536 &&
+                (best < 0 || g_pool[k].bytes < g_pool[best].bytes))
+                best = k;
+        if (best >= 0) {
+            Block b = g_pool[best];
+            g_pool.erase(g_pool.begin() + best);
+            g_pool_bytes -= b.bytes;
+            *got = b.bytes;
+            return b.p;
+        }
+    }
+    void *p = nullptr;
+    if (cudaMalloc(&p, need) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    *got = need;
+    return p;
+}
+
+void pool_free(int device, void *p, size_t bytes)
+{
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.push_back({p, bytes, device});
+    g_pool_bytes += bytes;
+    while (g_pool.size() > POOL_MAX_BLOCKS || g_pool_bytes > POOL_MAX_BYTES) {
+        Block b = g_pool.front();
+        g_pool.erase(g_pool.begin());
+        g_pool_bytes -= b.bytes;
+        cudaSetDevice(b.device);
+        cudaFree(b.p);
+    }
+}
+
+// pinned host staging buffer for instance uploads (one copy per qapb_create)
+std::mutex g_stage_mu;
+void *g_stage = nullptr;
+size_t g_stage_bytes = 0;
+
+struct DevAttr { int valid = 0, sm_count = 0, smem_optin = 0; };
+DevAttr g_attr[64];
+}  // namespace
+
 static int ensure_ws(qapb_handle *h, size_t bytes)
 {
     if (bytes <= h->ws_bytes) return QAPB_OK;
-    if (h->ws) cudaFree(h->ws);
+    pool_free(h->device, h->ws, h->ws_bytes);
     h->ws = nullptr;
     h->ws_bytes = 0;
-    size_t want = bytes + bytes / 4 + 4096;
-    if (cudaMalloc(&h->ws, want) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(QAPB_ERR_NOMEM, "workspace allocation of " + std::to_string(want) + " bytes failed");
-    }
-    h->ws_bytes = want;
+    size_t want = bytes + bytes / 4 + 4096, got = 0;
+    h->ws = pool_alloc(h->device, want, &got);
+    if (!h->ws) return fail(QAPB_ERR_NOMEM, "workspace allocation of " + std::to_string(want) + " bytes failed");
+    h->ws_bytes = got;
     return QAPB_OK;
 }
 
@@ -182,10 +245,13 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     // units and CTA shape
     h->noff = nb * (nb - 1) / 2;
     h->nunits = h->noff + nb;
-    cudaDeviceProp prop;
-    CU(cudaGetDeviceProperties(&prop, device));
-    h->sm_count = prop.multiProcessorCount;
-    const unsigned smem_cap = (unsigned)prop.sharedMemPerBlockOptin;
+    if (device < 64 && !g_attr[device].valid) {
+        CU(cudaDeviceGetAttribute(&g_attr[device].sm_count, cudaDevAttrMultiProcessorCount, device));
+        CU(cudaDeviceGetAttribute(&g_attr[device].smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        g_attr[device].valid = 1;
+    }
+    h->sm_count = g_attr[device & 63].sm_count;
+    const unsigned smem_cap = (unsigned)g_attr[device & 63].smem_optin;
     const int acc_bytes = h->acc_bits / 8;
     int upt = (h->nunits + 383) / 384;
     if (upt < 1) upt = 1;
@@ -217,45 +283,59 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     }
     h->storage = storage;
 
-    // device copies
-    std::vector<int32_t> pF((size_t)npad * npad, 0), pFT((size_t)npad * npad, 0), pD((size_t)npad * npad, 0), pDT((size_t)npad * npad, 0);
-    std::vector<int32_t> pfd(npad, 0), pdd(npad, 0);
-    for (int i = 0; i < n; ++i) {
-        pfd[i] = (int32_t)fd[i];
-        pdd[i] = (int32_t)dd[i];
-        for (int j = 0; j < n; ++j) {
-            pF[(size_t)i * npad + j] = (int32_t)F0[(size_t)i * n + j];
-            pFT[(size_t)j * npad + i] = (int32_t)F0[(size_t)i * n + j];
-            pD[(size_t)i * npad + j] = (int32_t)D0[(size_t)i * n + j];
-            pDT[(size_t)j * npad + i] = (int32_t)D0[(size_t)i * n + j];
+    // device copies: one arena, filled in a pinned staging buffer and uploaded with one copy
+    const size_t mb = (size_t)npad * npad * sizeof(int32_t), vb = (size_t)npad * sizeof(int32_t);
+    const size_t ub = ((size_t)h->nunits * sizeof(uint16_t) + 15) / 16 * 16;
+    const size_t total = 4 * mb + 2 * vb + ub;
+    cudaError_t e = cudaSuccess;
+    h->arena = pool_alloc(device, total, &h->arena_bytes);
+    if (!h->arena) {
+        delete h;
+        return fail(QAPB_ERR_NOMEM, "instance allocation of " + std::to_string(total) + " bytes failed");
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_stage_mu);
+        if (g_stage_bytes < total) {
+            if (g_stage) cudaFreeHost(g_stage);
+            g_stage = nullptr;
+            g_stage_bytes = 0;
+            e = cudaHostAlloc(&g_stage, total + total / 2, cudaHostAllocDefault);
+            if (e == cudaSuccess) g_stage_bytes = total + total / 2;
+        }
+        if (e == cudaSuccess) {
+            memset(g_stage, 0, total);
+            int32_t *pF = (int32_t *)g_stage, *pFT = pF + (size_t)npad * npad, *pD = pFT + (size_t)npad * npad,
+                    *pDT = pD + (size_t)npad * npad, *pfd = pDT + (size_t)npad * npad, *pdd = pfd + npad;
+            uint16_t *units = (uint16_t *)(pdd + npad);
+            for (int i = 0; i < n; ++i) {
+                pfd[i] = (int32_t)fd[i];
+                pdd[i] = (int32_t)dd[i];
+                for (int j = 0; j < n; ++j) {
+                    const int32_t f = (int32_t)F0[(size_t)i * n + j], d = (int32_t)D0[(size_t)i * n + j];
+                    pF[(size_t)i * npad + j] = f;
+                    pFT[(size_t)j * npad + i] = f;
+                    pD[(size_t)i * npad + j] = d;
+                    pDT[(size_t)j * npad + i] = d;
+                }
+            }
+            int u = 0;
+            for (int I = 0; I < nb; ++I)
+                for (int J = I + 1; J < nb; ++J) units[u++] = (uint16_t)(I | (J << 8));
+            for (int I = 0; I < nb; ++I) units[u++] = (uint16_t)(I | (I << 8));
+            e = cudaMemcpy(h->arena, g_stage, total, cudaMemcpyHostToDevice);
         }
     }
-    std::vector<uint16_t> units(h->nunits);
-    {
-        int u = 0;
-        for (int I = 0; I < nb; ++I)
-            for (int J = I + 1; J < nb; ++J) units[u++] = (uint16_t)(I | (J << 8));
-        for (int I = 0; I < nb; ++I) units[u++] = (uint16_t)(I | (I << 8));
-    }
-    const size_t mb = (size_t)npad * npad * sizeof(int32_t);
-    auto up = [&](void **dst, const void *src, size_t bytes) -> cudaError_t {
-        cudaError_t e = cudaMalloc(dst, bytes);
-        if (e != cudaSuccess) return e;
-        return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
-    };
-    cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = up((void **)&h->dF, pF.data(), mb);
-    if (e == cudaSuccess) e = up((void **)&h->dFT, pFT.data(), mb);
-    if (e == cudaSuccess) e = up((void **)&h->dD, pD.data(), mb);
-    if (e == cudaSuccess) e = up((void **)&h->dDT, pDT.data(), mb);
-    if (e == cudaSuccess) e = up((void **)&h->dfd, pfd.data(), npad * sizeof(int32_t));
-    if (e == cudaSuccess) e = up((void **)&h->ddd, pdd.data(), npad * sizeof(int32_t));
-    if (e == cudaSuccess) e = up((void **)&h->dunit, units.data(), units.size() * sizeof(uint16_t));
+    h->dF = (int32_t *)h->arena;
+    h->dFT = h->dF + (size_t)npad * npad;
+    h->dD = h->dFT + (size_t)npad * npad;
+    h->dDT = h->dD + (size_t)npad * npad;
+    h->dfd = h->dDT + (size_t)npad * npad;
+    h->ddd = h->dfd + npad;
+    h->dunit = (uint16_t *)(h->ddd + npad);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
     kern_t kern = handle_kernel(h);
     if (e == cudaSuccess) e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, (const void *)kern, h->threads, h->smem_bytes);
     if (e != cudaSuccess) {
         std::string msg = std::string("instance upload failed: ") + cudaGetErrorString(e);
         qapb_destroy(h);
@@ -269,8 +349,10 @@ extern "C" int qapb_destroy(qapb_handle *h)
 {
     if (!h) return QAPB_OK;
     cudaSetDevice(h->device);
-    cudaFree(h->dF); cudaFree(h->dFT); cudaFree(h->dD); cudaFree(h->dDT);
-    cudaFree(h->dfd); cudaFree(h->ddd); cudaFree(h->dunit); cudaFree(h->ws);
+    // pending work on this handle's buffers must finish before another handle may reuse them
+    if (h->have_timing) cudaEventSynchronize(h->ev1);
+    pool_free(h->device, h->arena, h->arena_bytes);
+    pool_free(h->device, h->ws, h->ws_bytes);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     delete h;
@@ -280,6 +362,12 @@ extern "C" int qapb_destroy(qapb_handle *h)
 extern "C" int qapb_get_info(const qapb_handle *h, qapb_info *info)
 {
     if (!h || !info) return fail(QAPB_ERR_INVALID, "NULL argument");
+    if (h->ctas_per_sm == 0) {
+        qapb_handle *hm = const_cast<qapb_handle *>(h);
+        cudaSetDevice(h->device);
+        cudaFuncSetAttribute((const void *)handle_kernel(h), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hm->ctas_per_sm, (const void *)handle_kernel(h), h->threads, h->smem_bytes);
+    }
     info->n = h->n; info->device = h->device; info->acc_bits = h->acc_bits; info->symmetric = h->symmetric;
     info->threads = h->threads; info->units_per_thread = h->upt; info->storage = h->storage;
     info->smem_bytes = (int32_t)h->smem_bytes; info->ctas_per_sm = h->ctas_per_sm; info->sm_count = h->sm_count;
@@ -494,10 +582,17 @@ extern "C" int qapb_last_kernel_ms(qapb_handle *h, float *ms)
 
 // ------------------------------------------------------------ host variants --
 namespace {
-struct DevBuf {
+struct DevBuf {  // scratch from the block cache; released after the (synchronous) read-back
     void *p = nullptr;
-    ~DevBuf() { if (p) cudaFree(p); }
-    cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 1); }
+    size_t bytes = 0;
+    int device = 0;
+    ~DevBuf() { pool_free(device, p, bytes); }
+    cudaError_t alloc(size_t want)
+    {
+        cudaGetDevice(&device);
+        p = pool_alloc(device, want ? want : 1, &bytes);
+        return p ? cudaSuccess : cudaErrorMemoryAllocation;
+    }
     template <typename T> T *as() { return (T *)p; }
 };
 }  // namespace
@@ -597,14 +692,19 @@ extern "C" int qapb_multistart_host(qapb_handle *h, int algo, uint64_t master_se
     int rc = check_common(h, count);
     if (rc) return rc;
     if (!per_start_costs || !best_key || !best_perm) return fail(QAPB_ERR_INVALID, "NULL buffer");
-    DevBuf dc, dk, dp;
-    CU(dc.alloc((size_t)count * 8)); CU(dk.alloc(16)); CU(dp.alloc((size_t)h->n * 8));
-    rc = qapb_multistart(h, algo, master_seed, first_index, count, iterations, ten_low, ten_high, dc.as<int64_t>(),
-                         dk.as<int64_t>(), dp.as<int64_t>(), nullptr);
+    // one device block [costs | key | perm], one read-back
+    DevBuf out;
+    const size_t words = (size_t)count + 2 + (size_t)h->n;
+    CU(out.alloc(words * 8));
+    int64_t *d = out.as<int64_t>();
+    rc = qapb_multistart(h, algo, master_seed, first_index, count, iterations, ten_low, ten_high, d, d + count,
+                         d + count + 2, nullptr);
     if (rc) return rc;
-    D2H(per_start_costs, dc.p, (size_t)count * 8);
-    D2H(best_key, dk.p, 16);
-    D2H(best_perm, dp.p, (size_t)h->n * 8);
+    std::vector<int64_t> host(words);
+    D2H(host.data(), d, words * 8);
+    memcpy(per_start_costs, host.data(), (size_t)count * 8);
+    memcpy(best_key, host.data() + count, 16);
+    memcpy(best_perm, host.data() + count + 2, (size_t)h->n * 8);
     return QAPB_OK;
 }
 
