@@ -68,16 +68,21 @@ static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
     return tab[acc_bits == 64][storage][lb_class];
 }
 
-static kern_t pick_reg_kernel(int symmetric, int lb_class)
+static kern_t pick_reg_kernel(int symmetric, int packed, int lb_class)
 {
-#define KR(S, MT, MB) (kern_t) qap_search_reg_kernel<S, MT, MB>
-    static kern_t tab[2][2] = {{KR(false, 352, 2), KR(false, 544, 1)}, {KR(true, 352, 2), KR(true, 544, 1)}};
+#define KR(S, PK, MT, MB) (kern_t) qap_search_reg_kernel<S, PK, MT, MB>
+    static kern_t tab[2][2][2] = {
+        {{KR(false, false, 352, 2), KR(false, false, 544, 1)}, {KR(false, true, 352, 2), KR(false, true, 544, 1)}},
+        {{KR(true, false, 352, 2), KR(true, false, 544, 1)}, {KR(true, true, 352, 2), KR(true, true, 544, 1)}}};
 #undef KR
-    return tab[symmetric != 0][lb_class];
+    return tab[symmetric != 0][packed != 0][lb_class];
 }
 static kern_t handle_kernel(const qapb_handle *h)
 {
-    return h->storage == 3 ? pick_reg_kernel(h->symmetric, h->lb_class) : pick_kernel(h->acc_bits, h->storage, h->lb_class);
+    // packed (delta, slot) keys need |delta|*16 + 15 < 2^31
+    const int packed = h->delta_bound < ((1LL << 27) - 1);
+    return h->storage == 3 ? pick_reg_kernel(h->symmetric, packed, h->lb_class)
+                           : pick_kernel(h->acc_bits, h->storage, h->lb_class);
 }
 
 extern "C" int qapb_version(void) { return 1; }
@@ -399,6 +404,8 @@ static void base_params(const qapb_handle *h, SearchParams &P)
     P.n = h->n; P.nb = h->nb; P.npad = h->npad; P.nunits = h->nunits; P.noff = h->noff; P.upt = h->upt;
     P.symmetric = h->symmetric;
     P.force_seq_rng = h->force_seq_rng;
+    P.one = 1;
+    P.sixteen = 16;
     P.F = h->dF; P.FT = h->dFT; P.D = h->dD; P.DT = h->dDT; P.fd = h->dfd; P.dd = h->ddd;
     P.unit_ij = h->dunit;
     P.dbg = g_dbg;

@@ -83,6 +83,7 @@ struct SearchParams {
     int iterations;
     int symmetric;
     int force_seq_rng;  // test hook: take the sequential (rejection-exact) RNG path
+    int one, sixteen;   // runtime constants 1 and 16: multiplying by them keeps adds/shifts on the FMA (IMAD) pipe
     const int32_t *F, *FT, *D, *DT;  // [npad*npad], zero diagonal, zero padded
     const int32_t *fd, *dd;          // [npad] diagonals
     const uint16_t *unit_ij;         // [nunits]  I | J<<8

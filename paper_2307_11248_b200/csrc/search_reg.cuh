@@ -143,7 +143,7 @@ __device__ __forceinline__ void build_unit(const SearchParams &P, const int32_t 
         case 2: { constexpr int qv = 2; BODY } break;                     \
         default: { constexpr int qv = 3; BODY } break; } })
 
-template <bool SYM, int MAXT, int MINB>
+template <bool SYM, bool PACKED, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const SearchParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
     const int32_t *__restrict__ D = P.D;
     const int32_t *__restrict__ DT = P.DT;
     const int32_t MAXV = 0x7fffffff;
+    const int one = P.one, sixteen = P.sixteen;
 
     // ---------------------------------------------------------------- setup
     for (int i = tid; i < npad; i += T) {
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
     int R = -1, S = -1, ru = 0, su = 0;  // previous move (block and in-block indices)
 
     long long tacc[5] = {0, 0, 0, 0, 0};
+    long long psub[3] = {0, 0, 0};
     const bool timing = P.dbg != nullptr && b == 0 && (tid == 0 || tid == 128 || tid == Toff);
     for (int c = 1; c <= iters; ++c) {
         long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0;
@@ -290,6 +292,8 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
 
         int32_t my_d = MAXV;
         int my_slot = 0;
+        long long q0 = 0, q1 = 0, q2 = 0;
+        if (timing) q0 = clock64();
         if (offd) {
             if (R >= 0) {
                 // ---- generic rank-2 update (a is pre-doubled for symmetric instances)
@@ -314,6 +318,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
                             L[v][u] -= aJ[v] * bI[u] + cJ[v] * eI[u];
                         }
                 }
+                if (timing) q1 = clock64();
                 // ---- rows / columns r and s of the previous move
                 if (I == R || J == R || I == S || J == S) {
                     if (I == R) {
@@ -350,30 +355,51 @@ _Pragma("unroll")
                     }
                 }
             }
-            // ---- delta, admissibility (_kernels.pyx:162), first minimum: four independent row
-            // chains (instruction-level parallelism), merged in row order so ties keep the
-            // lexicographically first pair.
+            if (timing) q2 = clock64();
+            // ---- delta, admissibility (_kernels.pyx:162), first minimum.  The ALU pipe (IADD3 /
+            // ISETP / IMNMX, half rate) is the binding resource of this pass, so the first add of
+            // each delta and the (delta, slot) packing are written as multiplications by the
+            // runtime constants 1 and 16: they issue as IMAD on the otherwise idle FMA pipe.
             int32_t hI[4], hJ[4];
             ld_vec4(sH, I, hI);
             ld_vec4(sH, J, hJ);
-            int32_t rd[4];
-            int rs[4];
+            if (PACKED) {
+                // |delta| < 2^27 (host-proven): key = delta*16 + slot orders by (delta, slot), so the
+                // running first-minimum is one predicated IMNMX per pair; four independent chains.
+                int32_t km[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                rd[u] = MAXV;
-                rs[u] = u * 4;
+                for (int u = 0; u < 4; ++u) {
+                    km[u] = MAXV;
 #pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const int32_t d = U[u][v] + L[v][u] - hI[u] - hJ[v];
-                    const bool adm = (E[u][v] <= c) || (d < thr);
-                    if (adm && d < rd[u]) { rd[u] = d; rs[u] = u * 4 + v; }
+                    for (int v = 0; v < 4; ++v) {
+                        const int32_t d = (U[u][v] * one + L[v][u]) - hI[u] - hJ[v];
+                        const bool adm = (E[u][v] <= c) || (d < thr);
+                        const int32_t kd = (int32_t)((uint32_t)d * (uint32_t)sixteen + (uint32_t)(u * 4 + v));
+                        if (adm) km[u] = min(km[u], kd);
+                    }
                 }
+                const int32_t m = min(min(km[0], km[1]), min(km[2], km[3]));
+                if (m != MAXV) { my_d = m >> 4; my_slot = m & 15; }
+            } else {
+                int32_t rd[4];
+                int rs[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    rd[u] = MAXV;
+                    rs[u] = u * 4;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const int32_t d = (U[u][v] * one + L[v][u]) - hI[u] - hJ[v];
+                        const bool adm = (E[u][v] <= c) || (d < thr);
+                        if (adm && d < rd[u]) { rd[u] = d; rs[u] = u * 4 + v; }
+                    }
+                }
+                if (rd[1] < rd[0]) { rd[0] = rd[1]; rs[0] = rs[1]; }
+                if (rd[3] < rd[2]) { rd[2] = rd[3]; rs[2] = rs[3]; }
+                if (rd[2] < rd[0]) { rd[0] = rd[2]; rs[0] = rs[2]; }
+                my_d = rd[0];
+                my_slot = rs[0];
             }
-            if (rd[1] < rd[0]) { rd[0] = rd[1]; rs[0] = rs[1]; }
-            if (rd[3] < rd[2]) { rd[2] = rd[3]; rs[2] = rs[3]; }
-            if (rd[2] < rd[0]) { rd[0] = rd[2]; rs[0] = rs[2]; }
-            my_d = rd[0];
-            my_slot = rs[0];
         } else if (diag) {
             if (R >= 0) {
                 int32_t aI[4], bI[4];
@@ -441,7 +467,7 @@ _Pragma("unroll")
         }
         const unsigned my_key = (my_d != MAXV) ? pair_key(4 * I + (my_slot >> 2), 4 * J + (my_slot & 3), 0) : 0xffffffffu;
 
-        if (timing) tB = clock64();
+        if (timing) { tB = clock64(); psub[0] += q1 - q0; psub[1] += q2 - q1; psub[2] += tB - q2; }
         int32_t bd = my_d;
         unsigned bkey = my_key;
         warp_argmin(bd, bkey);
@@ -470,30 +496,53 @@ _Pragma("unroll")
         if (tid < n) {
             const int i = tid;
             const int pi = sP[i];
-            const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
-            const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
-            const int32_t Dsi = D[s * npad + i], Dri = D[r * npad + i];
-            const int32_t Dis = DT[s * npad + i], Dir = DT[r * npad + i];
-            const int32_t Fpips = FT[ps * npad + pi], Fpipr = FT[pr * npad + pi];
-            const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
-            if (improved) best_out[i] = (i == r) ? ps : (i == s) ? pr : pi;
             const bool mid = (i != r) && (i != s);
-            const int32_t a = mid ? Dis - Dir : 0, cc = mid ? Dsi - Dri : 0;
-            const int32_t bb = mid ? Fpips - Fpipr : 0, e = mid ? Fpspi - Fprpi : 0;
-            const int32_t be = bb + e;
-            sA[i] = SYM ? 2 * a : a;
-            sB[i] = bb;
-            if (!SYM) { sC[i] = cc; sE[i] = e; }
-            sXR[i] = -Drs * bb - Dsr * e + (mid ? Dri : 0) * be;
-            sXS[i] = Dsr * bb + Drs * e - (mid ? Dsi : 0) * be;
-            if (mid) {
-                sH[i] -= a * bb + cc * e;
-                sTR[i] = a * (Fpspr - (Fpips + Fpspi)) + cc * Fprps;
-                sTS[i] = a * ((Fpipr + Fprpi) - Fprps) - cc * Fpspr;
-            } else if (i == r) {
-                sTR[i] = 0;  // tS[r] is written by the owner of the pair
+            if (improved) best_out[i] = (i == r) ? ps : (i == s) ? pr : pi;
+            if (SYM) {
+                // D = D^T, F = F^T: a = c, b = e, and the closed forms collapse
+                const int32_t Drs = D[r * npad + s], Fpspr = F[ps * npad + pr];
+                const int32_t Dsi = D[s * npad + i], Dri = D[r * npad + i];
+                const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
+                const int32_t a = mid ? Dsi - Dri : 0, bb = mid ? Fpspi - Fprpi : 0;
+                const int32_t a2 = 2 * a, b2 = 2 * bb;
+                sA[i] = a2;
+                sB[i] = bb;
+                sXR[i] = b2 * ((mid ? Dri : 0) - Drs);
+                sXS[i] = b2 * (Drs - (mid ? Dsi : 0));
+                if (mid) {
+                    sH[i] -= a2 * bb;
+                    sTR[i] = a2 * (Fpspr - Fpspi);
+                    sTS[i] = a2 * (Fprpi - Fpspr);
+                } else if (i == r) {
+                    sTR[i] = 0;  // tS[r] is written by the owner of the pair
+                } else {
+                    sTS[i] = 0;  // tR[s] is written by the owner of the pair
+                }
             } else {
-                sTS[i] = 0;  // tR[s] is written by the owner of the pair
+                const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
+                const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
+                const int32_t Dsi = D[s * npad + i], Dri = D[r * npad + i];
+                const int32_t Dis = DT[s * npad + i], Dir = DT[r * npad + i];
+                const int32_t Fpips = FT[ps * npad + pi], Fpipr = FT[pr * npad + pi];
+                const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
+                const int32_t a = mid ? Dis - Dir : 0, cc = mid ? Dsi - Dri : 0;
+                const int32_t bb = mid ? Fpips - Fpipr : 0, e = mid ? Fpspi - Fprpi : 0;
+                const int32_t be = bb + e;
+                sA[i] = a;
+                sB[i] = bb;
+                sC[i] = cc;
+                sE[i] = e;
+                sXR[i] = -Drs * bb - Dsr * e + (mid ? Dri : 0) * be;
+                sXS[i] = Dsr * bb + Drs * e - (mid ? Dsi : 0) * be;
+                if (mid) {
+                    sH[i] -= a * bb + cc * e;
+                    sTR[i] = a * (Fpspr - (Fpips + Fpspi)) + cc * Fprps;
+                    sTS[i] = a * ((Fpipr + Fprpi) - Fprps) - cc * Fpspr;
+                } else if (i == r) {
+                    sTR[i] = 0;
+                } else {
+                    sTS[i] = 0;
+                }
             }
         }
         // ---- the thread owning the winning pair: corners, h[r], h[s], tabu memory, trail
@@ -554,6 +603,7 @@ _Pragma("unroll")
     if (timing) {
         const int slot = tid == 0 ? 0 : (tid == 128 ? 1 : 2);
         for (int q = 0; q < 5; ++q) P.dbg[slot * 5 + q] = tacc[q];
+        if (tid == 128) for (int q = 0; q < 3; ++q) P.dbg[10 + q] = psub[q];  // overwrites the diag slot's first entries
     }
     __syncthreads();
 
