@@ -68,20 +68,20 @@ static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
     return tab[acc_bits == 64][storage][lb_class];
 }
 
-static kern_t pick_reg_kernel(int symmetric, int packed, int lb_class)
+static kern_t pick_reg_kernel(int symmetric, int packed, int upt)
 {
-#define KR(S, PK, MT, MB) (kern_t) qap_search_reg_kernel<S, PK, MT, MB>
-    static kern_t tab[2][2][2] = {
-        {{KR(false, false, 352, 2), KR(false, false, 544, 1)}, {KR(false, true, 352, 2), KR(false, true, 544, 1)}},
-        {{KR(true, false, 352, 2), KR(true, false, 544, 1)}, {KR(true, true, 352, 2), KR(true, true, 544, 1)}}};
+    // one register budget for both shapes: 112 registers/thread (2 CTAs x 288 threads, or 3 x 192)
+#define KR(S, PK, UP) (kern_t) qap_search_reg_kernel<S, PK, UP, (UP == 2 ? 104 : 80)>
+    static kern_t tab[2][2][2] = {{{KR(false, false, 1), KR(false, false, 2)}, {KR(false, true, 1), KR(false, true, 2)}},
+                                  {{KR(true, false, 1), KR(true, false, 2)}, {KR(true, true, 1), KR(true, true, 2)}}};
 #undef KR
-    return tab[symmetric != 0][packed != 0][lb_class];
+    return tab[symmetric != 0][packed != 0][upt - 1];
 }
 static kern_t handle_kernel(const qapb_handle *h)
 {
     // packed (delta, slot) keys need |delta|*16 + 15 < 2^31
     const int packed = h->delta_bound < ((1LL << 27) - 1);
-    return h->storage == 3 ? pick_reg_kernel(h->symmetric, packed, h->lb_class)
+    return h->storage == 3 ? pick_reg_kernel(h->symmetric, packed, h->upt)
                            : pick_kernel(h->acc_bits, h->storage, h->lb_class);
 }
 
@@ -271,10 +271,12 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     const char *force = getenv("QAPB_FORCE_GENERIC");
     if (h->acc_bits == 32 && nb <= 32 && !(force && force[0] == '1')) {
         // register-resident plan: one thread per off-diagonal unit + one warp for the diagonal blocks
+        // (two units per thread once there are enough of them: fewer threads -> fewer overhead
+        // registers per search -> more resident searches per SM)
         storage = 3;
-        h->upt = 1;
-        h->threads = (h->noff + 31) / 32 * 32 + 32;
-        h->lb_class = h->threads <= 352 ? 0 : 1;
+        h->upt = 1;  // UPT = 2 halves the threads but CTAs are charged registers in 4-warp granules: no occupancy gain
+        h->threads = ((h->noff + h->upt - 1) / h->upt + 31) / 32 * 32 + 32;
+        h->lb_class = 0;
         h->smem_bytes = make_reg_layout(npad, nb).total;
     } else {
         for (; storage < 3; ++storage) {

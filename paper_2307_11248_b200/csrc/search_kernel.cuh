@@ -73,7 +73,7 @@ __host__ __device__ inline SmemLayout make_layout(int npad, int nunits, int T, i
 
 struct RegLayout {
     unsigned offA, offC, offB, offE, offH, offColR, offColS, offTR, offTS, offXR, offXS;
-    unsigned offP, offJ, offDM, offDT, offRedD, offRedK, offMisc, offTen, total;
+    unsigned offP, offJ, offDM, offDT, offRedD, offRedK, offMisc, offTen, offExp, total;
 };
 
 struct SearchParams {

@@ -2,8 +2,9 @@
 //
 // Same algorithm and the same integers as qap_search_kernel (search_kernel.cuh), but the
 // placement matrix M and the tabu triangle never leave the register file: thread t < noff
-// owns off-diagonal unit t = block pair {(I,J),(J,I)} as 32 + 16 registers for the whole
-// run, so the per-iteration pass is pure ALU work (rank-2 update, delta, admissibility,
+// owns one or two off-diagonal units (block pairs {(I,J),(J,I)}, 32 registers each) plus a
+// 16-bit mask of their currently-tabu pairs for the whole run (expiry iterations live in a
+// shared-memory array that is only touched when a pair is set or expires), so the per-iteration pass is pure ALU work (rank-2 update, delta, admissibility,
 // running argmin) fed by a handful of 128-bit shared-memory vector loads.  The last warp
 // owns the nb diagonal 4x4 blocks, kept in shared memory.
 //
@@ -37,6 +38,7 @@ __host__ __device__ inline RegLayout make_reg_layout(int npad, int nb)
     L.offRedK = o; o += 32u * 4u;
     L.offMisc = o; o += 64u;
     L.offTen = o; o += 4u * TENURE_CHUNK;
+    L.offExp = o; o += 64u * (unsigned)(nb * (nb - 1) / 2 + nb);  // tabu expiry per (unit, slot)
     L.total = align16(o);
     return L;
 }
@@ -135,16 +137,10 @@ __device__ __forceinline__ void build_unit(const SearchParams &P, const int32_t 
         default: { constexpr int q = 3; BODY } break; \
     }
 
-// 16-way switch over slot = u*4+v; `qu`, `qv` are compile-time inside BODY.
-#define QAPB_SWITCH16(uu, vv, BODY)                                        \
-    QAPB_SWITCH4(uu, { constexpr int qu = q; switch (vv) {                 \
-        case 0: { constexpr int qv = 0; BODY } break;                     \
-        case 1: { constexpr int qv = 1; BODY } break;                     \
-        case 2: { constexpr int qv = 2; BODY } break;                     \
-        default: { constexpr int qv = 3; BODY } break; } })
 
-template <bool SYM, bool PACKED, int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const SearchParams P)
+// Upper bound (exclusive) on unit ids handled by off-diagonal threads: uid = t + k*Toff.
+template <bool SYM, bool PACKED, int UPT, int MAXREG>
+__global__ void __maxnreg__(MAXREG) qap_search_reg_kernel(const SearchParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
@@ -170,6 +166,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
     unsigned *sRedK = reinterpret_cast<unsigned *>(smem_raw + lay.offRedK);
     long long *sMisc = reinterpret_cast<long long *>(smem_raw + lay.offMisc);
     int32_t *sTen = reinterpret_cast<int32_t *>(smem_raw + lay.offTen);
+    int32_t *sExp = reinterpret_cast<int32_t *>(smem_raw + lay.offExp);  // [unit][16] expiry iteration
 
     const int32_t *__restrict__ F = P.F;
     const int32_t *__restrict__ FT = P.FT;
@@ -245,22 +242,36 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
         sH[i] = acc;
     }
 
-    // Unit ownership.  Off-diagonal thread: U = block (I,J), L = block (J,I), E = tabu expiry of
-    // the 16 pairs.  Diagonal lane: I == J, U = the block itself (L unused), E valid for u < v.
-    const bool offd = tid < noff;
+    // Unit ownership.  Off-diagonal thread t owns units t + k*Toff (k < UPT): U = block (I,J),
+    // L = block (J,I).  Diagonal lane: one unit, I == J, U = the block itself (L unused), pairs u < v.
+    // tb = mask of pairs that are tabu now (pads and non-pairs permanently set), mexp = earliest
+    // expiry among the clearable bits.
     const bool diag = tid >= Toff && (tid - Toff) < nb;
-    int I = 0, J = 0;
-    if (offd) { I = P.unit_ij[tid] & 0xff; J = P.unit_ij[tid] >> 8; }
-    if (diag) { I = tid - Toff; J = I; }
-    int32_t U[4][4], L[4][4], E[4][4];
-    if (offd || diag) {
-        build_unit(P, sP, I, J, SYM, U, L, E);
-        if (diag) {
+    int I[UPT], J[UPT], uidv[UPT];
+    bool own[UPT];
+    int32_t U[UPT][4][4], L[UPT][4][4];
+    unsigned tb[UPT];
+    int32_t mexp[UPT];
+#pragma unroll
+    for (int k = 0; k < UPT; ++k) {
+        const int uid = tid + k * Toff;
+        own[k] = (tid < Toff) && (uid < noff);
+        I[k] = 0; J[k] = 0; uidv[k] = 0; tb[k] = 0xffffu; mexp[k] = MAXV;
+        if (own[k]) { I[k] = P.unit_ij[uid] & 0xff; J[k] = P.unit_ij[uid] >> 8; uidv[k] = uid; }
+        if (k == 0 && diag) { I[0] = tid - Toff; J[0] = I[0]; uidv[0] = noff + I[0]; own[0] = true; }
+        if (own[k]) {
+            int32_t Ex[4][4];
+            build_unit(P, sP, I[k], J[k], SYM, U[k], L[k], Ex);
+            unsigned m = 0;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v)
-                    if (u >= v) E[u][v] = 0x7fffffff;  // only pairs u < v exist in a diagonal block
+                for (int v = 0; v < 4; ++v) {
+                    const bool dead = (Ex[u][v] != 0) || (diag && u >= v);  // pad pair or not a pair
+                    if (dead) m |= 1u << (u * 4 + v);
+                    sExp[uidv[k] * 16 + u * 4 + v] = dead ? MAXV : 0;
+                }
+            tb[k] = m;
         }
     }
     __syncthreads();
@@ -275,12 +286,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
     for (int i = tid; i < n; i += T) best_out[i] = sP[i];
     int R = -1, S = -1, ru = 0, su = 0;  // previous move (block and in-block indices)
 
-    long long tacc[5] = {0, 0, 0, 0, 0};
-    long long psub[3] = {0, 0, 0};
-    const bool timing = P.dbg != nullptr && b == 0 && (tid == 0 || tid == 128 || tid == Toff);
     for (int c = 1; c <= iters; ++c) {
-        long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0;
-        if (timing) tA = clock64();
         long long ten = 0;
         if (tabu) {
             if (!P.rng) {
@@ -291,189 +297,212 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_reg_kernel(const Search
         }
 
         int32_t my_d = MAXV;
-        int my_slot = 0;
-        long long q0 = 0, q1 = 0, q2 = 0;
-        if (timing) q0 = clock64();
-        if (offd) {
-            if (R >= 0) {
-                // ---- generic rank-2 update (a is pre-doubled for symmetric instances)
-                int32_t aI[4], bI[4], aJ[4], bJ[4];
-                ld_vec4(sA, I, aI); ld_vec4(sB, I, bI); ld_vec4(sA, J, aJ); ld_vec4(sB, J, bJ);
-                if (SYM) {
+        unsigned my_key = 0xffffffffu;
+        int my_k = 0, my_slot = 0;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) {
-                            U[u][v] -= aI[u] * bJ[v];
-                            L[v][u] -= aJ[v] * bI[u];
-                        }
-                } else {
-                    int32_t cI[4], eI[4], cJ[4], eJ[4];
-                    ld_vec4(sC, I, cI); ld_vec4(sE, I, eI); ld_vec4(sC, J, cJ); ld_vec4(sE, J, eJ);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) {
-                            U[u][v] -= aI[u] * bJ[v] + cI[u] * eJ[v];
-                            L[v][u] -= aJ[v] * bI[u] + cJ[v] * eI[u];
-                        }
+        for (int k = 0; k < UPT; ++k) {
+            if (!own[k]) continue;
+            const int Ik = I[k], Jk = J[k];
+            // expire tabu bits (rare: only when the earliest expiry of this unit is reached)
+            if (c >= mexp[k]) {
+                unsigned bits = tb[k];
+                int32_t nm = MAXV;
+                while (bits) {
+                    const int q = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    const int32_t e = sExp[uidv[k] * 16 + q];
+                    if (e <= c) tb[k] &= ~(1u << q);
+                    else if (e != MAXV) nm = min(nm, e);
                 }
-                if (timing) q1 = clock64();
-                // ---- rows / columns r and s of the previous move
-                if (I == R || J == R || I == S || J == S) {
-                    if (I == R) {
-                        int32_t x[4], cs[4], t[4];
-                        ld_vec4(sXR, J, x); ld_vec4(sColS, J, cs); ld_vec4(sTR, J, t);
-                        QAPB_SWITCH4(ru, {
-_Pragma("unroll")
-                            for (int v = 0; v < 4; ++v) { U[q][v] += x[v]; L[v][q] = cs[v] + t[v]; }
-                        })
-                    }
-                    if (J == R) {
-                        int32_t x[4], cs[4], t[4];
-                        ld_vec4(sXR, I, x); ld_vec4(sColS, I, cs); ld_vec4(sTR, I, t);
-                        QAPB_SWITCH4(ru, {
-_Pragma("unroll")
-                            for (int u = 0; u < 4; ++u) { L[q][u] += x[u]; U[u][q] = cs[u] + t[u]; }
-                        })
-                    }
-                    if (I == S) {
-                        int32_t x[4], cr[4], t[4];
-                        ld_vec4(sXS, J, x); ld_vec4(sColR, J, cr); ld_vec4(sTS, J, t);
-                        QAPB_SWITCH4(su, {
-_Pragma("unroll")
-                            for (int v = 0; v < 4; ++v) { U[q][v] += x[v]; L[v][q] = cr[v] + t[v]; }
-                        })
-                    }
-                    if (J == S) {
-                        int32_t x[4], cr[4], t[4];
-                        ld_vec4(sXS, I, x); ld_vec4(sColR, I, cr); ld_vec4(sTS, I, t);
-                        QAPB_SWITCH4(su, {
-_Pragma("unroll")
-                            for (int u = 0; u < 4; ++u) { L[q][u] += x[u]; U[u][q] = cr[u] + t[u]; }
-                        })
-                    }
-                }
+                mexp[k] = nm;
             }
-            if (timing) q2 = clock64();
-            // ---- delta, admissibility (_kernels.pyx:162), first minimum.  The ALU pipe (IADD3 /
-            // ISETP / IMNMX, half rate) is the binding resource of this pass, so the first add of
-            // each delta and the (delta, slot) packing are written as multiplications by the
-            // runtime constants 1 and 16: they issue as IMAD on the otherwise idle FMA pipe.
-            int32_t hI[4], hJ[4];
-            ld_vec4(sH, I, hI);
-            ld_vec4(sH, J, hJ);
-            if (PACKED) {
-                // |delta| < 2^27 (host-proven): key = delta*16 + slot orders by (delta, slot), so the
-                // running first-minimum is one predicated IMNMX per pair; four independent chains.
-                int32_t km[4];
+            int32_t kd_best = MAXV;  // PACKED: delta*16+slot; else plain delta
+            int slot_best = 0;
+            if (Ik != Jk) {
+                if (R >= 0) {
+                    // ---- generic rank-2 update (a is pre-doubled for symmetric instances)
+                    int32_t aI[4], bI[4], aJ[4], bJ[4];
+                    ld_vec4(sA, Ik, aI); ld_vec4(sB, Ik, bI); ld_vec4(sA, Jk, aJ); ld_vec4(sB, Jk, bJ);
+                    if (SYM) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    km[u] = MAXV;
+                        for (int u = 0; u < 4; ++u)
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const int32_t d = (U[u][v] * one + L[v][u]) - hI[u] - hJ[v];
-                        const bool adm = (E[u][v] <= c) || (d < thr);
-                        const int32_t kd = (int32_t)((uint32_t)d * (uint32_t)sixteen + (uint32_t)(u * 4 + v));
-                        if (adm) km[u] = min(km[u], kd);
+                            for (int v = 0; v < 4; ++v) {
+                                U[k][u][v] -= aI[u] * bJ[v];
+                                L[k][v][u] -= aJ[v] * bI[u];
+                            }
+                    } else {
+                        int32_t cI[4], eI[4], cJ[4], eJ[4];
+                        ld_vec4(sC, Ik, cI); ld_vec4(sE, Ik, eI); ld_vec4(sC, Jk, cJ); ld_vec4(sE, Jk, eJ);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                U[k][u][v] -= aI[u] * bJ[v] + cI[u] * eJ[v];
+                                L[k][v][u] -= aJ[v] * bI[u] + cJ[v] * eI[u];
+                            }
+                    }
+                    // ---- rows / columns r and s of the previous move
+                    if (Ik == R || Jk == R || Ik == S || Jk == S) {
+                        if (Ik == R) {
+                            int32_t x[4], cs[4], t[4];
+                            ld_vec4(sXR, Jk, x); ld_vec4(sColS, Jk, cs); ld_vec4(sTR, Jk, t);
+                            QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+                                for (int v = 0; v < 4; ++v) { U[k][q][v] += x[v]; L[k][v][q] = cs[v] + t[v]; }
+                            })
+                        }
+                        if (Jk == R) {
+                            int32_t x[4], cs[4], t[4];
+                            ld_vec4(sXR, Ik, x); ld_vec4(sColS, Ik, cs); ld_vec4(sTR, Ik, t);
+                            QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+                                for (int u = 0; u < 4; ++u) { L[k][q][u] += x[u]; U[k][u][q] = cs[u] + t[u]; }
+                            })
+                        }
+                        if (Ik == S) {
+                            int32_t x[4], cr[4], t[4];
+                            ld_vec4(sXS, Jk, x); ld_vec4(sColR, Jk, cr); ld_vec4(sTS, Jk, t);
+                            QAPB_SWITCH4(su, {
+_Pragma("unroll")
+                                for (int v = 0; v < 4; ++v) { U[k][q][v] += x[v]; L[k][v][q] = cr[v] + t[v]; }
+                            })
+                        }
+                        if (Jk == S) {
+                            int32_t x[4], cr[4], t[4];
+                            ld_vec4(sXS, Ik, x); ld_vec4(sColR, Ik, cr); ld_vec4(sTS, Ik, t);
+                            QAPB_SWITCH4(su, {
+_Pragma("unroll")
+                                for (int u = 0; u < 4; ++u) { L[k][q][u] += x[u]; U[k][u][q] = cr[u] + t[u]; }
+                            })
+                        }
                     }
                 }
-                const int32_t m = min(min(km[0], km[1]), min(km[2], km[3]));
-                if (m != MAXV) { my_d = m >> 4; my_slot = m & 15; }
+                // ---- delta, admissibility (_kernels.pyx:162), first minimum.  The ALU pipe (IADD3 /
+                // ISETP / IMNMX, half rate) is the busiest pipe of this pass, so the first add of each
+                // delta and the (delta, slot) packing are multiplications by the runtime constants 1
+                // and 16: they issue as IMAD on the FMA pipe.
+                int32_t hI[4], hJ[4];
+                ld_vec4(sH, Ik, hI);
+                ld_vec4(sH, Jk, hJ);
+                const unsigned tbk = tb[k];
+                if (PACKED) {
+                    int32_t km[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        km[u] = MAXV;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            const int32_t d = (U[k][u][v] * one + L[k][v][u]) - hI[u] - hJ[v];
+                            const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
+                            const int32_t kd = (int32_t)((uint32_t)d * (uint32_t)sixteen + (uint32_t)(u * 4 + v));
+                            if (adm) km[u] = min(km[u], kd);
+                        }
+                    }
+                    kd_best = min(min(km[0], km[1]), min(km[2], km[3]));
+                } else {
+                    int32_t rd[4];
+                    int rs[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        rd[u] = MAXV;
+                        rs[u] = u * 4;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            const int32_t d = (U[k][u][v] * one + L[k][v][u]) - hI[u] - hJ[v];
+                            const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
+                            if (adm && d < rd[u]) { rd[u] = d; rs[u] = u * 4 + v; }
+                        }
+                    }
+                    if (rd[1] < rd[0]) { rd[0] = rd[1]; rs[0] = rs[1]; }
+                    if (rd[3] < rd[2]) { rd[2] = rd[3]; rs[2] = rs[3]; }
+                    if (rd[2] < rd[0]) { rd[0] = rd[2]; rs[0] = rs[2]; }
+                    kd_best = rd[0];
+                    slot_best = rs[0];
+                }
             } else {
-                int32_t rd[4];
-                int rs[4];
+                // ---- diagonal block
+                if (R >= 0) {
+                    int32_t aI[4], bI[4];
+                    ld_vec4(sA, Ik, aI); ld_vec4(sB, Ik, bI);
+                    if (SYM) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    rd[u] = MAXV;
-                    rs[u] = u * 4;
+                        for (int u = 0; u < 4; ++u)
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const int32_t d = (U[u][v] * one + L[v][u]) - hI[u] - hJ[v];
-                        const bool adm = (E[u][v] <= c) || (d < thr);
-                        if (adm && d < rd[u]) { rd[u] = d; rs[u] = u * 4 + v; }
+                            for (int v = 0; v < 4; ++v)
+                                if (u != v) U[k][u][v] -= aI[u] * bI[v];
+                    } else {
+                        int32_t cI[4], eI[4];
+                        ld_vec4(sC, Ik, cI); ld_vec4(sE, Ik, eI);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int v = 0; v < 4; ++v)
+                                if (u != v) U[k][u][v] -= aI[u] * bI[v] + cI[u] * eI[v];
+                    }
+                    // column assignments first, then the row increments (x is 0 at the corners)
+                    if (Ik == R) {
+                        int32_t cs[4], t[4];
+                        ld_vec4(sColS, Ik, cs); ld_vec4(sTR, Ik, t);
+                        QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+                            for (int u = 0; u < 4; ++u) if (u != q) U[k][u][q] = cs[u] + t[u];
+                        })
+                    }
+                    if (Ik == S) {
+                        int32_t cr[4], t[4];
+                        ld_vec4(sColR, Ik, cr); ld_vec4(sTS, Ik, t);
+                        QAPB_SWITCH4(su, {
+_Pragma("unroll")
+                            for (int u = 0; u < 4; ++u) if (u != q) U[k][u][q] = cr[u] + t[u];
+                        })
+                    }
+                    if (Ik == R) {
+                        int32_t x[4];
+                        ld_vec4(sXR, Ik, x);
+                        QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+                            for (int v = 0; v < 4; ++v) if (v != q) U[k][q][v] += x[v];
+                        })
+                    }
+                    if (Ik == S) {
+                        int32_t x[4];
+                        ld_vec4(sXS, Ik, x);
+                        QAPB_SWITCH4(su, {
+_Pragma("unroll")
+                            for (int v = 0; v < 4; ++v) if (v != q) U[k][q][v] += x[v];
+                        })
                     }
                 }
-                if (rd[1] < rd[0]) { rd[0] = rd[1]; rs[0] = rs[1]; }
-                if (rd[3] < rd[2]) { rd[2] = rd[3]; rs[2] = rs[3]; }
-                if (rd[2] < rd[0]) { rd[0] = rd[2]; rs[0] = rs[2]; }
-                my_d = rd[0];
-                my_slot = rs[0];
+                int32_t hI[4];
+                ld_vec4(sH, Ik, hI);
+                const unsigned tbk = tb[k];
+                int32_t bdv = MAXV;
+                int bsl = 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = u + 1; v < 4; ++v) {
+                        const int32_t d = U[k][u][v] + U[k][v][u] - hI[u] - hI[v];
+                        const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
+                        if (adm && d < bdv) { bdv = d; bsl = u * 4 + v; }
+                    }
+                if (PACKED) kd_best = (bdv == MAXV) ? MAXV : (int32_t)((uint32_t)bdv * 16u + (uint32_t)bsl);
+                else { kd_best = bdv; slot_best = bsl; }
             }
-        } else if (diag) {
-            if (R >= 0) {
-                int32_t aI[4], bI[4];
-                ld_vec4(sA, I, aI); ld_vec4(sB, I, bI);
-                if (SYM) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int v = 0; v < 4; ++v)
-                            if (u != v) U[u][v] -= aI[u] * bI[v];
-                } else {
-                    int32_t cI[4], eI[4];
-                    ld_vec4(sC, I, cI); ld_vec4(sE, I, eI);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int v = 0; v < 4; ++v)
-                            if (u != v) U[u][v] -= aI[u] * bI[v] + cI[u] * eI[v];
-                }
-                // rows / columns r and s inside this diagonal block: column assignments first,
-                // then the row increments (x is 0 at the corner positions)
-                if (I == R) {
-                    int32_t cs[4], t[4];
-                    ld_vec4(sColS, I, cs); ld_vec4(sTR, I, t);
-                    QAPB_SWITCH4(ru, {
-_Pragma("unroll")
-                        for (int u = 0; u < 4; ++u) if (u != q) U[u][q] = cs[u] + t[u];
-                    })
-                }
-                if (I == S) {
-                    int32_t cr[4], t[4];
-                    ld_vec4(sColR, I, cr); ld_vec4(sTS, I, t);
-                    QAPB_SWITCH4(su, {
-_Pragma("unroll")
-                        for (int u = 0; u < 4; ++u) if (u != q) U[u][q] = cr[u] + t[u];
-                    })
-                }
-                if (I == R) {
-                    int32_t x[4];
-                    ld_vec4(sXR, I, x);
-                    QAPB_SWITCH4(ru, {
-_Pragma("unroll")
-                        for (int v = 0; v < 4; ++v) if (v != q) U[q][v] += x[v];
-                    })
-                }
-                if (I == S) {
-                    int32_t x[4];
-                    ld_vec4(sXS, I, x);
-                    QAPB_SWITCH4(su, {
-_Pragma("unroll")
-                        for (int v = 0; v < 4; ++v) if (v != q) U[q][v] += x[v];
-                    })
-                }
+            if (kd_best != MAXV) {
+                const int32_t dk = PACKED ? (kd_best >> 4) : kd_best;
+                const int sk = PACKED ? (kd_best & 15) : slot_best;
+                const unsigned key = pair_key(4 * Ik + (sk >> 2), 4 * Jk + (sk & 3), 0);
+                if (dk < my_d || (dk == my_d && key < my_key)) { my_d = dk; my_key = key; my_k = k; my_slot = sk; }
             }
-            int32_t hI[4];
-            ld_vec4(sH, I, hI);
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = u + 1; v < 4; ++v) {
-                    const int32_t d = U[u][v] + U[v][u] - hI[u] - hI[v];
-                    const bool adm = (E[u][v] <= c) || (d < thr);
-                    if (adm && d < my_d) { my_d = d; my_slot = u * 4 + v; }
-                }
         }
-        const unsigned my_key = (my_d != MAXV) ? pair_key(4 * I + (my_slot >> 2), 4 * J + (my_slot & 3), 0) : 0xffffffffu;
 
-        if (timing) { tB = clock64(); psub[0] += q1 - q0; psub[1] += q2 - q1; psub[2] += tB - q2; }
         int32_t bd = my_d;
         unsigned bkey = my_key;
         warp_argmin(bd, bkey);
         if (lane == 0) { sRedD[warp] = bd; sRedK[warp] = bkey; }
         __syncthreads();  // ---------------------------------------------- sync #1
-        if (timing) tC = clock64();
         bd = lane < W ? sRedD[lane] : MAXV;
         bkey = lane < W ? sRedK[lane] : 0xffffffffu;
         warp_argmin(bd, bkey);
@@ -490,7 +519,6 @@ _Pragma("unroll")
         steps_done = c;
         R = r >> 2; S = s >> 2; ru = r & 3; su = s & 3;
         const int pr = sP[r], ps = sP[s];
-        if (timing) tD = clock64();
 
         // ---- difference vectors of the move (old permutation), additive terms, h: thread i < n
         if (tid < n) {
@@ -549,18 +577,20 @@ _Pragma("unroll")
         if (my_key == bkey) {
             const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
             const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
-            int32_t mrs = 0, msr = 0, old_exp = 0;
-            const int32_t new_exp = (int32_t)(c + ten);
-            if (offd) {
-                QAPB_SWITCH16(ru, su, {
-                    mrs = U[qu][qv]; msr = L[qv][qu]; old_exp = E[qu][qv];
-                    if (tabu) E[qu][qv] = new_exp;
-                })
-            } else {
-                QAPB_SWITCH16(ru, su, {
-                    mrs = U[qu][qv]; msr = U[qv][qu]; old_exp = E[qu][qv];
-                    if (tabu) E[qu][qv] = new_exp;
-                })
+            int32_t mrs = 0, msr = 0;
+            unsigned was = 0;
+#pragma unroll
+            for (int k = 0; k < UPT; ++k) {
+                if (k != my_k) continue;
+                mrs = pick16(U[k], ru * 4 + su);
+                msr = (I[k] != J[k]) ? pick16(L[k], su * 4 + ru) : pick16(U[k], su * 4 + ru);
+                was = (tb[k] >> my_slot) & 1u;
+                if (tabu) {
+                    const int32_t new_exp = (int32_t)(c + ten);
+                    tb[k] |= 1u << my_slot;
+                    mexp[k] = min(mexp[k], new_exp);
+                    sExp[uidv[k] * 16 + my_slot] = new_exp;
+                }
             }
             const int32_t hr = sH[r], hs = sH[s];
             sTS[r] = hr + (Drs - Dsr) * Fpspr;  // M'[r][s]
@@ -570,7 +600,7 @@ _Pragma("unroll")
             if (P.tr_i) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
                 const size_t o = (size_t)b * iters + (c - 1);
                 P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
-                if (P.tr_tabu) P.tr_tabu[o] = old_exp > c ? 1 : 0;
+                if (P.tr_tabu) P.tr_tabu[o] = (int64_t)was;
             }
             if (tabu && P.cells) {
                 int64_t *cz = P.cells + (size_t)b * n * n;
@@ -579,31 +609,26 @@ _Pragma("unroll")
             }
         }
         // ---- owners of columns r and s publish them (colR[r] = colS[s] = 0 by the diagonal lanes)
-        if (offd) {
-            if (J == R) { QAPB_SWITCH4(ru, { st_vec4(sColR, I, U[0][q], U[1][q], U[2][q], U[3][q]); }) }
-            if (I == R) { QAPB_SWITCH4(ru, { st_vec4(sColR, J, L[0][q], L[1][q], L[2][q], L[3][q]); }) }
-            if (J == S) { QAPB_SWITCH4(su, { st_vec4(sColS, I, U[0][q], U[1][q], U[2][q], U[3][q]); }) }
-            if (I == S) { QAPB_SWITCH4(su, { st_vec4(sColS, J, L[0][q], L[1][q], L[2][q], L[3][q]); }) }
-        } else if (diag) {
-            if (I == R) {
-                QAPB_SWITCH4(ru, { st_vec4(sColR, I, q == 0 ? 0 : U[0][q], q == 1 ? 0 : U[1][q], q == 2 ? 0 : U[2][q], q == 3 ? 0 : U[3][q]); })
-            }
-            if (I == S) {
-                QAPB_SWITCH4(su, { st_vec4(sColS, I, q == 0 ? 0 : U[0][q], q == 1 ? 0 : U[1][q], q == 2 ? 0 : U[2][q], q == 3 ? 0 : U[3][q]); })
+#pragma unroll
+        for (int k = 0; k < UPT; ++k) {
+            if (!own[k]) continue;
+            const int Ik = I[k], Jk = J[k];
+            if (Ik != Jk) {
+                if (Jk == R) { QAPB_SWITCH4(ru, { st_vec4(sColR, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]); }) }
+                if (Ik == R) { QAPB_SWITCH4(ru, { st_vec4(sColR, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]); }) }
+                if (Jk == S) { QAPB_SWITCH4(su, { st_vec4(sColS, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]); }) }
+                if (Ik == S) { QAPB_SWITCH4(su, { st_vec4(sColS, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]); }) }
+            } else {
+                if (Ik == R) {
+                    QAPB_SWITCH4(ru, { st_vec4(sColR, Ik, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
+                }
+                if (Ik == S) {
+                    QAPB_SWITCH4(su, { st_vec4(sColS, Ik, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
+                }
             }
         }
-        if (timing) tE = clock64();
         __syncthreads();  // ---------------------------------------------- sync #2
-        if (timing) {
-            const long long tF = clock64();
-            tacc[0] += tB - tA; tacc[1] += tC - tB; tacc[2] += tD - tC; tacc[3] += tE - tD; tacc[4] += tF - tE;
-        }
         if (tid == 0) { sP[r] = ps; sP[s] = pr; }
-    }
-    if (timing) {
-        const int slot = tid == 0 ? 0 : (tid == 128 ? 1 : 2);
-        for (int q = 0; q < 5; ++q) P.dbg[slot * 5 + q] = tacc[q];
-        if (tid == 128) for (int q = 0; q < 3; ++q) P.dbg[10 + q] = psub[q];  // overwrites the diag slot's first entries
     }
     __syncthreads();
 

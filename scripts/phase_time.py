@@ -22,6 +22,7 @@ ms = di.last_kernel_ms()
 L.qapb_debug_phase_cycles(buf.ctypes.data)   # read
 names = ["pass", "wait1", "reduce+book", "winner/publish/vector", "wait2"]
 print(f"{shape} starts={starts} iters={iters} {algo}: {ms:.3f} ms  ({ms*1e3/iters:.2f} us/iter)")
+print("  thread0 S split: vector=%.0f winner=%.0f (publish = rest)" % tuple(buf[13:15] / iters))
 print("  thread128 pass split: update=%.0f special=%.0f select=%.0f" % tuple(buf[10:13] / iters))
 for slot, who in enumerate(["thread0 (owner+vector)", "thread128 (owner)"]):
     v = buf[slot*5:(slot+1)*5] / iters
