@@ -6,7 +6,7 @@
 // per thread, where the placement matrix lives), workspace and launches.
 #include "../../include/qapb.h"
 #include "search_kernel.cuh"
-#include "search_reg.cuh"
+#include "search_hybrid.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -37,7 +37,8 @@ struct qapb_handle {
     int acc_bits = 32, symmetric = 0;
     int nunits = 0, noff = 0, threads = 0, upt = 0, storage = 0;
     int lb_class = 0;  // 0: <=384 threads, 2 CTAs/SM register budget; 1: <=512 threads
-    int g_threads = 0, g_upt = 0, g_lb_class = 0;  // generic-kernel plan (all_deltas on register-resident handles)
+    int g_threads = 0, g_upt = 0, g_lb_class = 0;  // generic-kernel plan (all_deltas on hybrid handles)
+    int toff = 0, us = 0, exp_in_smem = 1;         // hybrid plan
     unsigned smem_bytes = 0;
     int ctas_per_sm = 0, sm_count = 0;
     long long delta_bound = 0;
@@ -68,21 +69,57 @@ static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
     return tab[acc_bits == 64][storage][lb_class];
 }
 
-static kern_t pick_reg_kernel(int symmetric, int packed, int upt)
+static kern_t pick_hybrid_kernel(int symmetric, int packed, int ur, int smemu)
 {
-    // one register budget for both shapes: 112 registers/thread (2 CTAs x 288 threads, or 3 x 192)
-#define KR(S, PK, UP) (kern_t) qap_search_reg_kernel<S, PK, UP, (UP == 2 ? 104 : 80)>
-    static kern_t tab[2][2][2] = {{{KR(false, false, 1), KR(false, false, 2)}, {KR(false, true, 1), KR(false, true, 2)}},
-                                  {{KR(true, false, 1), KR(true, false, 2)}, {KR(true, true, 1), KR(true, true, 2)}}};
-#undef KR
-    return tab[symmetric != 0][packed != 0][upt - 1];
+    // register-only plans (n <= 128): 80 registers/thread, two 352-thread CTAs per SM at n = 100;
+    // plans with shared-memory units: 128 registers/thread (one 512-thread CTA per SM at n = 256)
+#define KH(S, PK, UP, SM) (kern_t) qap_search_hybrid_kernel<S, PK, UP, SM, (SM ? 128 : (UP == 2 ? 104 : 80))>
+#define KH4(S, PK) {{KH(S, PK, 1, false), KH(S, PK, 1, true)}, {KH(S, PK, 2, false), KH(S, PK, 2, true)}}
+    static kern_t tab[2][2][2][2] = {{KH4(false, false), KH4(false, true)}, {KH4(true, false), KH4(true, true)}};
+#undef KH4
+#undef KH
+    return tab[symmetric != 0][packed != 0][ur - 1][smemu != 0];
 }
 static kern_t handle_kernel(const qapb_handle *h)
 {
     // packed (delta, slot) keys need |delta|*16 + 15 < 2^31
     const int packed = h->delta_bound < ((1LL << 27) - 1);
-    return h->storage == 3 ? pick_reg_kernel(h->symmetric, packed, h->upt)
+    return h->storage == 3 ? pick_hybrid_kernel(h->symmetric, packed, h->upt, h->us > 0)
                            : pick_kernel(h->acc_bits, h->storage, h->lb_class);
+}
+
+// Split of the off-diagonal units of one search between registers (UR per thread) and shared
+// memory (US per thread) for the hybrid kernel.  Returns false if the instance does not fit.
+static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
+{
+    const int nb = h->nb, noff = h->noff, dw = (nb + 31) / 32;
+    int ur = 1, toff = (noff + 31) / 32 * 32, us = 0;
+    if (nb > 32) {                 // n <= 256: two register units per thread, the rest in shared memory
+        ur = 2;
+        toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
+        us = std::max(0, (noff - ur * toff + toff - 1) / toff);
+    }
+    if (const char *pl = getenv("QAPB_PLAN")) {  // development override: "UR,Toff,US"
+        int a, b, c;
+        if (sscanf(pl, "%d,%d,%d", &a, &b, &c) == 3 && (a == 1 || a == 2) && b % 32 == 0 && b >= 0 && c >= 0 &&
+            (long long)(a + c) * b >= noff)
+            ur = a, toff = b, us = c;
+    }
+    const int threads = toff + 32 * dw;
+    if (threads > 1024 || (us > 0 && threads > 512) || (us == 0 && ur == 2 && threads > 608)) return false;
+    int exp_in_smem = 1;
+    HybLayout L = make_hyb_layout(h->npad, nb, toff, us, 1);
+    // keep the expiry array in shared memory only while it does not cost a resident CTA
+    if (L.total > smem_cap && us > 0) {
+        exp_in_smem = 0;
+        L = make_hyb_layout(h->npad, nb, toff, us, 0);
+    }
+    if (L.total > smem_cap) return false;
+    h->upt = ur; h->toff = toff; h->us = us; h->exp_in_smem = exp_in_smem;
+    h->threads = threads;
+    h->lb_class = 0;
+    h->smem_bytes = L.total;
+    return true;
 }
 
 extern "C" int qapb_version(void) { return 1; }
@@ -269,16 +306,11 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     h->g_threads = threads; h->g_upt = upt; h->g_lb_class = h->lb_class;
     int storage = 0;
     const char *force = getenv("QAPB_FORCE_GENERIC");
-    if (h->acc_bits == 32 && nb <= 32 && !(force && force[0] == '1')) {
-        // register-resident plan: one thread per off-diagonal unit + one warp for the diagonal blocks
-        // (two units per thread once there are enough of them: fewer threads -> fewer overhead
-        // registers per search -> more resident searches per SM)
+    if (h->acc_bits == 32 && nb <= 64 && !(force && force[0] == '1') && plan_hybrid(h, smem_cap)) {
         storage = 3;
-        h->upt = 1;  // UPT = 2 halves the threads but CTAs are charged registers in 4-warp granules: no occupancy gain
-        h->threads = ((h->noff + h->upt - 1) / h->upt + 31) / 32 * 32 + 32;
-        h->lb_class = 0;
-        h->smem_bytes = make_reg_layout(npad, nb).total;
     } else {
+        const char *fs = getenv("QAPB_FORCE_STORAGE");  // development: 1 or 2
+        if (fs && (fs[0] == '1' || fs[0] == '2')) storage = fs[0] - '0';
         for (; storage < 3; ++storage) {
             SmemLayout L = make_layout(npad, h->nunits, threads, upt, acc_bytes, storage);
             if (L.total <= smem_cap) { h->smem_bytes = L.total; break; }
@@ -425,17 +457,21 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     if ((h->storage == 1 || h->storage == 2) && P.mode != MODE_ALL_DELTAS) need += m_elems * acc_bytes * batch;
     size_t offT = need;
     if (h->storage == 2 && P.mode != MODE_ALL_DELTAS) need += t_elems * sizeof(int32_t) * batch;
+    const size_t x_elems = (size_t)h->nunits * 16;
+    if (h->storage == 3 && !h->exp_in_smem && P.mode != MODE_ALL_DELTAS) need += x_elems * sizeof(int32_t) * batch;
     int rc = ensure_ws(h, need);
     if (rc) return rc;
     P.gM = (char *)h->ws + offM;
     P.gT = (char *)h->ws + offT;
     P.gM_stride = m_elems;
-    P.gT_stride = t_elems;
+    P.gT_stride = (h->storage == 3) ? x_elems : t_elems;
     kern_t kern = handle_kernel(h);
     int threads = h->threads;
     unsigned smem = h->smem_bytes;
-    if (h->storage == 3) P.rlay = make_reg_layout(h->npad, h->nb);
-    else P.lay = make_layout(h->npad, h->nunits, h->threads, h->upt, h->acc_bits / 8, h->storage);
+    if (h->storage == 3) {
+        P.hlay = make_hyb_layout(h->npad, h->nb, h->toff, h->us, h->exp_in_smem);
+        P.toff = h->toff; P.us = h->us; P.exp_in_smem = h->exp_in_smem;
+    } else P.lay = make_layout(h->npad, h->nunits, h->threads, h->upt, h->acc_bits / 8, h->storage);
     if (h->storage == 3 && P.mode == MODE_ALL_DELTAS) {
         // the full evaluator lives in the generic kernel; it keeps no per-search state
         kern = pick_kernel(32, 2, h->g_lb_class);
@@ -564,6 +600,7 @@ extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, u
         size_t need = (head + 255) / 256 * 256;
         if (h->storage == 1 || h->storage == 2) need += m_elems * acc_bytes * count;
         if (h->storage == 2) need += t_elems * sizeof(int32_t) * count;
+        if (h->storage == 3 && !h->exp_in_smem) need += (size_t)h->nunits * 16 * sizeof(int32_t) * count;
         rc = ensure_ws(h, need);
         if (rc) return rc;
     }

@@ -1,0 +1,762 @@
+// search_hybrid.cuh -- the flagship search kernel (int32 state, n <= 256).
+//
+// Same algorithm and the same integers as qap_search_kernel (search_kernel.cuh).  The
+// placement matrix M is split between the two on-chip memories of the SM:
+//   * every off-diagonal thread keeps UR units (block pairs {(I,J),(J,I)}, 32 registers each)
+//     in REGISTERS for the whole run, and
+//   * a further US units per thread in SHARED MEMORY in a spill layout (row w of slot k of
+//     thread t at ((k*8+w)*Toff + t)*16 bytes: every access is a conflict-free 128-bit
+//     LDS/STS) that are streamed through registers once per iteration.
+// The last DW warps own the nb diagonal 4x4 blocks (registers).  The tabu triangle is a
+// 16-bit mask per unit (pairs that are tabu now); expiry iterations live in an array that
+// is only touched when a pair is set or expires (shared memory when it fits, else L2).
+// The split is chosen per instance on the host (qapb.cu, plan_hybrid): n = 100 runs 3
+// searches per SM (160 units in registers + 140 in shared memory per search), n = 256 runs
+// one search per SM with 896 units in registers and 1120 in 140 KB of shared memory --
+// neither memory alone can hold the 256 KB of state of an n = 256 search.
+//
+// After move (r,s) the 4n entries on rows/columns r,s do not follow the rank-2 rule.  They
+// are fixed at the start of the next pass from six n-vectors published between the two
+// barriers of an iteration:
+//   colR[i] = M[i][r], colS[i] = M[i][s]     dumped by the threads that own those columns
+//   tR[i], tS[i]                             additive terms of  M'[i][r] = colS[i] + tR[i],
+//                                                               M'[i][s] = colR[i] + tS[i]
+//   xR[i], xS[i]                             additive terms of  M'[r][i] = M[r][i] + xR[i], ...
+// with the corner values M'[r][s], M'[s][r] folded into tS[r], tR[s] (colR[r] = colS[s] = 0)
+// and h[r], h[s] written by the thread that owns the winning pair.  r & 3 and s & 3 are
+// uniform across the CTA, so register indices are selected with uniform switches.
+#pragma once
+#include "search_kernel.cuh"
+
+namespace qapb {
+
+__host__ __device__ inline HybLayout make_hyb_layout(int npad, int nb, int toff, int us, int exp_in_smem)
+{
+    HybLayout L;
+    unsigned o = 0;
+    const unsigned v = 4u * (unsigned)npad;
+    L.offM = o; o += (unsigned)us * 8u * (unsigned)toff * 16u;
+    L.offTB = o; o += align16(4u * (unsigned)us * (unsigned)toff);
+    L.offMX = o; o += align16(4u * (unsigned)us * (unsigned)toff);
+    L.offA = o; o += v; L.offC = o; o += v; L.offB = o; o += v; L.offE = o; o += v; L.offH = o; o += v;
+    L.offColR = o; o += v; L.offColS = o; o += v; L.offTR = o; o += v; L.offTS = o; o += v;
+    L.offXR = o; o += v; L.offXS = o; o += v;
+    L.offP = o; o += v; L.offJ = o; o += v;
+    L.offRedD = o; o += 32u * 8u + 16u;
+    L.offRedK = o; o += 32u * 4u;
+    L.offMisc = o; o += 64u;
+    L.offTen = o; o += 4u * TENURE_CHUNK;
+    L.offExp = o;
+    if (exp_in_smem) o += 64u * (unsigned)(nb * (nb - 1) / 2 + nb);  // tabu expiry per (unit, slot)
+    L.total = align16(o);
+    return L;
+}
+
+struct Vecs {
+    int32_t *A, *C, *B, *E, *H, *ColR, *ColS, *TR, *TS, *XR, *XS;
+};
+
+__device__ __forceinline__ int32_t pick16(const int32_t (&A)[4][4], int slot)
+{
+    int32_t r = A[0][0];
+#pragma unroll
+    for (int q = 1; q < 16; ++q) r = (slot == q) ? A[q >> 2][q & 3] : r;
+    return r;
+}
+__device__ __forceinline__ void st_vec4(int32_t *arr, int blk, int32_t a, int32_t b, int32_t c, int32_t d)
+{
+    reinterpret_cast<int4 *>(arr)[blk] = make_int4(a, b, c, d);
+}
+
+// M entries of one unit from scratch (O(n) per entry): the full evaluator.
+// U[u][v] = M[4I+u][4J+v], L[v][u] = M[4J+v][4I+u]; dead = mask of pad pairs.
+__device__ __forceinline__ void build_unit(const SearchParams &P, const int32_t *sP, int I, int J, bool sym,
+                                           int32_t (&U)[4][4], int32_t (&L)[4][4], unsigned &dead)
+{
+    const int n = P.n, npad = P.npad;
+    const int32_t *__restrict__ F = P.F;
+    const int32_t *__restrict__ FT = P.FT;
+    const int32_t *__restrict__ D = P.D;
+    const int32_t *__restrict__ DT = P.DT;
+    int pI[4], pJ[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { pI[u] = sP[4 * I + u]; pJ[u] = sP[4 * J + u]; }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) { U[u][v] = 0; L[u][v] = 0; }
+    for (int kk = 0; kk < n; ++kk) {
+        const int pk = sP[kk];
+        int32_t dI[4], dJ[4], fI[4], fJ[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            dI[u] = D[(4 * I + u) * npad + kk];
+            dJ[u] = D[(4 * J + u) * npad + kk];
+            fI[u] = F[pI[u] * npad + pk];
+            fJ[u] = F[pJ[u] * npad + pk];
+        }
+        if (sym) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    U[u][v] += dI[u] * fJ[v];
+                    L[v][u] += dJ[v] * fI[u];
+                }
+        } else {
+            int32_t dtI[4], dtJ[4], ftI[4], ftJ[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                dtI[u] = DT[(4 * I + u) * npad + kk];
+                dtJ[u] = DT[(4 * J + u) * npad + kk];
+                ftI[u] = FT[pI[u] * npad + pk];
+                ftJ[u] = FT[pJ[u] * npad + pk];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    U[u][v] += dI[u] * fJ[v] + dtI[u] * ftJ[v];
+                    L[v][u] += dJ[v] * fI[u] + dtJ[v] * ftI[u];
+                }
+        }
+    }
+    dead = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int i = 4 * I + u, j = 4 * J + v;
+            if (sym) { U[u][v] *= 2; L[v][u] *= 2; }
+            const int32_t fs = F[pI[u] * npad + pJ[v]] + F[pJ[v] * npad + pI[u]];
+            U[u][v] += D[i * npad + j] * fs + P.dd[i] * P.fd[pJ[v]];
+            L[v][u] += D[j * npad + i] * fs + P.dd[j] * P.fd[pI[u]];
+            const bool pad = (i >= n) || (j >= n);
+            if (pad) { U[u][v] = 1 << 29; L[v][u] = 1 << 29; dead |= 1u << (u * 4 + v); }
+            if (i == j) { U[u][v] = 0; L[v][u] = 0; }
+        }
+}
+
+#define QAPB_SWITCH4(idx, BODY)            \
+    switch (idx) {                         \
+        case 0: { constexpr int q = 0; BODY } break; \
+        case 1: { constexpr int q = 1; BODY } break; \
+        case 2: { constexpr int q = 2; BODY } break; \
+        default: { constexpr int q = 3; BODY } break; \
+    }
+
+// ---- one off-diagonal unit: rank-2 update, then rows / columns r,s of the previous move --------
+template <bool SYM>
+__device__ __forceinline__ void unit_update(int32_t (&U)[4][4], int32_t (&L)[4][4], int Ik, int Jk, int R, int S,
+                                            int ru, int su, const Vecs &V)
+{
+    int32_t aI[4], bI[4], aJ[4], bJ[4];
+    ld_vec4(V.A, Ik, aI); ld_vec4(V.B, Ik, bI); ld_vec4(V.A, Jk, aJ); ld_vec4(V.B, Jk, bJ);
+    if (SYM) {  // a is pre-doubled: a == c, b == e
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                U[u][v] -= aI[u] * bJ[v];
+                L[v][u] -= aJ[v] * bI[u];
+            }
+    } else {
+        int32_t cI[4], eI[4], cJ[4], eJ[4];
+        ld_vec4(V.C, Ik, cI); ld_vec4(V.E, Ik, eI); ld_vec4(V.C, Jk, cJ); ld_vec4(V.E, Jk, eJ);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                U[u][v] -= aI[u] * bJ[v] + cI[u] * eJ[v];
+                L[v][u] -= aJ[v] * bI[u] + cJ[v] * eI[u];
+            }
+    }
+    if (Ik == R || Jk == R || Ik == S || Jk == S) {
+        if (Ik == R) {
+            int32_t x[4], cs[4], t[4];
+            ld_vec4(V.XR, Jk, x); ld_vec4(V.ColS, Jk, cs); ld_vec4(V.TR, Jk, t);
+            QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+                for (int v = 0; v < 4; ++v) { U[q][v] += x[v]; L[v][q] = cs[v] + t[v]; }
+            })
+        }
+        if (Jk == R) {
+            int32_t x[4], cs[4], t[4];
+            ld_vec4(V.XR, Ik, x); ld_vec4(V.ColS, Ik, cs); ld_vec4(V.TR, Ik, t);
+            QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+                for (int u = 0; u < 4; ++u) { L[q][u] += x[u]; U[u][q] = cs[u] + t[u]; }
+            })
+        }
+        if (Ik == S) {
+            int32_t x[4], cr[4], t[4];
+            ld_vec4(V.XS, Jk, x); ld_vec4(V.ColR, Jk, cr); ld_vec4(V.TS, Jk, t);
+            QAPB_SWITCH4(su, {
+_Pragma("unroll")
+                for (int v = 0; v < 4; ++v) { U[q][v] += x[v]; L[v][q] = cr[v] + t[v]; }
+            })
+        }
+        if (Jk == S) {
+            int32_t x[4], cr[4], t[4];
+            ld_vec4(V.XS, Ik, x); ld_vec4(V.ColR, Ik, cr); ld_vec4(V.TS, Ik, t);
+            QAPB_SWITCH4(su, {
+_Pragma("unroll")
+                for (int u = 0; u < 4; ++u) { L[q][u] += x[u]; U[u][q] = cr[u] + t[u]; }
+            })
+        }
+    }
+}
+
+// ---- delta, admissibility (_kernels.pyx:162), first minimum of one off-diagonal unit -----------
+// The ALU pipe (IADD3 / ISETP / IMNMX, half rate) is the busiest pipe of the pass, so the first
+// add of each delta and the (delta, slot) packing are multiplications by the runtime constants
+// 1 and 16: they issue as IMAD on the FMA pipe.  PACKED: |delta| < 2^27 (host-proven), key =
+// delta*16 + slot orders by (delta, slot), so the running first-minimum is one predicated
+// IMNMX per pair in four independent chains.
+template <bool PACKED>
+__device__ __forceinline__ void unit_select(const int32_t (&U)[4][4], const int32_t (&L)[4][4], unsigned tbk, int Ik,
+                                            int Jk, int32_t thr, const int32_t *sH, int one, int sixteen,
+                                            int32_t &dbest, int &sbest)
+{
+    const int32_t MAXV = 0x7fffffff;
+    int32_t hI[4], hJ[4];
+    ld_vec4(sH, Ik, hI);
+    ld_vec4(sH, Jk, hJ);
+    if (PACKED) {
+        int32_t km[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            km[u] = MAXV;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int32_t d = (U[u][v] * one + L[v][u]) - hI[u] - hJ[v];
+                const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
+                const int32_t kd = (int32_t)((uint32_t)d * (uint32_t)sixteen + (uint32_t)(u * 4 + v));
+                if (adm) km[u] = min(km[u], kd);
+            }
+        }
+        const int32_t m = min(min(km[0], km[1]), min(km[2], km[3]));
+        dbest = (m == MAXV) ? MAXV : (m >> 4);
+        sbest = m & 15;
+    } else {
+        int32_t rd[4];
+        int rs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            rd[u] = MAXV;
+            rs[u] = u * 4;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int32_t d = (U[u][v] * one + L[v][u]) - hI[u] - hJ[v];
+                const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
+                if (adm && d < rd[u]) { rd[u] = d; rs[u] = u * 4 + v; }
+            }
+        }
+        if (rd[1] < rd[0]) { rd[0] = rd[1]; rs[0] = rs[1]; }
+        if (rd[3] < rd[2]) { rd[2] = rd[3]; rs[2] = rs[3]; }
+        if (rd[2] < rd[0]) { rd[0] = rd[2]; rs[0] = rs[2]; }
+        dbest = rd[0];
+        sbest = rs[0];
+    }
+}
+
+// ---- diagonal block: update + fix-ups (column assignments first, then row increments) ----------
+template <bool SYM>
+__device__ __forceinline__ void diag_update(int32_t (&U)[4][4], int Ik, int R, int S, int ru, int su, const Vecs &V)
+{
+    int32_t aI[4], bI[4];
+    ld_vec4(V.A, Ik, aI); ld_vec4(V.B, Ik, bI);
+    if (SYM) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                if (u != v) U[u][v] -= aI[u] * bI[v];
+    } else {
+        int32_t cI[4], eI[4];
+        ld_vec4(V.C, Ik, cI); ld_vec4(V.E, Ik, eI);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                if (u != v) U[u][v] -= aI[u] * bI[v] + cI[u] * eI[v];
+    }
+    if (Ik == R) {
+        int32_t cs[4], t[4];
+        ld_vec4(V.ColS, Ik, cs); ld_vec4(V.TR, Ik, t);
+        QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+            for (int u = 0; u < 4; ++u) if (u != q) U[u][q] = cs[u] + t[u];
+        })
+    }
+    if (Ik == S) {
+        int32_t cr[4], t[4];
+        ld_vec4(V.ColR, Ik, cr); ld_vec4(V.TS, Ik, t);
+        QAPB_SWITCH4(su, {
+_Pragma("unroll")
+            for (int u = 0; u < 4; ++u) if (u != q) U[u][q] = cr[u] + t[u];
+        })
+    }
+    if (Ik == R) {
+        int32_t x[4];
+        ld_vec4(V.XR, Ik, x);
+        QAPB_SWITCH4(ru, {
+_Pragma("unroll")
+            for (int v = 0; v < 4; ++v) if (v != q) U[q][v] += x[v];
+        })
+    }
+    if (Ik == S) {
+        int32_t x[4];
+        ld_vec4(V.XS, Ik, x);
+        QAPB_SWITCH4(su, {
+_Pragma("unroll")
+            for (int v = 0; v < 4; ++v) if (v != q) U[q][v] += x[v];
+        })
+    }
+}
+
+__device__ __forceinline__ void diag_select(const int32_t (&U)[4][4], unsigned tbk, int Ik, int32_t thr,
+                                            const int32_t *sH, int32_t &dbest, int &sbest)
+{
+    int32_t hI[4];
+    ld_vec4(sH, Ik, hI);
+    dbest = 0x7fffffff;
+    sbest = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = u + 1; v < 4; ++v) {
+            const int32_t d = U[u][v] + U[v][u] - hI[u] - hI[v];
+            const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
+            if (adm && d < dbest) { dbest = d; sbest = u * 4 + v; }
+        }
+}
+
+// ---- tabu bits of a unit: clear the ones whose expiry has been reached ------------------------
+__device__ __forceinline__ void expire_bits(unsigned &tb, int32_t &mexp, int c, const int32_t *xp16)
+{
+    unsigned bits = tb;
+    int32_t nm = 0x7fffffff;
+    while (bits) {
+        const int q = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int32_t e = xp16[q];
+        if (e <= c) tb &= ~(1u << q);
+        else if (e != 0x7fffffff) nm = min(nm, e);
+    }
+    mexp = nm;
+}
+
+template <bool SYM, bool PACKED, int UR, bool SMEMU, int MAXREG>
+__global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
+    const int b = blockIdx.x;
+    const int n = P.n, nb = P.nb, npad = P.npad, noff = P.noff;
+    const int Toff = P.toff;              // off-diagonal threads
+    const int US = SMEMU ? P.us : 0;      // shared-memory units per thread (compiled out when none)
+    const HybLayout &lay = P.hlay;
+    int32_t *sM = reinterpret_cast<int32_t *>(smem_raw + lay.offM);
+    unsigned *sTB = reinterpret_cast<unsigned *>(smem_raw + lay.offTB);
+    int32_t *sMX = reinterpret_cast<int32_t *>(smem_raw + lay.offMX);
+    Vecs V;
+    V.A = reinterpret_cast<int32_t *>(smem_raw + lay.offA);
+    V.C = reinterpret_cast<int32_t *>(smem_raw + lay.offC);
+    V.B = reinterpret_cast<int32_t *>(smem_raw + lay.offB);
+    V.E = reinterpret_cast<int32_t *>(smem_raw + lay.offE);
+    V.H = reinterpret_cast<int32_t *>(smem_raw + lay.offH);
+    V.ColR = reinterpret_cast<int32_t *>(smem_raw + lay.offColR);
+    V.ColS = reinterpret_cast<int32_t *>(smem_raw + lay.offColS);
+    V.TR = reinterpret_cast<int32_t *>(smem_raw + lay.offTR);
+    V.TS = reinterpret_cast<int32_t *>(smem_raw + lay.offTS);
+    V.XR = reinterpret_cast<int32_t *>(smem_raw + lay.offXR);
+    V.XS = reinterpret_cast<int32_t *>(smem_raw + lay.offXS);
+    int32_t *sP = reinterpret_cast<int32_t *>(smem_raw + lay.offP);
+    unsigned *sJ = reinterpret_cast<unsigned *>(smem_raw + lay.offJ);
+    long long *sRed64 = reinterpret_cast<long long *>(smem_raw + lay.offRedD);
+    int32_t *sRedD = reinterpret_cast<int32_t *>(smem_raw + lay.offRedD);
+    unsigned *sRedK = reinterpret_cast<unsigned *>(smem_raw + lay.offRedK);
+    long long *sMisc = reinterpret_cast<long long *>(smem_raw + lay.offMisc);
+    int32_t *sTen = reinterpret_cast<int32_t *>(smem_raw + lay.offTen);
+    // expiry iteration per (unit, slot): shared memory when it fits, else the L2-resident workspace
+    // (register-only plans always keep it in shared memory, so the pointer stays in the shared window)
+    int32_t *xp = (!SMEMU || P.exp_in_smem) ? reinterpret_cast<int32_t *>(smem_raw + lay.offExp)
+                                            : reinterpret_cast<int32_t *>(P.gT) + (size_t)b * P.gT_stride;
+
+    const int32_t *__restrict__ F = P.F;
+    const int32_t *__restrict__ FT = P.FT;
+    const int32_t *__restrict__ D = P.D;
+    const int32_t *__restrict__ DT = P.DT;
+    const int32_t MAXV = 0x7fffffff;
+    const int one = P.one, sixteen = P.sixteen;
+
+    // ---------------------------------------------------------------- setup
+    for (int i = tid; i < npad; i += T) {
+        V.A[i] = 0; V.C[i] = 0; V.B[i] = 0; V.E[i] = 0; V.H[i] = 0;
+        V.ColR[i] = 0; V.ColS[i] = 0; V.TR[i] = 0; V.TS[i] = 0; V.XR[i] = 0; V.XS[i] = 0;
+        sP[i] = (P.rng || i >= n) ? (i < n ? i : 0) : (int32_t)P.perms[(size_t)b * n + i];
+    }
+    unsigned long long rng_state = 0;
+    if (P.rng) {
+        // multistart.py:88: state = derive_seed(master, index); core.py:81-87 shuffle.  Draws are
+        // computed in parallel assuming no rejection; a rejection (probability ~ n^2/2^64) falls
+        // back to the exact sequential loop.
+        const unsigned long long seed = mix64(P.master_seed + QAPB_GAMMA * (P.first_index + (unsigned long long)b + 1ULL));
+        int reject = P.force_seq_rng;
+        for (int k = tid; k < n - 1; k += T) {
+            unsigned long long bound = (unsigned long long)(n - 1 - k) + 1ULL;
+            unsigned long long r = mix64(seed + QAPB_GAMMA * ((unsigned long long)k + 1ULL));
+            unsigned long long rem = (0ULL - bound) % bound;
+            if (r > ~0ULL - rem) reject = 1;
+            sJ[n - 1 - k] = (unsigned)(r % bound);
+        }
+        reject = __syncthreads_or(reject);
+        if (tid == 0) {
+            rng_state = seed;
+            if (reject) {
+                for (int i = n - 1; i >= 1; --i) {
+                    unsigned j = (unsigned)randbelow_seq(rng_state, (unsigned long long)i + 1ULL);
+                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
+                }
+            } else {
+                for (int i = n - 1; i >= 1; --i) {
+                    unsigned j = sJ[i];
+                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
+                }
+                rng_state = seed + QAPB_GAMMA * (unsigned long long)(n - 1);
+            }
+            sMisc[2] = (long long)rng_state;
+        }
+    }
+    if (P.cells) {
+        int64_t *cz = P.cells + (size_t)b * n * n;
+        for (int i = tid; i < n * n; i += T) cz[i] = 0;
+    }
+    __syncthreads();
+    if (P.rng) rng_state = (unsigned long long)sMisc[2];
+
+    long long cost;
+    {
+        long long part = 0;
+        for (int idx = tid; idx < n * n; idx += T) {
+            int i = idx / n, j = idx - i * n;
+            int pi = sP[i], pj = sP[j];
+            part += (i == j) ? (long long)P.fd[pi] * P.dd[i] : (long long)F[pi * npad + pj] * D[i * npad + j];
+        }
+        cost = block_sum_i64(part, sRed64, tid, T);
+        __syncthreads();
+    }
+    for (int i = tid; i < n; i += T) {
+        int pi = sP[i];
+        int32_t acc = P.dd[i] * P.fd[pi];
+        if (SYM) {
+            for (int k = 0; k < n; ++k) acc += 2 * (D[i * npad + k] * F[pi * npad + sP[k]]);
+        } else {
+            for (int k = 0; k < n; ++k) {
+                int pk = sP[k];
+                acc += D[i * npad + k] * F[pi * npad + pk] + DT[i * npad + k] * FT[pi * npad + pk];
+            }
+        }
+        V.H[i] = acc;
+    }
+
+    // ---- unit ownership.  tb = mask of pairs that are tabu now (pads / non-pairs permanently
+    // set, expiry MAXV), mexp = earliest expiry among the clearable bits.
+    const bool offt = tid < Toff;
+    const bool diag = tid >= Toff && (tid - Toff) < nb;
+    int I[UR], J[UR], uidv[UR];
+    bool own[UR];
+    int32_t U[UR][4][4], L[UR][4][4];
+    unsigned tb[UR];
+    int32_t mexp[UR];
+#pragma unroll
+    for (int k = 0; k < UR; ++k) {
+        const int uid = tid + k * Toff;
+        own[k] = offt && (uid < noff);
+        I[k] = 0; J[k] = 0; uidv[k] = 0; tb[k] = 0xffffu; mexp[k] = MAXV;
+        if (own[k]) { I[k] = P.unit_ij[uid] & 0xff; J[k] = P.unit_ij[uid] >> 8; uidv[k] = uid; }
+        if (k == 0 && diag) { I[0] = tid - Toff; J[0] = I[0]; uidv[0] = noff + I[0]; own[0] = true; }
+        if (own[k]) {
+            unsigned dead;
+            build_unit(P, sP, I[k], J[k], SYM, U[k], L[k], dead);
+            if (diag) dead |= 0xF731u;  // slots with u >= v are not pairs of a diagonal block
+            tb[k] = dead;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) xp[uidv[k] * 16 + q] = ((dead >> q) & 1u) ? MAXV : 0;
+        }
+    }
+    if (SMEMU && offt) {
+        for (int k2 = 0; k2 < US; ++k2) {
+            const int uid = UR * Toff + k2 * Toff + tid;
+            if (uid < noff) {
+                int32_t Us[4][4], Ls[4][4];
+                unsigned dead;
+                const int Ik = P.unit_ij[uid] & 0xff, Jk = P.unit_ij[uid] >> 8;
+                build_unit(P, sP, Ik, Jk, SYM, Us, Ls, dead);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    st_row(sM, k2 * 8 + u, Toff, tid, Us[u]);
+                    st_row(sM, k2 * 8 + 4 + u, Toff, tid, Ls[u]);
+                }
+                sTB[k2 * Toff + tid] = dead;
+                sMX[k2 * Toff + tid] = MAXV;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) xp[uid * 16 + q] = ((dead >> q) & 1u) ? MAXV : 0;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ------------------------------------------------------------ iterations
+    long long best_cost = cost;
+    int32_t thr = 0;  // best_cost - cost, clamped; aspiration <=> delta < thr  (_kernels.pyx:162)
+    const bool tabu = P.mode == MODE_TABU;
+    const int iters = P.iterations;
+    int steps_done = 0, stopped = 0;
+    int64_t *best_out = P.best + (size_t)b * n;
+    for (int i = tid; i < n; i += T) best_out[i] = sP[i];
+    int R = -1, S = -1, ru = 0, su = 0;  // previous move (block and in-block indices)
+
+    for (int c = 1; c <= iters; ++c) {
+        long long ten = 0;
+        if (tabu) {
+            if (!P.rng) {
+                ten = P.tenures[(size_t)b * iters + (c - 1)];
+            } else if (((c - 1) & (TENURE_CHUNK - 1)) == 0) {
+                fill_tenure_chunk(rng_state, P.ten_lo, P.ten_hi, P.force_seq_rng, sTen, sMisc, tid, T);
+            }
+        }
+
+        // ---------------- pass: update + select over this thread's units
+        int32_t my_d = MAXV;
+        unsigned my_key = 0xffffffffu;
+        int my_which = 0, my_slot = 0;  // which: register unit k, or UR + k2 for a shared-memory unit
+#pragma unroll
+        for (int k = 0; k < UR; ++k) {
+            if (!own[k]) continue;
+            int32_t dk;
+            int sk;
+            if (I[k] != J[k]) {
+                if (R >= 0) unit_update<SYM>(U[k], L[k], I[k], J[k], R, S, ru, su, V);
+                unit_select<PACKED>(U[k], L[k], tb[k], I[k], J[k], thr, V.H, one, sixteen, dk, sk);
+            } else {
+                if (R >= 0) diag_update<SYM>(U[k], I[k], R, S, ru, su, V);
+                diag_select(U[k], tb[k], I[k], thr, V.H, dk, sk);
+            }
+            if (dk != MAXV) {
+                const unsigned key = pair_key(4 * I[k] + (sk >> 2), 4 * J[k] + (sk & 3), 0);
+                if (dk < my_d || (dk == my_d && key < my_key)) { my_d = dk; my_key = key; my_which = k; my_slot = sk; }
+            }
+        }
+        if (SMEMU && offt) {
+#pragma unroll 1
+            for (int k2 = 0; k2 < US; ++k2) {
+                const int uid = UR * Toff + k2 * Toff + tid;
+                if (uid >= noff) break;
+                const int Ik = P.unit_ij[uid] & 0xff, Jk = P.unit_ij[uid] >> 8;
+                int32_t Us[4][4], Ls[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    ld_row(sM, k2 * 8 + u, Toff, tid, Us[u]);
+                    ld_row(sM, k2 * 8 + 4 + u, Toff, tid, Ls[u]);
+                }
+                if (R >= 0) {
+                    unit_update<SYM>(Us, Ls, Ik, Jk, R, S, ru, su, V);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        st_row(sM, k2 * 8 + u, Toff, tid, Us[u]);
+                        st_row(sM, k2 * 8 + 4 + u, Toff, tid, Ls[u]);
+                    }
+                }
+                int32_t dk;
+                int sk;
+                unit_select<PACKED>(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V.H, one, sixteen, dk, sk);
+                if (dk != MAXV) {
+                    const unsigned key = pair_key(4 * Ik + (sk >> 2), 4 * Jk + (sk & 3), 0);
+                    if (dk < my_d || (dk == my_d && key < my_key)) { my_d = dk; my_key = key; my_which = UR + k2; my_slot = sk; }
+                }
+            }
+        }
+
+        int32_t bd = my_d;
+        unsigned bkey = my_key;
+        warp_argmin(bd, bkey);
+        if (lane == 0) { sRedD[warp] = bd; sRedK[warp] = bkey; }
+        __syncthreads();  // ---------------------------------------------- sync #1
+        bd = lane < W ? sRedD[lane] : MAXV;
+        bkey = lane < W ? sRedK[lane] : 0xffffffffu;
+        warp_argmin(bd, bkey);
+        if (bd == MAXV) {  // no admissible move: premature stop (_kernels.pyx:168-170)
+            stopped = 1;
+            break;
+        }
+        const int r = (int)(bkey >> 17), s = (int)((bkey >> 1) & 0xffffu);
+        cost += (long long)bd;
+        const bool improved = cost < best_cost;
+        if (improved) best_cost = cost;
+        thr = Acc<int32_t>::clamp_thr(best_cost - cost);
+        if (tabu && P.rng) ten = sTen[(c - 1) & (TENURE_CHUNK - 1)];
+        steps_done = c;
+        R = r >> 2; S = s >> 2; ru = r & 3; su = s & 3;
+        const int pr = sP[r], ps = sP[s];
+
+        // ---------------- publish: difference vectors of the move (old permutation), additive
+        // terms, h'[i] -- one location per thread
+        for (int i = tid; i < n; i += T) {
+            const int pi = sP[i];
+            const bool mid = (i != r) && (i != s);
+            if (improved) best_out[i] = (i == r) ? ps : (i == s) ? pr : pi;
+            if (SYM) {
+                // D = D^T, F = F^T: a = c, b = e, and the closed forms collapse
+                const int32_t Drs = D[r * npad + s], Fpspr = F[ps * npad + pr];
+                const int32_t Dsi = D[s * npad + i], Dri = D[r * npad + i];
+                const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
+                const int32_t a = mid ? Dsi - Dri : 0, bb = mid ? Fpspi - Fprpi : 0;
+                const int32_t a2 = 2 * a, b2 = 2 * bb;
+                V.A[i] = a2;
+                V.B[i] = bb;
+                V.XR[i] = b2 * ((mid ? Dri : 0) - Drs);
+                V.XS[i] = b2 * (Drs - (mid ? Dsi : 0));
+                if (mid) {
+                    V.H[i] -= a2 * bb;
+                    V.TR[i] = a2 * (Fpspr - Fpspi);
+                    V.TS[i] = a2 * (Fprpi - Fpspr);
+                } else if (i == r) {
+                    V.TR[i] = 0;  // tS[r] is written by the owner of the pair
+                } else {
+                    V.TS[i] = 0;  // tR[s] is written by the owner of the pair
+                }
+            } else {
+                const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
+                const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
+                const int32_t Dsi = D[s * npad + i], Dri = D[r * npad + i];
+                const int32_t Dis = DT[s * npad + i], Dir = DT[r * npad + i];
+                const int32_t Fpips = FT[ps * npad + pi], Fpipr = FT[pr * npad + pi];
+                const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
+                const int32_t a = mid ? Dis - Dir : 0, cc = mid ? Dsi - Dri : 0;
+                const int32_t bb = mid ? Fpips - Fpipr : 0, e = mid ? Fpspi - Fprpi : 0;
+                const int32_t be = bb + e;
+                V.A[i] = a;
+                V.B[i] = bb;
+                V.C[i] = cc;
+                V.E[i] = e;
+                V.XR[i] = -Drs * bb - Dsr * e + (mid ? Dri : 0) * be;
+                V.XS[i] = Dsr * bb + Drs * e - (mid ? Dsi : 0) * be;
+                if (mid) {
+                    V.H[i] -= a * bb + cc * e;
+                    V.TR[i] = a * (Fpspr - (Fpips + Fpspi)) + cc * Fprps;
+                    V.TS[i] = a * ((Fpipr + Fprpi) - Fprps) - cc * Fpspr;
+                } else if (i == r) {
+                    V.TR[i] = 0;
+                } else {
+                    V.TS[i] = 0;
+                }
+            }
+        }
+        // ---- the thread owning the winning pair: corners, h[r], h[s], tabu memory, trail
+        if (my_key == bkey) {
+            const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
+            const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
+            const int32_t new_exp = (int32_t)(c + ten);
+            int32_t mrs = 0, msr = 0;
+            unsigned was = 0;
+            if (!SMEMU || my_which < UR) {
+#pragma unroll
+                for (int k = 0; k < UR; ++k) {
+                    if (k != my_which) continue;
+                    mrs = pick16(U[k], ru * 4 + su);
+                    msr = (I[k] != J[k]) ? pick16(L[k], su * 4 + ru) : pick16(U[k], su * 4 + ru);
+                    was = (tb[k] >> my_slot) & 1u;
+                    if (tabu) {
+                        tb[k] |= 1u << my_slot;
+                        mexp[k] = min(mexp[k], new_exp);
+                        xp[uidv[k] * 16 + my_slot] = new_exp;
+                    }
+                }
+            } else {
+                const int k2 = my_which - UR;
+                mrs = sM[((size_t)((k2 * 8 + ru) * Toff + tid)) * 4 + su];      // U[ru][su]
+                msr = sM[((size_t)((k2 * 8 + 4 + su) * Toff + tid)) * 4 + ru];  // L[su][ru]
+                const unsigned old = sTB[k2 * Toff + tid];
+                was = (old >> my_slot) & 1u;
+                if (tabu) {
+                    sTB[k2 * Toff + tid] = old | (1u << my_slot);
+                    sMX[k2 * Toff + tid] = min(sMX[k2 * Toff + tid], new_exp);
+                    xp[(UR * Toff + k2 * Toff + tid) * 16 + my_slot] = new_exp;
+                }
+            }
+            const int32_t hr = V.H[r], hs = V.H[s];
+            V.TS[r] = hr + (Drs - Dsr) * Fpspr;  // M'[r][s]
+            V.TR[s] = hs + (Dsr - Drs) * Fprps;  // M'[s][r]
+            V.H[r] = mrs + (Dsr - Drs) * Fprps;
+            V.H[s] = msr + (Drs - Dsr) * Fpspr;
+            if (P.tr_i) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
+                const size_t o = (size_t)b * iters + (c - 1);
+                P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
+                if (P.tr_tabu) P.tr_tabu[o] = (int64_t)was;
+            }
+            if (tabu && P.cells) {
+                int64_t *cz = P.cells + (size_t)b * n * n;
+                cz[(size_t)r * n + s] = (int64_t)c + ten;
+                cz[(size_t)s * n + r] += 1;
+            }
+        }
+        // ---- owners of columns r and s publish them (colR[r] = colS[s] = 0 by the diagonal lanes),
+        // and tabu bits that expire at the next iteration are cleared here, off the critical path
+#pragma unroll
+        for (int k = 0; k < UR; ++k) {
+            if (!own[k]) continue;
+            const int Ik = I[k], Jk = J[k];
+            if (Ik != Jk) {
+                if (Jk == R) { QAPB_SWITCH4(ru, { st_vec4(V.ColR, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]); }) }
+                if (Ik == R) { QAPB_SWITCH4(ru, { st_vec4(V.ColR, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]); }) }
+                if (Jk == S) { QAPB_SWITCH4(su, { st_vec4(V.ColS, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]); }) }
+                if (Ik == S) { QAPB_SWITCH4(su, { st_vec4(V.ColS, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]); }) }
+            } else {
+                if (Ik == R) {
+                    QAPB_SWITCH4(ru, { st_vec4(V.ColR, Ik, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
+                }
+                if (Ik == S) {
+                    QAPB_SWITCH4(su, { st_vec4(V.ColS, Ik, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
+                }
+            }
+            if (c + 1 >= mexp[k]) expire_bits(tb[k], mexp[k], c + 1, xp + uidv[k] * 16);
+        }
+        if (SMEMU && offt) {
+#pragma unroll 1
+            for (int k2 = 0; k2 < US; ++k2) {
+                const int uid = UR * Toff + k2 * Toff + tid;
+                if (uid >= noff) break;
+                const int Ik = P.unit_ij[uid] & 0xff, Jk = P.unit_ij[uid] >> 8;
+                // element (row w, lane l) of this unit: sM[((k2*8 + w)*Toff + tid)*4 + l]
+                const int32_t *base = sM + ((size_t)(k2 * 8) * Toff + tid) * 4;
+                const size_t rs4 = (size_t)Toff * 4;  // stride between rows
+                if (Jk == R) st_vec4(V.ColR, Ik, base[0 * rs4 + ru], base[1 * rs4 + ru], base[2 * rs4 + ru], base[3 * rs4 + ru]);
+                if (Ik == R) st_vec4(V.ColR, Jk, base[4 * rs4 + ru], base[5 * rs4 + ru], base[6 * rs4 + ru], base[7 * rs4 + ru]);
+                if (Jk == S) st_vec4(V.ColS, Ik, base[0 * rs4 + su], base[1 * rs4 + su], base[2 * rs4 + su], base[3 * rs4 + su]);
+                if (Ik == S) st_vec4(V.ColS, Jk, base[4 * rs4 + su], base[5 * rs4 + su], base[6 * rs4 + su], base[7 * rs4 + su]);
+                int32_t mx = sMX[k2 * Toff + tid];
+                if (c + 1 >= mx) {
+                    unsigned tbv = sTB[k2 * Toff + tid];
+                    expire_bits(tbv, mx, c + 1, xp + uid * 16);
+                    sTB[k2 * Toff + tid] = tbv;
+                    sMX[k2 * Toff + tid] = mx;
+                }
+            }
+        }
+        __syncthreads();  // ---------------------------------------------- sync #2
+        if (tid == 0) { sP[r] = ps; sP[s] = pr; }
+    }
+    __syncthreads();
+
+    for (int i = tid; i < n; i += T) P.cur[(size_t)b * n + i] = sP[i];
+    if (tid == 0) {
+        P.best_cost[b] = best_cost;
+        P.cur_cost[b] = cost;
+        if (P.stopped) P.stopped[b] = stopped;
+        if (P.steps) P.steps[b] = steps_done;
+    }
+}
+
+}  // namespace qapb

@@ -71,9 +71,9 @@ __host__ __device__ inline SmemLayout make_layout(int npad, int nunits, int T, i
     return L;
 }
 
-struct RegLayout {
-    unsigned offA, offC, offB, offE, offH, offColR, offColS, offTR, offTS, offXR, offXS;
-    unsigned offP, offJ, offDM, offDT, offRedD, offRedK, offMisc, offTen, offExp, total;
+struct HybLayout {  // search_hybrid.cuh
+    unsigned offM, offTB, offMX, offA, offC, offB, offE, offH, offColR, offColS, offTR, offTS, offXR, offXS;
+    unsigned offP, offJ, offRedD, offRedK, offMisc, offTen, offExp, total;
 };
 
 struct SearchParams {
@@ -101,7 +101,8 @@ struct SearchParams {
     unsigned long long gM_stride, gT_stride;  // elements per start
     long long *dbg;                  // optional phase-cycle counters (development), else null
     SmemLayout lay;                  // generic kernel: offsets live in the constant bank
-    RegLayout rlay;                  // register-resident kernel
+    HybLayout hlay;                  // hybrid kernel
+    int toff, us, exp_in_smem;       // hybrid plan: off-diagonal threads, shared-memory units per thread
 };
 
 // ---- accumulator traits -----------------------------------------------------
