@@ -1,0 +1,178 @@
+// build_kernels.cuh -- start generation and the O(n^3) construction of the placement matrix.
+//
+//   qap_start_kernel      per start: derive_seed (rng.py:62-70), Fisher-Yates shuffle
+//                         (core.py:81-87, rng.py:55-59) -> int32 permutation + stream state,
+//                         or conversion of caller-provided int64 permutations.
+//   qap_build_m_kernel    M[b] = W + D0.Fp^T-type products (see search_kernel.cuh header) for a
+//                         batch of permutations: a tiled integer matrix product -- 64x64 output
+//                         tile per CTA, 4x4 micro-tile per thread, k-chunks of 32 staged in shared
+//                         memory.  A-tiles are rows of D^T / D (coalesced, already k-major),
+//                         B-tiles are rows p_k of F^T / F gathered at columns p_j.  This is the
+//                         full evaluator of kernels.all_deltas expressed as a contraction, which
+//                         is exactly how the reference's NumPy backend states it
+//                         (_purekernels.py:25-56: P = D Fp^T, Q = D^T Fp).
+#pragma once
+#include "search_kernel.cuh"
+
+namespace qapb {
+
+struct StartParams {
+    int n, npad, rng, force_seq_rng;
+    unsigned long long master_seed, first_index;
+    const int64_t *perms;            // [B,n] (rng == 0)
+    int32_t *perm32;                 // [B,npad] out
+    unsigned long long *state;       // [B] out: SplitMix64 state after the shuffle
+};
+
+__global__ void __launch_bounds__(128) qap_start_kernel(const StartParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int32_t *sP = reinterpret_cast<int32_t *>(smem_raw);
+    unsigned *sJ = reinterpret_cast<unsigned *>(smem_raw) + P.npad;
+    const int tid = threadIdx.x, T = blockDim.x, b = blockIdx.x, n = P.n;
+    for (int i = tid; i < P.npad; i += T)
+        sP[i] = (P.rng || i >= n) ? (i < n ? i : 0) : (int32_t)P.perms[(size_t)b * n + i];
+    unsigned long long st = 0;
+    if (P.rng) {
+        // draws computed in parallel assuming no rejection; a rejection (probability ~ n^2/2^64)
+        // falls back to the exact sequential loop
+        const unsigned long long seed = mix64(P.master_seed + QAPB_GAMMA * (P.first_index + (unsigned long long)b + 1ULL));
+        int reject = P.force_seq_rng;
+        for (int k = tid; k < n - 1; k += T) {
+            unsigned long long bound = (unsigned long long)(n - 1 - k) + 1ULL;
+            unsigned long long r = mix64(seed + QAPB_GAMMA * ((unsigned long long)k + 1ULL));
+            unsigned long long rem = (0ULL - bound) % bound;
+            if (r > ~0ULL - rem) reject = 1;
+            sJ[n - 1 - k] = (unsigned)(r % bound);
+        }
+        reject = __syncthreads_or(reject);
+        if (tid == 0) {
+            st = seed;
+            if (reject) {
+                for (int i = n - 1; i >= 1; --i) {
+                    unsigned j = (unsigned)randbelow_seq(st, (unsigned long long)i + 1ULL);
+                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
+                }
+            } else {
+                for (int i = n - 1; i >= 1; --i) {
+                    unsigned j = sJ[i];
+                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
+                }
+                st = seed + QAPB_GAMMA * (unsigned long long)(n - 1);
+            }
+            P.state[b] = st;
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < P.npad; i += T) P.perm32[(size_t)b * P.npad + i] = sP[i];
+}
+
+struct BuildParams {
+    int n, npad, symmetric;
+    const int32_t *F, *FT, *D, *DT, *fd, *dd;
+    const int32_t *perm32;           // [B,npad]
+    int32_t *M;                      // [B,npad,npad] out (row-major; pads = 2^29, diagonal 0)
+    int32_t *h;                      // [B,npad] out
+};
+
+enum { BT = 64, BK = 32 };
+
+__global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
+{
+    __shared__ __align__(16) int32_t sA[2][BK][BT];  // [term][k][i]
+    __shared__ __align__(16) int32_t sB[2][BK][BT];  // [term][k][j]
+    __shared__ int32_t sPk[BK];
+    extern __shared__ __align__(16) unsigned char dyn[];
+    int32_t *sPerm = reinterpret_cast<int32_t *>(dyn);  // [npad]
+    const int tid = threadIdx.x;
+    const int n = P.n, npad = P.npad;
+    const int tiles = (npad + BT - 1) / BT;
+    const int b = blockIdx.y, ti = blockIdx.x / tiles, tj = blockIdx.x % tiles;
+    const int i0 = ti * BT, j0 = tj * BT;
+    const int32_t *perm = P.perm32 + (size_t)b * npad;
+    for (int i = tid; i < npad; i += 256) sPerm[i] = perm[i];
+    __syncthreads();
+    const bool sym = P.symmetric != 0;
+    const int ty = tid >> 4, tx = tid & 15;  // micro-tile rows 4*ty.., cols 4*tx..
+    int32_t acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0;
+
+    for (int k0 = 0; k0 < n; k0 += BK) {
+        // stage: A[k][i] = D0[i0+i][k0+k] (= row k0+k of D^T), B[k][j] = F0[p_j][p_k] (= row p_k of F^T
+        // gathered at p_j); second term (asymmetric only): A2 = D0[k][i] (row of D), B2 = F0[p_k][p_j]
+        if (tid < BK) sPk[tid] = (k0 + tid < n) ? sPerm[k0 + tid] : 0;
+        __syncthreads();
+        for (int e = tid; e < BK * BT; e += 256) {
+            const int k = e / BT, x = e % BT;
+            const int kk = k0 + k;
+            const bool kin = kk < n;
+            const int gi = i0 + x, gj = j0 + x;
+            const int pk = sPk[k];
+            const int pj = (gj < npad) ? sPerm[gj] : 0;
+            sA[0][k][x] = (kin && gi < npad) ? P.DT[(size_t)kk * npad + gi] : 0;
+            sB[0][k][x] = (kin && gj < n) ? P.FT[(size_t)pk * npad + pj] : 0;
+            if (!sym) {
+                sA[1][k][x] = (kin && gi < npad) ? P.D[(size_t)kk * npad + gi] : 0;
+                sB[1][k][x] = (kin && gj < n) ? P.F[(size_t)pk * npad + pj] : 0;
+            }
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < BK; ++k) {
+            const int4 a = *reinterpret_cast<const int4 *>(&sA[0][k][4 * ty]);
+            const int4 bq = *reinterpret_cast<const int4 *>(&sB[0][k][4 * tx]);
+            const int32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {bq.x, bq.y, bq.z, bq.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] += av[u] * bv[v];
+            if (!sym) {
+                const int4 a2 = *reinterpret_cast<const int4 *>(&sA[1][k][4 * ty]);
+                const int4 b2 = *reinterpret_cast<const int4 *>(&sB[1][k][4 * tx]);
+                const int32_t av2[4] = {a2.x, a2.y, a2.z, a2.w}, bv2[4] = {b2.x, b2.y, b2.z, b2.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[u][v] += av2[u] * bv2[v];
+            }
+        }
+        __syncthreads();
+    }
+    // epilogue: direct term, diagonal products, pads, h on the diagonal
+    int32_t *Mb = P.M + (size_t)b * npad * npad;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 4 * ty + u;
+        if (i >= npad) continue;
+        int32_t out[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int j = j0 + 4 * tx + v;
+            int32_t val = sym ? 2 * acc[u][v] : acc[u][v];
+            if (j < npad) {
+                if (i >= n || j >= n) {
+                    val = (i == j) ? 0 : (1 << 29);
+                } else {
+                    const int pi = sPerm[i], pj = sPerm[j];
+                    if (i == j) {
+                        P.h[(size_t)b * npad + i] = val + P.dd[i] * P.fd[pi];
+                        val = 0;
+                    } else {
+                        val += P.D[(size_t)i * npad + j] * (P.F[(size_t)pi * npad + pj] + P.F[(size_t)pj * npad + pi]) +
+                               P.dd[i] * P.fd[pj];
+                    }
+                }
+            }
+            out[v] = val;
+        }
+        const int jb = j0 + 4 * tx;
+        if (jb < npad) *reinterpret_cast<int4 *>(&Mb[(size_t)i * npad + jb]) = make_int4(out[0], out[1], out[2], out[3]);
+    }
+    if (ti == 0 && tj == 0)
+        for (int i = n + tid; i < npad; i += 256) P.h[(size_t)b * npad + i] = 0;
+}
+
+}  // namespace qapb

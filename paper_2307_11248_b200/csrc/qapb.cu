@@ -6,6 +6,7 @@
 // per thread, where the placement matrix lives), workspace and launches.
 #include "../../include/qapb.h"
 #include "search_kernel.cuh"
+#include "build_kernels.cuh"
 #include "search_hybrid.cuh"
 
 #include <algorithm>
@@ -459,6 +460,14 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     if (h->storage == 2 && P.mode != MODE_ALL_DELTAS) need += t_elems * sizeof(int32_t) * batch;
     const size_t x_elems = (size_t)h->nunits * 16;
     if (h->storage == 3 && !h->exp_in_smem && P.mode != MODE_ALL_DELTAS) need += x_elems * sizeof(int32_t) * batch;
+    // hybrid pipeline buffers: start permutations, stream states, initial M and h
+    const bool hyb = h->storage == 3 && P.mode != MODE_ALL_DELTAS;
+    const size_t np = (size_t)h->npad;
+    need = (need + 255) / 256 * 256;
+    const size_t offPerm = need;  if (hyb) need += (np * 4 * batch + 255) / 256 * 256;
+    const size_t offState = need; if (hyb) need += ((size_t)8 * batch + 255) / 256 * 256;
+    const size_t offInitH = need; if (hyb) need += (np * 4 * batch + 255) / 256 * 256;
+    const size_t offInitM = need; if (hyb) need += np * np * 4 * batch;
     int rc = ensure_ws(h, need);
     if (rc) return rc;
     P.gM = (char *)h->ws + offM;
@@ -483,6 +492,26 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     // several handles share one kernel instantiation: (re)assert this launch's opt-in size
     CU(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CU(cudaEventRecord(h->ev0, st));
+    if (hyb) {
+        // start permutations (+ stream state), then M and h as one batched tiled integer product
+        StartParams SP;
+        SP.n = h->n; SP.npad = h->npad; SP.rng = P.rng; SP.force_seq_rng = P.force_seq_rng;
+        SP.master_seed = P.master_seed; SP.first_index = P.first_index; SP.perms = P.perms;
+        SP.perm32 = (int32_t *)((char *)h->ws + offPerm);
+        SP.state = (unsigned long long *)((char *)h->ws + offState);
+        qap_start_kernel<<<batch, 128, 2 * np * sizeof(int32_t), st>>>(SP);
+        CU(cudaGetLastError());
+        BuildParams BP;
+        BP.n = h->n; BP.npad = h->npad; BP.symmetric = h->symmetric;
+        BP.F = h->dF; BP.FT = h->dFT; BP.D = h->dD; BP.DT = h->dDT; BP.fd = h->dfd; BP.dd = h->ddd;
+        BP.perm32 = SP.perm32;
+        BP.M = (int32_t *)((char *)h->ws + offInitM);
+        BP.h = (int32_t *)((char *)h->ws + offInitH);
+        const int tiles = (h->npad + BT - 1) / BT;
+        qap_build_m_kernel<<<dim3(tiles * tiles, batch), 256, np * sizeof(int32_t), st>>>(BP);
+        CU(cudaGetLastError());
+        P.perm32 = SP.perm32; P.start_state = SP.state; P.initM = BP.M; P.initH = BP.h;
+    }
     kern<<<batch, threads, smem, st>>>(P);
     CU(cudaGetLastError());
     CU(cudaEventRecord(h->ev1, st));
@@ -601,6 +630,11 @@ extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, u
         if (h->storage == 1 || h->storage == 2) need += m_elems * acc_bytes * count;
         if (h->storage == 2) need += t_elems * sizeof(int32_t) * count;
         if (h->storage == 3 && !h->exp_in_smem) need += (size_t)h->nunits * 16 * sizeof(int32_t) * count;
+        if (h->storage == 3) {
+            const size_t np = (size_t)h->npad;
+            need = (need + 255) / 256 * 256;
+            need += 2 * ((np * 4 * count + 255) / 256 * 256) + ((size_t)8 * count + 255) / 256 * 256 + np * np * 4 * count;
+        }
         rc = ensure_ws(h, need);
         if (rc) return rc;
     }

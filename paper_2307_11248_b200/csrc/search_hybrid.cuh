@@ -68,73 +68,21 @@ __device__ __forceinline__ void st_vec4(int32_t *arr, int blk, int32_t a, int32_
     reinterpret_cast<int4 *>(arr)[blk] = make_int4(a, b, c, d);
 }
 
-// M entries of one unit from scratch (O(n) per entry): the full evaluator.
-// U[u][v] = M[4I+u][4J+v], L[v][u] = M[4J+v][4I+u]; dead = mask of pad pairs.
-__device__ __forceinline__ void build_unit(const SearchParams &P, const int32_t *sP, int I, int J, bool sym,
-                                           int32_t (&U)[4][4], int32_t (&L)[4][4], unsigned &dead)
+// One unit from the row-major M of qap_build_m_kernel; dead = mask of pad pairs.
+__device__ __forceinline__ void load_unit(const int32_t *__restrict__ Mi, int npad, int n, int I, int J,
+                                          int32_t (&U)[4][4], int32_t (&L)[4][4], unsigned &dead)
 {
-    const int n = P.n, npad = P.npad;
-    const int32_t *__restrict__ F = P.F;
-    const int32_t *__restrict__ FT = P.FT;
-    const int32_t *__restrict__ D = P.D;
-    const int32_t *__restrict__ DT = P.DT;
-    int pI[4], pJ[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { pI[u] = sP[4 * I + u]; pJ[u] = sP[4 * J + u]; }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) { U[u][v] = 0; L[u][v] = 0; }
-    for (int kk = 0; kk < n; ++kk) {
-        const int pk = sP[kk];
-        int32_t dI[4], dJ[4], fI[4], fJ[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            dI[u] = D[(4 * I + u) * npad + kk];
-            dJ[u] = D[(4 * J + u) * npad + kk];
-            fI[u] = F[pI[u] * npad + pk];
-            fJ[u] = F[pJ[u] * npad + pk];
-        }
-        if (sym) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    U[u][v] += dI[u] * fJ[v];
-                    L[v][u] += dJ[v] * fI[u];
-                }
-        } else {
-            int32_t dtI[4], dtJ[4], ftI[4], ftJ[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                dtI[u] = DT[(4 * I + u) * npad + kk];
-                dtJ[u] = DT[(4 * J + u) * npad + kk];
-                ftI[u] = FT[pI[u] * npad + pk];
-                ftJ[u] = FT[pJ[u] * npad + pk];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    U[u][v] += dI[u] * fJ[v] + dtI[u] * ftJ[v];
-                    L[v][u] += dJ[v] * fI[u] + dtJ[v] * ftI[u];
-                }
-        }
-    }
     dead = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 4; ++u) {
+        const int4 a = *reinterpret_cast<const int4 *>(Mi + (size_t)(4 * I + u) * npad + 4 * J);
+        const int4 c = *reinterpret_cast<const int4 *>(Mi + (size_t)(4 * J + u) * npad + 4 * I);
+        U[u][0] = a.x; U[u][1] = a.y; U[u][2] = a.z; U[u][3] = a.w;
+        L[u][0] = c.x; L[u][1] = c.y; L[u][2] = c.z; L[u][3] = c.w;
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int i = 4 * I + u, j = 4 * J + v;
-            if (sym) { U[u][v] *= 2; L[v][u] *= 2; }
-            const int32_t fs = F[pI[u] * npad + pJ[v]] + F[pJ[v] * npad + pI[u]];
-            U[u][v] += D[i * npad + j] * fs + P.dd[i] * P.fd[pJ[v]];
-            L[v][u] += D[j * npad + i] * fs + P.dd[j] * P.fd[pI[u]];
-            const bool pad = (i >= n) || (j >= n);
-            if (pad) { U[u][v] = 1 << 29; L[v][u] = 1 << 29; dead |= 1u << (u * 4 + v); }
-            if (i == j) { U[u][v] = 0; L[v][u] = 0; }
-        }
+        for (int v = 0; v < 4; ++v)
+            if (4 * I + u >= n || 4 * J + v >= n) dead |= 1u << (u * 4 + v);
+    }
 }
 
 #define QAPB_SWITCH4(idx, BODY)            \
@@ -373,7 +321,6 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     V.XR = reinterpret_cast<int32_t *>(smem_raw + lay.offXR);
     V.XS = reinterpret_cast<int32_t *>(smem_raw + lay.offXS);
     int32_t *sP = reinterpret_cast<int32_t *>(smem_raw + lay.offP);
-    unsigned *sJ = reinterpret_cast<unsigned *>(smem_raw + lay.offJ);
     long long *sRed64 = reinterpret_cast<long long *>(smem_raw + lay.offRedD);
     int32_t *sRedD = reinterpret_cast<int32_t *>(smem_raw + lay.offRedD);
     unsigned *sRedK = reinterpret_cast<unsigned *>(smem_raw + lay.offRedK);
@@ -392,51 +339,21 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     const int one = P.one, sixteen = P.sixteen;
 
     // ---------------------------------------------------------------- setup
+    // start permutation, stream state, M and h come from qap_start_kernel / qap_build_m_kernel
     for (int i = tid; i < npad; i += T) {
-        V.A[i] = 0; V.C[i] = 0; V.B[i] = 0; V.E[i] = 0; V.H[i] = 0;
+        V.A[i] = 0; V.C[i] = 0; V.B[i] = 0; V.E[i] = 0;
         V.ColR[i] = 0; V.ColS[i] = 0; V.TR[i] = 0; V.TS[i] = 0; V.XR[i] = 0; V.XS[i] = 0;
-        sP[i] = (P.rng || i >= n) ? (i < n ? i : 0) : (int32_t)P.perms[(size_t)b * n + i];
+        V.H[i] = P.initH[(size_t)b * npad + i];
+        sP[i] = P.perm32[(size_t)b * npad + i];
     }
-    unsigned long long rng_state = 0;
-    if (P.rng) {
-        // multistart.py:88: state = derive_seed(master, index); core.py:81-87 shuffle.  Draws are
-        // computed in parallel assuming no rejection; a rejection (probability ~ n^2/2^64) falls
-        // back to the exact sequential loop.
-        const unsigned long long seed = mix64(P.master_seed + QAPB_GAMMA * (P.first_index + (unsigned long long)b + 1ULL));
-        int reject = P.force_seq_rng;
-        for (int k = tid; k < n - 1; k += T) {
-            unsigned long long bound = (unsigned long long)(n - 1 - k) + 1ULL;
-            unsigned long long r = mix64(seed + QAPB_GAMMA * ((unsigned long long)k + 1ULL));
-            unsigned long long rem = (0ULL - bound) % bound;
-            if (r > ~0ULL - rem) reject = 1;
-            sJ[n - 1 - k] = (unsigned)(r % bound);
-        }
-        reject = __syncthreads_or(reject);
-        if (tid == 0) {
-            rng_state = seed;
-            if (reject) {
-                for (int i = n - 1; i >= 1; --i) {
-                    unsigned j = (unsigned)randbelow_seq(rng_state, (unsigned long long)i + 1ULL);
-                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
-                }
-            } else {
-                for (int i = n - 1; i >= 1; --i) {
-                    unsigned j = sJ[i];
-                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
-                }
-                rng_state = seed + QAPB_GAMMA * (unsigned long long)(n - 1);
-            }
-            sMisc[2] = (long long)rng_state;
-        }
-    }
+    unsigned long long rng_state = P.rng ? P.start_state[b] : 0ULL;
     if (P.cells) {
         int64_t *cz = P.cells + (size_t)b * n * n;
         for (int i = tid; i < n * n; i += T) cz[i] = 0;
     }
     __syncthreads();
-    if (P.rng) rng_state = (unsigned long long)sMisc[2];
 
-    long long cost;
+    long long cost;  // _kernels.pyx:18-24, int64, including the diagonal products
     {
         long long part = 0;
         for (int idx = tid; idx < n * n; idx += T) {
@@ -447,19 +364,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         cost = block_sum_i64(part, sRed64, tid, T);
         __syncthreads();
     }
-    for (int i = tid; i < n; i += T) {
-        int pi = sP[i];
-        int32_t acc = P.dd[i] * P.fd[pi];
-        if (SYM) {
-            for (int k = 0; k < n; ++k) acc += 2 * (D[i * npad + k] * F[pi * npad + sP[k]]);
-        } else {
-            for (int k = 0; k < n; ++k) {
-                int pk = sP[k];
-                acc += D[i * npad + k] * F[pi * npad + pk] + DT[i * npad + k] * FT[pi * npad + pk];
-            }
-        }
-        V.H[i] = acc;
-    }
+    const int32_t *__restrict__ Minit = P.initM + (size_t)b * npad * npad;
 
     // ---- unit ownership.  tb = mask of pairs that are tabu now (pads / non-pairs permanently
     // set, expiry MAXV), mexp = earliest expiry among the clearable bits.
@@ -479,7 +384,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         if (k == 0 && diag) { I[0] = tid - Toff; J[0] = I[0]; uidv[0] = noff + I[0]; own[0] = true; }
         if (own[k]) {
             unsigned dead;
-            build_unit(P, sP, I[k], J[k], SYM, U[k], L[k], dead);
+            load_unit(Minit, npad, n, I[k], J[k], U[k], L[k], dead);
             if (diag) dead |= 0xF731u;  // slots with u >= v are not pairs of a diagonal block
             tb[k] = dead;
 #pragma unroll
@@ -493,7 +398,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 int32_t Us[4][4], Ls[4][4];
                 unsigned dead;
                 const int Ik = P.unit_ij[uid] & 0xff, Jk = P.unit_ij[uid] >> 8;
-                build_unit(P, sP, Ik, Jk, SYM, Us, Ls, dead);
+                load_unit(Minit, npad, n, Ik, Jk, Us, Ls, dead);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     st_row(sM, k2 * 8 + u, Toff, tid, Us[u]);

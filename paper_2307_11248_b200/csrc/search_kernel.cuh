@@ -102,6 +102,9 @@ struct SearchParams {
     long long *dbg;                  // optional phase-cycle counters (development), else null
     SmemLayout lay;                  // generic kernel: offsets live in the constant bank
     HybLayout hlay;                  // hybrid kernel
+    const int32_t *perm32;           // hybrid: [B,npad] start permutations (qap_start_kernel)
+    const unsigned long long *start_state;  // hybrid: [B] SplitMix64 state after the shuffle
+    const int32_t *initM, *initH;    // hybrid: [B,npad,npad], [B,npad] from qap_build_m_kernel
     int toff, us, exp_in_smem;       // hybrid plan: off-diagonal threads, shared-memory units per thread
 };
 
