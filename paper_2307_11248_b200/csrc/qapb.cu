@@ -40,6 +40,7 @@ struct qapb_handle {
     int lb_class = 0;  // 0: <=384 threads, 2 CTAs/SM register budget; 1: <=512 threads
     int g_threads = 0, g_upt = 0, g_lb_class = 0;  // generic-kernel plan (all_deltas on hybrid handles)
     int toff = 0, us = 0, exp_in_smem = 1;         // hybrid plan
+    int staged = 0, fits_i16 = 0;                  // int16 copies of D/F staged in shared memory
     unsigned smem_bytes = 0;
     int ctas_per_sm = 0, sm_count = 0;
     long long delta_bound = 0;
@@ -70,22 +71,23 @@ static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
     return tab[acc_bits == 64][storage][lb_class];
 }
 
-static kern_t pick_hybrid_kernel(int symmetric, int packed, int ur, int smemu)
+static kern_t pick_hybrid_kernel(int symmetric, int packed, int plan)
 {
-    // register-only plans (n <= 128): 80 registers/thread, two 352-thread CTAs per SM at n = 100;
-    // plans with shared-memory units: 128 registers/thread (one 512-thread CTA per SM at n = 256)
-#define KH(S, PK, UP, SM) (kern_t) qap_search_hybrid_kernel<S, PK, UP, SM, (SM ? 128 : (UP == 2 ? 104 : 80))>
-#define KH4(S, PK) {{KH(S, PK, 1, false), KH(S, PK, 1, true)}, {KH(S, PK, 2, false), KH(S, PK, 2, true)}}
-    static kern_t tab[2][2][2][2] = {{KH4(false, false), KH4(false, true)}, {KH4(true, false), KH4(true, true)}};
-#undef KH4
+    // plan 0: register-only (n <= 128), 80 registers/thread (two 352-thread CTAs per SM at n = 100)
+    // plan 1: the same with int16 copies of D and F staged in shared memory
+    // plan 2: two register units + shared-memory units per thread, 128 registers (n <= 256)
+#define KH(S, PK) {(kern_t) qap_search_hybrid_kernel<S, PK, 1, false, false, 80>, \
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, true, 80>,  \
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128>}
+    static kern_t tab[2][2][3] = {{KH(false, false), KH(false, true)}, {KH(true, false), KH(true, true)}};
 #undef KH
-    return tab[symmetric != 0][packed != 0][ur - 1][smemu != 0];
+    return tab[symmetric != 0][packed != 0][plan];
 }
 static kern_t handle_kernel(const qapb_handle *h)
 {
     // packed (delta, slot) keys need |delta|*16 + 15 < 2^31
     const int packed = h->delta_bound < ((1LL << 27) - 1);
-    return h->storage == 3 ? pick_hybrid_kernel(h->symmetric, packed, h->upt, h->us > 0)
+    return h->storage == 3 ? pick_hybrid_kernel(h->symmetric, packed, h->us > 0 ? 2 : (h->staged ? 1 : 0))
                            : pick_kernel(h->acc_bits, h->storage, h->lb_class);
 }
 
@@ -116,6 +118,15 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
         L = make_hyb_layout(h->npad, nb, toff, us, 0);
     }
     if (L.total > smem_cap) return false;
+    if (threads < h->n) return false;  // the publish phase maps one location per thread
+    if ((us > 0) != (ur == 2)) return false;  // only these two kernel shapes are instantiated
+    int staged = 0;
+    if (us == 0 && h->fits_i16 && !getenv("QAPB_NO_STAGE")) {
+        // stage while two CTAs per SM still fit (the register file allows no more at 80 regs x 352 threads)
+        HybLayout Ls = make_hyb_layout(h->npad, nb, toff, us, exp_in_smem, 1, h->symmetric);
+        if (Ls.total <= std::min(smem_cap, 110u * 1024u)) { staged = 1; L = Ls; }
+    }
+    h->staged = staged;
     h->upt = ur; h->toff = toff; h->us = us; h->exp_in_smem = exp_in_smem;
     h->threads = threads;
     h->lb_class = 0;
@@ -258,13 +269,14 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
 
     const int nb = (n + 3) / 4, npad = nb * 4;
     std::vector<long long> F0((size_t)n * n), D0((size_t)n * n), fd(n), dd(n);
-    bool sym = true;
+    bool sym = true, fits16 = true;
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
             long long f = flow[(size_t)i * n + j], d = dist[(size_t)i * n + j];
             if (std::llabs(f) >= (1LL << 30) || std::llabs(d) >= (1LL << 30))
                 return fail(QAPB_ERR_UNSUPPORTED, "matrix entries must satisfy |x| < 2^30");
             if (i == j) { fd[i] = f; dd[i] = d; f = 0; d = 0; }
+            if (std::llabs(f) > 32767 || std::llabs(d) > 32767) fits16 = false;
             F0[(size_t)i * n + j] = f;
             D0[(size_t)i * n + j] = d;
             if (i != j && (flow[(size_t)i * n + j] != flow[(size_t)j * n + i] || dist[(size_t)i * n + j] != dist[(size_t)j * n + i]))
@@ -273,6 +285,7 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
 
     qapb_handle *h = new qapb_handle();
     h->n = n; h->nb = nb; h->npad = npad; h->device = device; h->symmetric = sym ? 1 : 0;
+    h->fits_i16 = fits16 ? 1 : 0;
 
     // accumulator width: |delta| <= 4 * bound must stay below 2^31-1 for the int32 state
     const double lim32 = 2147483647.0 / 4.0 - 8.0;
@@ -478,7 +491,8 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     int threads = h->threads;
     unsigned smem = h->smem_bytes;
     if (h->storage == 3) {
-        P.hlay = make_hyb_layout(h->npad, h->nb, h->toff, h->us, h->exp_in_smem);
+        P.hlay = make_hyb_layout(h->npad, h->nb, h->toff, h->us, h->exp_in_smem, h->staged, h->symmetric);
+        P.staged = h->staged;
         P.toff = h->toff; P.us = h->us; P.exp_in_smem = h->exp_in_smem;
     } else P.lay = make_layout(h->npad, h->nunits, h->threads, h->upt, h->acc_bits / 8, h->storage);
     if (h->storage == 3 && P.mode == MODE_ALL_DELTAS) {

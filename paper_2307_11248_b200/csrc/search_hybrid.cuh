@@ -30,7 +30,8 @@
 
 namespace qapb {
 
-__host__ __device__ inline HybLayout make_hyb_layout(int npad, int nb, int toff, int us, int exp_in_smem)
+__host__ __device__ inline HybLayout make_hyb_layout(int npad, int nb, int toff, int us, int exp_in_smem,
+                                                     int staged = 0, int symmetric = 1)
 {
     HybLayout L;
     unsigned o = 0;
@@ -48,6 +49,11 @@ __host__ __device__ inline HybLayout make_hyb_layout(int npad, int nb, int toff,
     L.offTen = o; o += 4u * TENURE_CHUNK;
     L.offExp = o;
     if (exp_in_smem) o += 64u * (unsigned)(nb * (nb - 1) / 2 + nb);  // tabu expiry per (unit, slot)
+    const unsigned m16 = staged ? align16(2u * (unsigned)npad * (unsigned)npad) : 0u;
+    L.offD16 = o; o += m16;
+    L.offF16 = o; o += m16;
+    L.offDT16 = o; o += symmetric ? 0u : m16;
+    L.offFT16 = o; o += symmetric ? 0u : m16;
     L.total = align16(o);
     return L;
 }
@@ -295,7 +301,7 @@ __device__ __forceinline__ void expire_bits(unsigned &tb, int32_t &mexp, int c, 
     mexp = nm;
 }
 
-template <bool SYM, bool PACKED, int UR, bool SMEMU, int MAXREG>
+template <bool SYM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG>
 __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -337,6 +343,26 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     const int32_t *__restrict__ DT = P.DT;
     const int32_t MAXV = 0x7fffffff;
     const int one = P.one, sixteen = P.sixteen;
+    // STG: int16 copies of D, F (and their transposes when asymmetric) in shared memory, so the
+    // publish phase between the barriers never waits on an L1/L2 miss
+    const int16_t *sD16 = reinterpret_cast<const int16_t *>(smem_raw + lay.offD16);
+    const int16_t *sF16 = reinterpret_cast<const int16_t *>(smem_raw + lay.offF16);
+    const int16_t *sDT16 = SYM ? sD16 : reinterpret_cast<const int16_t *>(smem_raw + lay.offDT16);
+    const int16_t *sFT16 = SYM ? sF16 : reinterpret_cast<const int16_t *>(smem_raw + lay.offFT16);
+    auto ldD = [&](int a, int c2) -> int32_t { return STG ? (int32_t)sD16[a * npad + c2] : D[a * npad + c2]; };
+    auto ldF = [&](int a, int c2) -> int32_t { return STG ? (int32_t)sF16[a * npad + c2] : F[a * npad + c2]; };
+    auto ldDT = [&](int a, int c2) -> int32_t { return STG ? (int32_t)sDT16[a * npad + c2] : DT[a * npad + c2]; };
+    auto ldFT = [&](int a, int c2) -> int32_t { return STG ? (int32_t)sFT16[a * npad + c2] : FT[a * npad + c2]; };
+    if (STG) {
+        int16_t *wD = reinterpret_cast<int16_t *>(smem_raw + lay.offD16);
+        int16_t *wF = reinterpret_cast<int16_t *>(smem_raw + lay.offF16);
+        for (int e = tid; e < npad * npad; e += T) { wD[e] = (int16_t)D[e]; wF[e] = (int16_t)F[e]; }
+        if (!SYM) {
+            int16_t *wDT = reinterpret_cast<int16_t *>(smem_raw + lay.offDT16);
+            int16_t *wFT = reinterpret_cast<int16_t *>(smem_raw + lay.offFT16);
+            for (int e = tid; e < npad * npad; e += T) { wDT[e] = (int16_t)DT[e]; wFT[e] = (int16_t)FT[e]; }
+        }
+    }
 
     // ---------------------------------------------------------------- setup
     // start permutation, stream state, M and h come from qap_start_kernel / qap_build_m_kernel
@@ -359,11 +385,12 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         for (int idx = tid; idx < n * n; idx += T) {
             int i = idx / n, j = idx - i * n;
             int pi = sP[i], pj = sP[j];
-            part += (i == j) ? (long long)P.fd[pi] * P.dd[i] : (long long)F[pi * npad + pj] * D[i * npad + j];
+            part += (i == j) ? (long long)P.fd[pi] * P.dd[i] : (long long)ldF(pi, pj) * ldD(i, j);
         }
         cost = block_sum_i64(part, sRed64, tid, T);
         __syncthreads();
     }
+    int my_pi = tid < n ? sP[tid] : 0;  // unit at location tid, kept in a register (T >= n by plan)
     const int32_t *__restrict__ Minit = P.initM + (size_t)b * npad * npad;
 
     // ---- unit ownership.  tb = mask of pairs that are tabu now (pads / non-pairs permanently
@@ -508,15 +535,16 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
 
         // ---------------- publish: difference vectors of the move (old permutation), additive
         // terms, h'[i] -- one location per thread
-        for (int i = tid; i < n; i += T) {
-            const int pi = sP[i];
+        if (tid < n) {
+            const int i = tid;
+            const int pi = my_pi;
             const bool mid = (i != r) && (i != s);
             if (improved) best_out[i] = (i == r) ? ps : (i == s) ? pr : pi;
             if (SYM) {
                 // D = D^T, F = F^T: a = c, b = e, and the closed forms collapse
-                const int32_t Drs = D[r * npad + s], Fpspr = F[ps * npad + pr];
-                const int32_t Dsi = D[s * npad + i], Dri = D[r * npad + i];
-                const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
+                const int32_t Drs = ldD(r, s), Fpspr = ldF(ps, pr);
+                const int32_t Dsi = ldD(s, i), Dri = ldD(r, i);
+                const int32_t Fpspi = ldF(ps, pi), Fprpi = ldF(pr, pi);
                 const int32_t a = mid ? Dsi - Dri : 0, bb = mid ? Fpspi - Fprpi : 0;
                 const int32_t a2 = 2 * a, b2 = 2 * bb;
                 V.A[i] = a2;
@@ -533,12 +561,12 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                     V.TS[i] = 0;  // tR[s] is written by the owner of the pair
                 }
             } else {
-                const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
-                const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
-                const int32_t Dsi = D[s * npad + i], Dri = D[r * npad + i];
-                const int32_t Dis = DT[s * npad + i], Dir = DT[r * npad + i];
-                const int32_t Fpips = FT[ps * npad + pi], Fpipr = FT[pr * npad + pi];
-                const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
+                const int32_t Drs = ldD(r, s), Dsr = ldD(s, r);
+                const int32_t Fpspr = ldF(ps, pr), Fprps = ldF(pr, ps);
+                const int32_t Dsi = ldD(s, i), Dri = ldD(r, i);
+                const int32_t Dis = ldDT(s, i), Dir = ldDT(r, i);
+                const int32_t Fpips = ldFT(ps, pi), Fpipr = ldFT(pr, pi);
+                const int32_t Fpspi = ldF(ps, pi), Fprpi = ldF(pr, pi);
                 const int32_t a = mid ? Dis - Dir : 0, cc = mid ? Dsi - Dri : 0;
                 const int32_t bb = mid ? Fpips - Fpipr : 0, e = mid ? Fpspi - Fprpi : 0;
                 const int32_t be = bb + e;
@@ -558,11 +586,12 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                     V.TS[i] = 0;
                 }
             }
+            my_pi = (i == r) ? ps : (i == s) ? pr : pi;
         }
         // ---- the thread owning the winning pair: corners, h[r], h[s], tabu memory, trail
         if (my_key == bkey) {
-            const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
-            const int32_t Fpspr = F[ps * npad + pr], Fprps = F[pr * npad + ps];
+            const int32_t Drs = ldD(r, s), Dsr = ldD(s, r);
+            const int32_t Fpspr = ldF(ps, pr), Fprps = ldF(pr, ps);
             const int32_t new_exp = (int32_t)(c + ten);
             int32_t mrs = 0, msr = 0;
             unsigned was = 0;

@@ -73,7 +73,7 @@ __host__ __device__ inline SmemLayout make_layout(int npad, int nunits, int T, i
 
 struct HybLayout {  // search_hybrid.cuh
     unsigned offM, offTB, offMX, offA, offC, offB, offE, offH, offColR, offColS, offTR, offTS, offXR, offXS;
-    unsigned offP, offJ, offRedD, offRedK, offMisc, offTen, offExp, total;
+    unsigned offP, offJ, offRedD, offRedK, offMisc, offTen, offExp, offD16, offF16, offDT16, offFT16, total;
 };
 
 struct SearchParams {
@@ -106,6 +106,7 @@ struct SearchParams {
     const unsigned long long *start_state;  // hybrid: [B] SplitMix64 state after the shuffle
     const int32_t *initM, *initH;    // hybrid: [B,npad,npad], [B,npad] from qap_build_m_kernel
     int toff, us, exp_in_smem;       // hybrid plan: off-diagonal threads, shared-memory units per thread
+    int staged;                      // hybrid: int16 copies of D, F (and transposes) staged in shared memory
 };
 
 // ---- accumulator traits -----------------------------------------------------

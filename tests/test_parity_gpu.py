@@ -54,6 +54,12 @@ def _cases():
     for name in ("nug12", "tai30a", "sko49", "tai64c"):
         inst = shapes.by_name(name)
         out.append((name, inst.flow, inst.distance))
+    # kernel-plan coverage: |delta| >= 2^27 (unpacked argmin keys), entries > 32767 (no int16 staging),
+    # both symmetric and asymmetric
+    out.append(("fuzz-unpacked-asym30",) + _fuzz_instance(30, 7, lo=0, hi=1000))
+    out.append(("fuzz-unpacked-sym23",) + _fuzz_instance(23, 8, symmetric=True, diag=False, lo=0, hi=800))
+    big = _fuzz_instance(30, 9, lo=0, hi=6)
+    out.append(("fuzz-nostage-asym30", big[0] * 9000, big[1]))
     return out
 
 
@@ -148,10 +154,12 @@ def test_batched_runs_match_single(q, orc):
         assert costs[b] == orc.full_cost(inst.flow, inst.distance, perms[b])
 
 
-@pytest.mark.parametrize("shape,iters,starts", [("tai100a", 40, 3), ("sko100", 40, 2), ("tai150b", 24, 2), ("tai256c", 8, 2)])
+@pytest.mark.parametrize("shape,iters,starts", [("tai100a", 40, 3), ("sko100", 40, 2), ("rand100", 30, 2), ("tai128a", 24, 2),
+                                                ("rand160", 16, 2), ("tai150b", 24, 2), ("tai256c", 8, 2)])
 def test_large_shapes_short_runs(q, orc, shape, iters, starts):
-    """BASELINE.json configs 3-5 at oracle-affordable iteration counts: int32 state in
-    shared memory (n=100), int64 state (tai150b), L2-resident state (n=256)."""
+    """BASELINE.json configs 3-5 at oracle-affordable iteration counts, one case per kernel plan:
+    register-only (n=100 symmetric / asymmetric, n=128), registers + shared memory (n=160
+    asymmetric, n=256), int64 state in the generic kernel (tai150b)."""
     from paper_2307_11248_b200 import shapes
     from paper_2307_11248_b200.backend import device_instance
 
