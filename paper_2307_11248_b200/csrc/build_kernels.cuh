@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
     const int tid = threadIdx.x;
     const int n = P.n, npad = P.npad;
     const int tiles = (npad + BT - 1) / BT;
-    const int b = blockIdx.y, ti = blockIdx.x / tiles, tj = blockIdx.x % tiles;
+    const int b = blockIdx.x / (tiles * tiles), tt = blockIdx.x % (tiles * tiles);  // batch on grid.x (no 65535 limit)
+    const int ti = tt / tiles, tj = tt % tiles;
     const int i0 = ti * BT, j0 = tj * BT;
     const int32_t *perm = P.perm32 + (size_t)b * npad;
     for (int i = tid; i < npad; i += 256) sPerm[i] = perm[i];
@@ -173,6 +174,23 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
     }
     if (ti == 0 && tj == 0)
         for (int i = n + tid; i < npad; i += 256) P.h[(size_t)b * npad + i] = 0;
+}
+
+// kernels.all_deltas (_kernels.pyx:58-70) from M and h: out[b][k] = M[i][j] + M[j][i] - h[i] - h[j]
+// for the n(n-1)/2 moves in lexicographic (i, j) order, widened to int64.
+__global__ void __launch_bounds__(256) qap_emit_deltas_kernel(int n, int npad, const int32_t *__restrict__ M,
+                                                              const int32_t *__restrict__ h, int64_t *__restrict__ out)
+{
+    const int b = blockIdx.x;
+    const int32_t *Mb = M + (size_t)b * npad * npad;
+    const int32_t *hb = h + (size_t)b * npad;
+    int64_t *ob = out + (size_t)b * ((size_t)n * (n - 1) / 2);
+    for (int i = blockIdx.y; i < n - 1; i += gridDim.y) {
+        const size_t row0 = (size_t)i * n - ((size_t)i * (i + 1)) / 2 - (size_t)(i + 1);  // + j gives the index
+        const int32_t hi = hb[i];
+        for (int j = i + 1 + threadIdx.x; j < n; j += blockDim.x)
+            ob[row0 + j] = (int64_t)(Mb[(size_t)i * npad + j] + Mb[(size_t)j * npad + i] - hi - hb[j]);
+    }
 }
 
 }  // namespace qapb

@@ -522,7 +522,7 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
         BP.M = (int32_t *)((char *)h->ws + offInitM);
         BP.h = (int32_t *)((char *)h->ws + offInitH);
         const int tiles = (h->npad + BT - 1) / BT;
-        qap_build_m_kernel<<<dim3(tiles * tiles, batch), 256, np * sizeof(int32_t), st>>>(BP);
+        qap_build_m_kernel<<<(unsigned)(tiles * tiles) * (unsigned)batch, 256, np * sizeof(int32_t), st>>>(BP);
         CU(cudaGetLastError());
         P.perm32 = SP.perm32; P.start_state = SP.state; P.initM = BP.M; P.initH = BP.h;
     }
@@ -557,6 +557,34 @@ extern "C" int qapb_all_deltas(qapb_handle *h, const int64_t *perms, int batch, 
     int rc = check_common(h, batch);
     if (rc) return rc;
     if (!perms || !deltas) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    if (h->storage == 3) {
+        // int32 plans: the full evaluator as a tiled contraction (qap_build_m_kernel) + emission
+        cudaStream_t st = (cudaStream_t)stream;
+        const size_t np = (size_t)h->npad;
+        const size_t szPerm = (np * 4 * batch + 255) / 256 * 256, szState = ((size_t)8 * batch + 255) / 256 * 256;
+        rc = ensure_ws(h, 2 * szPerm + szState + np * np * 4 * batch + 256);
+        if (rc) return rc;
+        StartParams SP;
+        SP.n = h->n; SP.npad = h->npad; SP.rng = 0; SP.force_seq_rng = 0; SP.master_seed = 0; SP.first_index = 0;
+        SP.perms = perms;
+        SP.perm32 = (int32_t *)h->ws;
+        SP.state = (unsigned long long *)((char *)h->ws + szPerm);
+        BuildParams BP;
+        BP.n = h->n; BP.npad = h->npad; BP.symmetric = h->symmetric;
+        BP.F = h->dF; BP.FT = h->dFT; BP.D = h->dD; BP.DT = h->dDT; BP.fd = h->dfd; BP.dd = h->ddd;
+        BP.perm32 = SP.perm32;
+        BP.h = (int32_t *)((char *)h->ws + szPerm + szState);
+        BP.M = (int32_t *)((char *)h->ws + 2 * szPerm + szState);
+        CU(cudaEventRecord(h->ev0, st));
+        qap_start_kernel<<<batch, 128, 2 * np * sizeof(int32_t), st>>>(SP);
+        const int tiles = (h->npad + BT - 1) / BT;
+        qap_build_m_kernel<<<(unsigned)(tiles * tiles) * (unsigned)batch, 256, np * sizeof(int32_t), st>>>(BP);
+        qap_emit_deltas_kernel<<<dim3(batch, std::min(h->n - 1, 64)), 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
+        CU(cudaGetLastError());
+        CU(cudaEventRecord(h->ev1, st));
+        h->have_timing = 1;
+        return QAPB_OK;
+    }
     SearchParams P;
     base_params(h, P);
     P.mode = MODE_ALL_DELTAS;
