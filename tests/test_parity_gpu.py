@@ -252,3 +252,60 @@ def test_error_mapping(q):
         q.kernels.two_opt_run(inst.flow, inst.distance, np.arange(5), 0)
     with pytest.raises(q.DomainError):
         q.full_cost(inst, np.arange(4))
+
+
+def test_randomized_sweep(q, orc):
+    """Property sweep in the spirit of test_core.py:76-89 / test_acceptance.py:54-69: random sizes,
+    value ranges, symmetry and diagonals; deltas == oracle, run trajectories == oracle."""
+    rs = np.random.default_rng(20240824)
+    for case in range(40):
+        n = int(rs.integers(2, 41))
+        hi = int(rs.choice([3, 50, 400, 5000]))
+        f = rs.integers(-hi if case % 4 == 0 else 0, hi + 1, (n, n)).astype(np.int64)
+        d = rs.integers(0, hi + 1, (n, n)).astype(np.int64)
+        if case % 3 == 0:
+            f, d = f + f.T, d + d.T
+        if case % 2 == 0:
+            np.fill_diagonal(f, 0)
+            np.fill_diagonal(d, 0)
+        rng = orc.Rng(1000 + case)
+        perm = rng.permutation(n)
+        iters = 25
+        lo, hi_t = orc.tenure_bounds(n)
+        ten = rng.tenures(lo, hi_t, iters)
+        assert np.array_equal(q.kernels.all_deltas(f, d, perm), orc.all_deltas(f, d, perm)), case
+        got, want = q.kernels.tabu_run(f, d, perm, iters, ten), orc.tabu_run(f, d, perm, iters, ten)
+        for g, w in zip(got[:7], want[:7]):
+            assert np.array_equal(g, w), case
+        for g, w in zip(got[7], want[7]):
+            assert np.array_equal(g, w), case
+        got, want = q.kernels.two_opt_run(f, d, perm, iters), orc.two_opt_run(f, d, perm, iters)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w), case
+
+
+def test_exhaustive_solve_small(q, orc):
+    """core.exhaustive_solve (core.py:90-108) with GPU-batched costs == brute force with the oracle."""
+    import itertools
+
+    from paper_2307_11248_b200 import shapes
+
+    inst = shapes.rand(6, 21)
+    perm, cost = q.exhaustive_solve(inst)
+    best = min((orc.full_cost(inst.flow, inst.distance, np.array(p)), p) for p in itertools.permutations(range(6)))
+    assert cost == best[0] and tuple(perm.tolist()) == best[1]
+    # oracle-quality check of test_acceptance.py:73-91: tabu multi-start reaches the optimum on n=6
+    res = q.run_multistart(inst, q.SearchConfig(algorithm="tabu", n_starts=32, iterations=48, master_seed=2))
+    assert res.best.cost == cost
+
+
+def test_tabu_not_worse_than_two_opt_and_dominance(q):
+    """test_acceptance.py:123-137,194-202: more starts never hurt (subset dominance) and the
+    per-start vector of a larger run extends the smaller one."""
+    from paper_2307_11248_b200 import shapes
+
+    inst = shapes.rand(20, 5)
+    small = q.run_multistart(inst, q.SearchConfig(algorithm="tabu", n_starts=16, iterations=80, master_seed=4))
+    large = q.run_multistart(inst, q.SearchConfig(algorithm="tabu", n_starts=64, iterations=80, master_seed=4))
+    assert large.best.cost <= small.best.cost
+    assert np.array_equal(large.per_start_costs[:16], small.per_start_costs)
