@@ -120,6 +120,7 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
     if (L.total > smem_cap) return false;
     if (threads < h->n) return false;  // the publish phase maps one location per thread
     if ((us > 0) != (ur == 2)) return false;  // only these two kernel shapes are instantiated
+    if ((us > 0) != (h->npad > 128)) return false;  // layout size class (NPADMAX 128 / 256) is tied to the shape
     int staged = 0;
     if (us == 0 && h->fits_i16 && !getenv("QAPB_NO_STAGE")) {
         // stage while two CTAs per SM still fit (the register file allows no more at 80 regs x 352 threads)
@@ -430,11 +431,11 @@ extern "C" int qapb_get_info(const qapb_handle *h, qapb_info *info)
 
 // development hook (not in the public header): phase-cycle counters of CTA 0 of the next launches
 static long long *g_dbg = nullptr;
-extern "C" int qapb_debug_phase_cycles(long long *out15)
+extern "C" int qapb_debug_phase_cycles(long long *out18)
 {
-    if (!g_dbg) { if (cudaMalloc(&g_dbg, 15 * sizeof(long long)) != cudaSuccess) return QAPB_ERR_NOMEM; cudaMemset(g_dbg, 0, 15 * sizeof(long long)); return QAPB_OK; }
+    if (!g_dbg) { if (cudaMalloc(&g_dbg, 18 * sizeof(long long)) != cudaSuccess) return QAPB_ERR_NOMEM; cudaMemset(g_dbg, 0, 18 * sizeof(long long)); return QAPB_OK; }
     cudaDeviceSynchronize();
-    cudaMemcpy(out15, g_dbg, 15 * sizeof(long long), cudaMemcpyDeviceToHost);
+    cudaMemcpy(out18, g_dbg, 18 * sizeof(long long), cudaMemcpyDeviceToHost);
     return QAPB_OK;
 }
 

@@ -30,25 +30,34 @@
 
 namespace qapb {
 
+// Shared-memory layout.  The n-vectors and the small reduction / tenure buffers sit at offsets that
+// depend only on the size class NPADMAX (128 or 256), so the kernel addresses them with immediates
+// (HYB_* below) instead of recomputing bases from the constant bank in every phase; the big,
+// rarely-addressed regions (expiries, staged matrices, shared-memory units) follow at runtime offsets.
+#define HYB_VEC(k, NPM) ((k) * 4 * (NPM))               /* A,C,B,E,H,ColR,ColS,TR,TS,XR,XS,P,J: k = 0..12 */
+#define HYB_REDD(NPM) (13 * 4 * (NPM))
+#define HYB_REDK(NPM) (HYB_REDD(NPM) + 32 * 8 + 16)
+#define HYB_MISC(NPM) (HYB_REDK(NPM) + 32 * 4)
+#define HYB_TEN(NPM) (HYB_MISC(NPM) + 64)
+#define HYB_FIXED_END(NPM) (HYB_TEN(NPM) + 4 * TENURE_CHUNK)
+
 __host__ __device__ inline HybLayout make_hyb_layout(int npad, int nb, int toff, int us, int exp_in_smem,
                                                      int staged = 0, int symmetric = 1)
 {
     HybLayout L;
-    unsigned o = 0;
-    const unsigned v = 4u * (unsigned)npad;
+    const unsigned npm = npad <= 128 ? 128u : 256u;
+    L.offA = HYB_VEC(0, npm); L.offC = HYB_VEC(1, npm); L.offB = HYB_VEC(2, npm); L.offE = HYB_VEC(3, npm);
+    L.offH = HYB_VEC(4, npm); L.offColR = HYB_VEC(5, npm); L.offColS = HYB_VEC(6, npm); L.offTR = HYB_VEC(7, npm);
+    L.offTS = HYB_VEC(8, npm); L.offXR = HYB_VEC(9, npm); L.offXS = HYB_VEC(10, npm); L.offP = HYB_VEC(11, npm);
+    L.offJ = HYB_VEC(12, npm);
+    L.offRedD = HYB_REDD(npm); L.offRedK = HYB_REDK(npm); L.offMisc = HYB_MISC(npm); L.offTen = HYB_TEN(npm);
+    unsigned o = align16(HYB_FIXED_END(npm));
+    L.offExp = o;
+    if (exp_in_smem) o += 64u * (unsigned)(nb * (nb - 1) / 2 + nb);  // tabu expiry per (unit, slot)
+    o = align16(o);
     L.offM = o; o += (unsigned)us * 8u * (unsigned)toff * 16u;
     L.offTB = o; o += align16(4u * (unsigned)us * (unsigned)toff);
     L.offMX = o; o += align16(4u * (unsigned)us * (unsigned)toff);
-    L.offA = o; o += v; L.offC = o; o += v; L.offB = o; o += v; L.offE = o; o += v; L.offH = o; o += v;
-    L.offColR = o; o += v; L.offColS = o; o += v; L.offTR = o; o += v; L.offTS = o; o += v;
-    L.offXR = o; o += v; L.offXS = o; o += v;
-    L.offP = o; o += v; L.offJ = o; o += v;
-    L.offRedD = o; o += 32u * 8u + 16u;
-    L.offRedK = o; o += 32u * 4u;
-    L.offMisc = o; o += 64u;
-    L.offTen = o; o += 4u * TENURE_CHUNK;
-    L.offExp = o;
-    if (exp_in_smem) o += 64u * (unsigned)(nb * (nb - 1) / 2 + nb);  // tabu expiry per (unit, slot)
     const unsigned m16 = staged ? align16(2u * (unsigned)npad * (unsigned)npad) : 0u;
     L.offD16 = o; o += m16;
     L.offF16 = o; o += m16;
@@ -125,37 +134,43 @@ __device__ __forceinline__ void unit_update(int32_t (&U)[4][4], int32_t (&L)[4][
                 L[v][u] -= aJ[v] * bI[u] + cJ[v] * eI[u];
             }
     }
-    if (Ik == R || Jk == R || Ik == S || Jk == S) {
-        if (Ik == R) {
+    // Rows / columns r and s.  Block row I == R holds row r in U and column r in L; block column
+    // J == R holds row r in L and column r in U (I == R and J == R exclude each other).  r & 3 is
+    // uniform, so the register index is chosen by a uniform switch *outside* the per-thread test:
+    // one divergent region per moved location instead of two.
+    {
+        const bool hI = Ik == R, hJ = Jk == R;
+        if (hI | hJ) {
+            const int o = hI ? Jk : Ik;
             int32_t x[4], cs[4], t[4];
-            ld_vec4(V.XR, Jk, x); ld_vec4(V.ColS, Jk, cs); ld_vec4(V.TR, Jk, t);
+            ld_vec4(V.XR, o, x); ld_vec4(V.ColS, o, cs); ld_vec4(V.TR, o, t);
             QAPB_SWITCH4(ru, {
 _Pragma("unroll")
-                for (int v = 0; v < 4; ++v) { U[q][v] += x[v]; L[v][q] = cs[v] + t[v]; }
+                for (int w = 0; w < 4; ++w) {
+                    const int32_t nv = cs[w] + t[w];
+                    U[q][w] += hI ? x[w] : 0;
+                    L[w][q] = hI ? nv : L[w][q];
+                    L[q][w] += hJ ? x[w] : 0;
+                    U[w][q] = hJ ? nv : U[w][q];
+                }
             })
         }
-        if (Jk == R) {
-            int32_t x[4], cs[4], t[4];
-            ld_vec4(V.XR, Ik, x); ld_vec4(V.ColS, Ik, cs); ld_vec4(V.TR, Ik, t);
-            QAPB_SWITCH4(ru, {
-_Pragma("unroll")
-                for (int u = 0; u < 4; ++u) { L[q][u] += x[u]; U[u][q] = cs[u] + t[u]; }
-            })
-        }
-        if (Ik == S) {
+    }
+    {
+        const bool hI = Ik == S, hJ = Jk == S;
+        if (hI | hJ) {
+            const int o = hI ? Jk : Ik;
             int32_t x[4], cr[4], t[4];
-            ld_vec4(V.XS, Jk, x); ld_vec4(V.ColR, Jk, cr); ld_vec4(V.TS, Jk, t);
+            ld_vec4(V.XS, o, x); ld_vec4(V.ColR, o, cr); ld_vec4(V.TS, o, t);
             QAPB_SWITCH4(su, {
 _Pragma("unroll")
-                for (int v = 0; v < 4; ++v) { U[q][v] += x[v]; L[v][q] = cr[v] + t[v]; }
-            })
-        }
-        if (Jk == S) {
-            int32_t x[4], cr[4], t[4];
-            ld_vec4(V.XS, Ik, x); ld_vec4(V.ColR, Ik, cr); ld_vec4(V.TS, Ik, t);
-            QAPB_SWITCH4(su, {
-_Pragma("unroll")
-                for (int u = 0; u < 4; ++u) { L[q][u] += x[u]; U[u][q] = cr[u] + t[u]; }
+                for (int w = 0; w < 4; ++w) {
+                    const int32_t nv = cr[w] + t[w];
+                    U[q][w] += hI ? x[w] : 0;
+                    L[w][q] = hI ? nv : L[w][q];
+                    L[q][w] += hJ ? x[w] : 0;
+                    U[w][q] = hJ ? nv : U[w][q];
+                }
             })
         }
     }
@@ -314,24 +329,25 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     int32_t *sM = reinterpret_cast<int32_t *>(smem_raw + lay.offM);
     unsigned *sTB = reinterpret_cast<unsigned *>(smem_raw + lay.offTB);
     int32_t *sMX = reinterpret_cast<int32_t *>(smem_raw + lay.offMX);
+    constexpr int NPM = SMEMU ? 256 : 128;  // size class of the plan (host: make_hyb_layout)
     Vecs V;
-    V.A = reinterpret_cast<int32_t *>(smem_raw + lay.offA);
-    V.C = reinterpret_cast<int32_t *>(smem_raw + lay.offC);
-    V.B = reinterpret_cast<int32_t *>(smem_raw + lay.offB);
-    V.E = reinterpret_cast<int32_t *>(smem_raw + lay.offE);
-    V.H = reinterpret_cast<int32_t *>(smem_raw + lay.offH);
-    V.ColR = reinterpret_cast<int32_t *>(smem_raw + lay.offColR);
-    V.ColS = reinterpret_cast<int32_t *>(smem_raw + lay.offColS);
-    V.TR = reinterpret_cast<int32_t *>(smem_raw + lay.offTR);
-    V.TS = reinterpret_cast<int32_t *>(smem_raw + lay.offTS);
-    V.XR = reinterpret_cast<int32_t *>(smem_raw + lay.offXR);
-    V.XS = reinterpret_cast<int32_t *>(smem_raw + lay.offXS);
-    int32_t *sP = reinterpret_cast<int32_t *>(smem_raw + lay.offP);
-    long long *sRed64 = reinterpret_cast<long long *>(smem_raw + lay.offRedD);
-    int32_t *sRedD = reinterpret_cast<int32_t *>(smem_raw + lay.offRedD);
-    unsigned *sRedK = reinterpret_cast<unsigned *>(smem_raw + lay.offRedK);
-    long long *sMisc = reinterpret_cast<long long *>(smem_raw + lay.offMisc);
-    int32_t *sTen = reinterpret_cast<int32_t *>(smem_raw + lay.offTen);
+    V.A = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(0, NPM));
+    V.C = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(1, NPM));
+    V.B = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(2, NPM));
+    V.E = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(3, NPM));
+    V.H = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(4, NPM));
+    V.ColR = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(5, NPM));
+    V.ColS = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(6, NPM));
+    V.TR = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(7, NPM));
+    V.TS = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(8, NPM));
+    V.XR = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(9, NPM));
+    V.XS = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(10, NPM));
+    int32_t *sP = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(11, NPM));
+    long long *sRed64 = reinterpret_cast<long long *>(smem_raw + HYB_REDD(NPM));
+    int32_t *sRedD = reinterpret_cast<int32_t *>(smem_raw + HYB_REDD(NPM));
+    unsigned *sRedK = reinterpret_cast<unsigned *>(smem_raw + HYB_REDK(NPM));
+    long long *sMisc = reinterpret_cast<long long *>(smem_raw + HYB_MISC(NPM));
+    int32_t *sTen = reinterpret_cast<int32_t *>(smem_raw + HYB_TEN(NPM));
     // expiry iteration per (unit, slot): shared memory when it fits, else the L2-resident workspace
     // (register-only plans always keep it in shared memory, so the pointer stays in the shared window)
     int32_t *xp = (!SMEMU || P.exp_in_smem) ? reinterpret_cast<int32_t *>(smem_raw + lay.offExp)
@@ -450,7 +466,11 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     for (int i = tid; i < n; i += T) best_out[i] = sP[i];
     int R = -1, S = -1, ru = 0, su = 0;  // previous move (block and in-block indices)
 
+    long long tacc[6] = {0, 0, 0, 0, 0, 0};
+    const bool timing = P.dbg != nullptr && b == 0 && (tid == 0 || tid == 128 || tid == Toff);
     for (int c = 1; c <= iters; ++c) {
+        long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0;
+        if (timing) tA = clock64();
         long long ten = 0;
         if (tabu) {
             if (!P.rng) {
@@ -511,6 +531,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             }
         }
 
+        if (timing) tB = clock64();
         int32_t bd = my_d;
         unsigned bkey = my_key;
         warp_argmin(bd, bkey);
@@ -532,6 +553,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         steps_done = c;
         R = r >> 2; S = s >> 2; ru = r & 3; su = s & 3;
         const int pr = sP[r], ps = sP[s];
+        if (timing) tC = clock64() + (pr & 0);
 
         // ---------------- publish: difference vectors of the move (old permutation), additive
         // terms, h'[i] -- one location per thread
@@ -588,6 +610,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             }
             my_pi = (i == r) ? ps : (i == s) ? pr : pi;
         }
+        if (timing) tD = clock64();
         // ---- the thread owning the winning pair: corners, h[r], h[s], tabu memory, trail
         if (my_key == bkey) {
             const int32_t Drs = ldD(r, s), Dsr = ldD(s, r);
@@ -636,6 +659,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 cz[(size_t)s * n + r] += 1;
             }
         }
+        if (timing) tE = clock64();
         // ---- owners of columns r and s publish them (colR[r] = colS[s] = 0 by the diagonal lanes),
         // and tabu bits that expire at the next iteration are cleared here, off the critical path
 #pragma unroll
@@ -643,10 +667,15 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             if (!own[k]) continue;
             const int Ik = I[k], Jk = J[k];
             if (Ik != Jk) {
-                if (Jk == R) { QAPB_SWITCH4(ru, { st_vec4(V.ColR, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]); }) }
-                if (Ik == R) { QAPB_SWITCH4(ru, { st_vec4(V.ColR, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]); }) }
-                if (Jk == S) { QAPB_SWITCH4(su, { st_vec4(V.ColS, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]); }) }
-                if (Ik == S) { QAPB_SWITCH4(su, { st_vec4(V.ColS, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]); }) }
+                // uniform switch on r & 3 / s & 3 outside, per-thread predicated 128-bit stores inside
+                QAPB_SWITCH4(ru, {
+                    if (Jk == R) st_vec4(V.ColR, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]);
+                    if (Ik == R) st_vec4(V.ColR, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]);
+                })
+                QAPB_SWITCH4(su, {
+                    if (Jk == S) st_vec4(V.ColS, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]);
+                    if (Ik == S) st_vec4(V.ColS, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]);
+                })
             } else {
                 if (Ik == R) {
                     QAPB_SWITCH4(ru, { st_vec4(V.ColR, Ik, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
@@ -679,8 +708,17 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 }
             }
         }
+        if (timing) tF = clock64();
         __syncthreads();  // ---------------------------------------------- sync #2
         if (tid == 0) { sP[r] = ps; sP[s] = pr; }
+        if (timing) {
+            const long long tG = clock64() + (sP[0] & 0);
+            tacc[0] += tB - tA; tacc[1] += tC - tB; tacc[2] += tD - tC; tacc[3] += tE - tD; tacc[4] += tF - tE; tacc[5] += tG - tF;
+        }
+    }
+    if (timing) {
+        const int slot = tid == 0 ? 0 : (tid == 128 ? 1 : 2);
+        for (int q = 0; q < 6; ++q) P.dbg[slot * 6 + q] = tacc[q];
     }
     __syncthreads();
 

@@ -1,4 +1,4 @@
-"""Per-phase cycle counters of CTA 0 (development aid)."""
+"""Per-phase cycle counters of CTA 0 of the hybrid search kernel (development aid)."""
 import ctypes, sys
 sys.path.insert(0, ".")
 import numpy as np
@@ -14,16 +14,14 @@ di = device_instance(inst.flow, inst.distance)
 t = q.tenure_bounds(inst.n)
 L = _lib.lib()
 L.qapb_debug_phase_cycles.argtypes = [ctypes.c_void_p]
-buf = np.zeros(15, np.int64)
+buf = np.zeros(18, np.int64)
 di.multistart(algo, 0, 0, starts, iters, t.low, t.high)
 L.qapb_debug_phase_cycles(buf.ctypes.data)   # enable
 di.multistart(algo, 1, 0, starts, iters, t.low, t.high)
 ms = di.last_kernel_ms()
 L.qapb_debug_phase_cycles(buf.ctypes.data)   # read
-names = ["pass", "wait1", "reduce+book", "winner/publish/vector", "wait2"]
+names = ["pass", "reduce+bar1+book", "vector", "winner", "publish+expire", "bar2"]
 print(f"{shape} starts={starts} iters={iters} {algo}: {ms:.3f} ms  ({ms*1e3/iters:.2f} us/iter)")
-print("  thread0 S split: vector=%.0f winner=%.0f (publish = rest)" % tuple(buf[13:15] / iters))
-print("  thread128 pass split: update=%.0f special=%.0f select=%.0f" % tuple(buf[10:13] / iters))
-for slot, who in enumerate(["thread0 (owner+vector)", "thread128 (owner)"]):
-    v = buf[slot*5:(slot+1)*5] / iters
-    print(f"  {who:24s} " + "  ".join(f"{n}={x:7.0f}" for n, x in zip(names, v)) + f"   total={v.sum():.0f} clk/iter")
+for slot, who in enumerate(["thread0 (owner+vector)", "thread128 (owner)", "diag lane0"]):
+    v = buf[slot*6:(slot+1)*6] / iters
+    print(f"  {who:24s} " + "  ".join(f"{n}={x:6.0f}" for n, x in zip(names, v)) + f"   total={v.sum():.0f} clk/iter")
