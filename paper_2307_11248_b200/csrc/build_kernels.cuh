@@ -71,12 +71,23 @@ struct BuildParams {
     int n, npad, symmetric;
     const int32_t *F, *FT, *D, *DT, *fd, *dd;
     const int32_t *perm32;           // [B,npad]
-    int32_t *M;                      // [B,npad,npad] out (row-major; pads = 2^29, diagonal 0)
-    int32_t *h;                      // [B,npad] out
+    void *M;                         // [B,npad,npad] out (row-major; pads = 2^29 / 2^61, diagonal 0), int32 or int64
+    void *h;                         // [B,npad] out
 };
 
 enum { BT = 64, BK = 32 };
 
+__device__ __forceinline__ void st_acc4(int32_t *dst, const int32_t (&v)[4])
+{
+    *reinterpret_cast<int4 *>(dst) = make_int4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void st_acc4(int64_t *dst, const int64_t (&v)[4])
+{
+    reinterpret_cast<longlong2 *>(dst)[0] = make_longlong2(v[0], v[1]);
+    reinterpret_cast<longlong2 *>(dst)[1] = make_longlong2(v[2], v[3]);
+}
+
+template <typename acc_t>
 __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
 {
     __shared__ __align__(16) int32_t sA[2][BK][BT];  // [term][k][i]
@@ -95,7 +106,7 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
     __syncthreads();
     const bool sym = P.symmetric != 0;
     const int ty = tid >> 4, tx = tid & 15;  // micro-tile rows 4*ty.., cols 4*tx..
-    int32_t acc[4][4];
+    acc_t acc[4][4];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -129,7 +140,7 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] += av[u] * bv[v];
+                for (int v = 0; v < 4; ++v) acc[u][v] += (acc_t)av[u] * (acc_t)bv[v];
             if (!sym) {
                 const int4 a2 = *reinterpret_cast<const int4 *>(&sA[1][k][4 * ty]);
                 const int4 b2 = *reinterpret_cast<const int4 *>(&sB[1][k][4 * tx]);
@@ -137,57 +148,60 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) acc[u][v] += av2[u] * bv2[v];
+                    for (int v = 0; v < 4; ++v) acc[u][v] += (acc_t)av2[u] * (acc_t)bv2[v];
             }
         }
         __syncthreads();
     }
     // epilogue: direct term, diagonal products, pads, h on the diagonal
-    int32_t *Mb = P.M + (size_t)b * npad * npad;
+    acc_t *Mb = reinterpret_cast<acc_t *>(P.M) + (size_t)b * npad * npad;
+    acc_t *hb = reinterpret_cast<acc_t *>(P.h) + (size_t)b * npad;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int i = i0 + 4 * ty + u;
         if (i >= npad) continue;
-        int32_t out[4];
+        acc_t out[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int j = j0 + 4 * tx + v;
-            int32_t val = sym ? 2 * acc[u][v] : acc[u][v];
+            acc_t val = sym ? 2 * acc[u][v] : acc[u][v];
             if (j < npad) {
                 if (i >= n || j >= n) {
-                    val = (i == j) ? 0 : (1 << 29);
+                    val = (i == j) ? (acc_t)0 : Acc<acc_t>::bighalf();
                 } else {
                     const int pi = sPerm[i], pj = sPerm[j];
                     if (i == j) {
-                        P.h[(size_t)b * npad + i] = val + P.dd[i] * P.fd[pi];
+                        hb[i] = val + (acc_t)P.dd[i] * (acc_t)P.fd[pi];
                         val = 0;
                     } else {
-                        val += P.D[(size_t)i * npad + j] * (P.F[(size_t)pi * npad + pj] + P.F[(size_t)pj * npad + pi]) +
-                               P.dd[i] * P.fd[pj];
+                        val += (acc_t)P.D[(size_t)i * npad + j] *
+                                   ((acc_t)P.F[(size_t)pi * npad + pj] + (acc_t)P.F[(size_t)pj * npad + pi]) +
+                               (acc_t)P.dd[i] * (acc_t)P.fd[pj];
                     }
                 }
             }
             out[v] = val;
         }
         const int jb = j0 + 4 * tx;
-        if (jb < npad) *reinterpret_cast<int4 *>(&Mb[(size_t)i * npad + jb]) = make_int4(out[0], out[1], out[2], out[3]);
+        if (jb < npad) st_acc4(&Mb[(size_t)i * npad + jb], out);
     }
     if (ti == 0 && tj == 0)
-        for (int i = n + tid; i < npad; i += 256) P.h[(size_t)b * npad + i] = 0;
+        for (int i = n + tid; i < npad; i += 256) hb[i] = 0;
 }
 
 // kernels.all_deltas (_kernels.pyx:58-70) from M and h: out[b][k] = M[i][j] + M[j][i] - h[i] - h[j]
 // for the n(n-1)/2 moves in lexicographic (i, j) order, widened to int64.
-__global__ void __launch_bounds__(256) qap_emit_deltas_kernel(int n, int npad, const int32_t *__restrict__ M,
-                                                              const int32_t *__restrict__ h, int64_t *__restrict__ out)
+template <typename acc_t>
+__global__ void __launch_bounds__(256) qap_emit_deltas_kernel(int n, int npad, const void *__restrict__ Mv,
+                                                              const void *__restrict__ hv, int64_t *__restrict__ out)
 {
     const int b = blockIdx.x;
-    const int32_t *Mb = M + (size_t)b * npad * npad;
-    const int32_t *hb = h + (size_t)b * npad;
+    const acc_t *Mb = reinterpret_cast<const acc_t *>(Mv) + (size_t)b * npad * npad;
+    const acc_t *hb = reinterpret_cast<const acc_t *>(hv) + (size_t)b * npad;
     int64_t *ob = out + (size_t)b * ((size_t)n * (n - 1) / 2);
     for (int i = blockIdx.y; i < n - 1; i += gridDim.y) {
         const size_t row0 = (size_t)i * n - ((size_t)i * (i + 1)) / 2 - (size_t)(i + 1);  // + j gives the index
-        const int32_t hi = hb[i];
+        const acc_t hi = hb[i];
         for (int j = i + 1 + threadIdx.x; j < n; j += blockDim.x)
             ob[row0 + j] = (int64_t)(Mb[(size_t)i * npad + j] + Mb[(size_t)j * npad + i] - hi - hb[j]);
     }

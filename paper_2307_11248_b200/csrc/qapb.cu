@@ -38,7 +38,6 @@ struct qapb_handle {
     int acc_bits = 32, symmetric = 0;
     int nunits = 0, noff = 0, threads = 0, upt = 0, storage = 0;
     int lb_class = 0;  // 0: <=384 threads, 2 CTAs/SM register budget; 1: <=512 threads
-    int g_threads = 0, g_upt = 0, g_lb_class = 0;  // generic-kernel plan (all_deltas on hybrid handles)
     int toff = 0, us = 0, exp_in_smem = 1;         // hybrid plan
     int staged = 0, fits_i16 = 0;                  // int16 copies of D/F staged in shared memory
     unsigned smem_bytes = 0;
@@ -59,13 +58,9 @@ typedef void (*kern_t)(const SearchParams);
 static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
 {
 #define K(A, S, MT, MB) (kern_t) qap_search_kernel<A, S, MT, MB>
-    static kern_t tab[2][3][2] = {
-        {{K(int32_t, 0, 384, 2), K(int32_t, 0, 512, 1)},
-         {K(int32_t, 1, 384, 2), K(int32_t, 1, 512, 1)},
-         {K(int32_t, 2, 384, 2), K(int32_t, 2, 512, 1)}},
-        {{K(int64_t, 0, 384, 1), K(int64_t, 0, 512, 1)},
-         {K(int64_t, 1, 384, 1), K(int64_t, 1, 512, 1)},
-         {K(int64_t, 2, 384, 1), K(int64_t, 2, 512, 1)}},
+    static kern_t tab[2][2][2] = {
+        {{K(int32_t, 0, 384, 2), K(int32_t, 0, 512, 1)}, {K(int32_t, 1, 384, 2), K(int32_t, 1, 512, 1)}},
+        {{K(int64_t, 0, 384, 1), K(int64_t, 0, 512, 1)}, {K(int64_t, 1, 384, 1), K(int64_t, 1, 512, 1)}},
     };
 #undef K
     return tab[acc_bits == 64][storage][lb_class];
@@ -78,8 +73,11 @@ static kern_t pick_hybrid_kernel(int symmetric, int packed, int plan)
     // plan 2: two register units + shared-memory units per thread, 128 registers (n <= 256)
 #define KH(S, PK) {(kern_t) qap_search_hybrid_kernel<S, PK, 1, false, false, 80>, \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, true, 80>,  \
-                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128>}
-    static kern_t tab[2][2][3] = {{KH(false, false), KH(false, true)}, {KH(true, false), KH(true, true)}};
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128>,  \
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, false, 112>, \
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, true, 112>, \
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 1, true, false, 80>}
+    static kern_t tab[2][2][6] = {{KH(false, false), KH(false, true)}, {KH(true, false), KH(true, true)}};
 #undef KH
     return tab[symmetric != 0][packed != 0][plan];
 }
@@ -87,7 +85,7 @@ static kern_t handle_kernel(const qapb_handle *h)
 {
     // packed (delta, slot) keys need |delta|*16 + 15 < 2^31
     const int packed = h->delta_bound < ((1LL << 27) - 1);
-    return h->storage == 3 ? pick_hybrid_kernel(h->symmetric, packed, h->us > 0 ? 2 : (h->staged ? 1 : 0))
+    return h->storage == 3 ? pick_hybrid_kernel(h->symmetric, packed, h->us > 0 ? (h->upt == 2 ? 2 : 5) : (h->upt == 2 ? (h->staged ? 4 : 3) : (h->staged ? 1 : 0)))
                            : pick_kernel(h->acc_bits, h->storage, h->lb_class);
 }
 
@@ -119,8 +117,8 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
     }
     if (L.total > smem_cap) return false;
     if (threads < h->n) return false;  // the publish phase maps one location per thread
-    if ((us > 0) != (ur == 2)) return false;  // only these two kernel shapes are instantiated
-    if ((us > 0) != (h->npad > 128)) return false;  // layout size class (NPADMAX 128 / 256) is tied to the shape
+    if (h->npad > 128 && !(us > 0 && ur == 2)) return false;  // layout size class 256 is tied to the (2 + smem) shape
+    if (h->npad <= 128 && us > 0 && ur != 1) return false;
     int staged = 0;
     if (us == 0 && h->fits_i16 && !getenv("QAPB_NO_STAGE")) {
         // stage while two CTAs per SM still fit (the register file allows no more at 80 regs x 352 threads)
@@ -310,6 +308,8 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     h->sm_count = g_attr[device & 63].sm_count;
     const unsigned smem_cap = (unsigned)g_attr[device & 63].smem_optin;
     const int acc_bytes = h->acc_bits / 8;
+    // generic kernel: at most 384 threads, several units per thread (measured: two units per
+    // thread on 384 threads beat one unit per thread on 768 at n = 150, int64 state)
     int upt = (h->nunits + 383) / 384;
     if (upt < 1) upt = 1;
     int threads = ((h->nunits + upt - 1) / upt + 31) / 32 * 32;
@@ -318,19 +318,19 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     h->upt = upt;
     h->threads = threads;
     h->lb_class = threads <= 384 ? 0 : 1;
-    h->g_threads = threads; h->g_upt = upt; h->g_lb_class = h->lb_class;
     int storage = 0;
     const char *force = getenv("QAPB_FORCE_GENERIC");
     if (h->acc_bits == 32 && nb <= 64 && !(force && force[0] == '1') && plan_hybrid(h, smem_cap)) {
         storage = 3;
     } else {
-        const char *fs = getenv("QAPB_FORCE_STORAGE");  // development: 1 or 2
-        if (fs && (fs[0] == '1' || fs[0] == '2')) storage = fs[0] - '0';
-        for (; storage < 3; ++storage) {
-            SmemLayout L = make_layout(npad, h->nunits, threads, upt, acc_bytes, storage);
-            if (L.total <= smem_cap) { h->smem_bytes = L.total; break; }
+        // generic kernel: M in shared memory when it fits, else in an L2-resident workspace
+        const char *fs = getenv("QAPB_FORCE_STORAGE");  // development: 1
+        storage = -1;
+        for (int k = (fs && fs[0] == '1') ? 1 : 0; k < 2; ++k) {
+            SmemLayout L = make_layout(npad, h->nunits, threads, upt, acc_bytes, k);
+            if (L.total <= smem_cap) { h->smem_bytes = L.total; storage = k; break; }
         }
-        if (storage == 3) {
+        if (storage < 0) {
             delete h;
             return fail(QAPB_ERR_UNSUPPORTED, "instance too large for shared-memory vectors");
         }
@@ -460,74 +460,84 @@ static void base_params(const qapb_handle *h, SearchParams &P)
     P.dbg = g_dbg;
 }
 
-// Launch the search kernel for `batch` starts.  `extra_ws` bytes are reserved at
+// Workspace of one launch: [caller head | M (storage 1) | tabu expiries | start permutations |
+// stream states | initial h | initial M], every block 256-byte aligned.
+struct WsPlan {
+    size_t offM, offT, offPerm, offState, offInitH, offInitM, total;
+    size_t m_elems, x_elems;
+};
+static WsPlan plan_ws(const qapb_handle *h, int batch, size_t head)
+{
+    auto up = [](size_t v) { return (v + 255) / 256 * 256; };
+    const size_t acc_bytes = h->acc_bits / 8, np = (size_t)h->npad;
+    WsPlan w;
+    w.m_elems = (size_t)h->upt * 8 * h->threads * 4;
+    w.x_elems = (size_t)h->nunits * 16;
+    size_t o = up(head);
+    w.offM = o;
+    if (h->storage == 1) o += up(w.m_elems * acc_bytes * batch);
+    w.offT = o;
+    if (h->storage != 3 || !h->exp_in_smem) o += up(w.x_elems * sizeof(int32_t) * batch);
+    w.offPerm = o;  o += up(np * 4 * batch);
+    w.offState = o; o += up((size_t)8 * batch);
+    w.offInitH = o; o += up(np * acc_bytes * batch);
+    w.offInitM = o; o += up(np * np * acc_bytes * batch);
+    w.total = o;
+    return w;
+}
+
+// qap_start_kernel + qap_build_m_kernel for `batch` permutations (caller-provided or device-drawn)
+static int launch_build(qapb_handle *h, const WsPlan &w, int batch, int rng, int force_seq, unsigned long long master_seed,
+                        unsigned long long first_index, const int64_t *perms, cudaStream_t st, BuildParams &BP,
+                        StartParams &SP)
+{
+    const size_t np = (size_t)h->npad;
+    SP.n = h->n; SP.npad = h->npad; SP.rng = rng; SP.force_seq_rng = force_seq;
+    SP.master_seed = master_seed; SP.first_index = first_index; SP.perms = perms;
+    SP.perm32 = (int32_t *)((char *)h->ws + w.offPerm);
+    SP.state = (unsigned long long *)((char *)h->ws + w.offState);
+    qap_start_kernel<<<batch, 128, 2 * np * sizeof(int32_t), st>>>(SP);
+    CU(cudaGetLastError());
+    BP.n = h->n; BP.npad = h->npad; BP.symmetric = h->symmetric;
+    BP.F = h->dF; BP.FT = h->dFT; BP.D = h->dD; BP.DT = h->dDT; BP.fd = h->dfd; BP.dd = h->ddd;
+    BP.perm32 = SP.perm32;
+    BP.M = (char *)h->ws + w.offInitM;
+    BP.h = (char *)h->ws + w.offInitH;
+    const int tiles = (h->npad + BT - 1) / BT;
+    const unsigned grid = (unsigned)(tiles * tiles) * (unsigned)batch;
+    if (h->acc_bits == 64) qap_build_m_kernel<int64_t><<<grid, 256, np * sizeof(int32_t), st>>>(BP);
+    else qap_build_m_kernel<int32_t><<<grid, 256, np * sizeof(int32_t), st>>>(BP);
+    CU(cudaGetLastError());
+    return QAPB_OK;
+}
+
+// Launch start + build + search kernels for `batch` starts.  `extra_ws` bytes are reserved at
 // the start of the workspace for the caller (multistart keeps best perms there).
 static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extra_ws, cudaStream_t st)
 {
-    const size_t acc_bytes = h->acc_bits / 8;
-    const size_t m_elems = (size_t)h->upt * 8 * h->threads * 4;
-    const size_t t_elems = (size_t)h->upt * 4 * h->threads * 4;
-    size_t need = (extra_ws + 255) / 256 * 256;
-    size_t offM = need;
-    if ((h->storage == 1 || h->storage == 2) && P.mode != MODE_ALL_DELTAS) need += m_elems * acc_bytes * batch;
-    size_t offT = need;
-    if (h->storage == 2 && P.mode != MODE_ALL_DELTAS) need += t_elems * sizeof(int32_t) * batch;
-    const size_t x_elems = (size_t)h->nunits * 16;
-    if (h->storage == 3 && !h->exp_in_smem && P.mode != MODE_ALL_DELTAS) need += x_elems * sizeof(int32_t) * batch;
-    // hybrid pipeline buffers: start permutations, stream states, initial M and h
-    const bool hyb = h->storage == 3 && P.mode != MODE_ALL_DELTAS;
-    const size_t np = (size_t)h->npad;
-    need = (need + 255) / 256 * 256;
-    const size_t offPerm = need;  if (hyb) need += (np * 4 * batch + 255) / 256 * 256;
-    const size_t offState = need; if (hyb) need += ((size_t)8 * batch + 255) / 256 * 256;
-    const size_t offInitH = need; if (hyb) need += (np * 4 * batch + 255) / 256 * 256;
-    const size_t offInitM = need; if (hyb) need += np * np * 4 * batch;
-    int rc = ensure_ws(h, need);
+    const WsPlan w = plan_ws(h, batch, extra_ws);
+    int rc = ensure_ws(h, w.total);
     if (rc) return rc;
-    P.gM = (char *)h->ws + offM;
-    P.gT = (char *)h->ws + offT;
-    P.gM_stride = m_elems;
-    P.gT_stride = (h->storage == 3) ? x_elems : t_elems;
+    P.gM = (char *)h->ws + w.offM;
+    P.gT = (char *)h->ws + w.offT;
+    P.gM_stride = w.m_elems;
+    P.gT_stride = w.x_elems;
     kern_t kern = handle_kernel(h);
-    int threads = h->threads;
-    unsigned smem = h->smem_bytes;
     if (h->storage == 3) {
         P.hlay = make_hyb_layout(h->npad, h->nb, h->toff, h->us, h->exp_in_smem, h->staged, h->symmetric);
         P.staged = h->staged;
         P.toff = h->toff; P.us = h->us; P.exp_in_smem = h->exp_in_smem;
     } else P.lay = make_layout(h->npad, h->nunits, h->threads, h->upt, h->acc_bits / 8, h->storage);
-    if (h->storage == 3 && P.mode == MODE_ALL_DELTAS) {
-        // the full evaluator lives in the generic kernel; it keeps no per-search state
-        kern = pick_kernel(32, 2, h->g_lb_class);
-        threads = h->g_threads;
-        P.upt = h->g_upt;
-        P.lay = make_layout(h->npad, h->nunits, threads, P.upt, 4, 2);
-        smem = P.lay.total;
-    }
     // several handles share one kernel instantiation: (re)assert this launch's opt-in size
-    CU(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes));
     CU(cudaEventRecord(h->ev0, st));
-    if (hyb) {
-        // start permutations (+ stream state), then M and h as one batched tiled integer product
-        StartParams SP;
-        SP.n = h->n; SP.npad = h->npad; SP.rng = P.rng; SP.force_seq_rng = P.force_seq_rng;
-        SP.master_seed = P.master_seed; SP.first_index = P.first_index; SP.perms = P.perms;
-        SP.perm32 = (int32_t *)((char *)h->ws + offPerm);
-        SP.state = (unsigned long long *)((char *)h->ws + offState);
-        qap_start_kernel<<<batch, 128, 2 * np * sizeof(int32_t), st>>>(SP);
-        CU(cudaGetLastError());
-        BuildParams BP;
-        BP.n = h->n; BP.npad = h->npad; BP.symmetric = h->symmetric;
-        BP.F = h->dF; BP.FT = h->dFT; BP.D = h->dD; BP.DT = h->dDT; BP.fd = h->dfd; BP.dd = h->ddd;
-        BP.perm32 = SP.perm32;
-        BP.M = (int32_t *)((char *)h->ws + offInitM);
-        BP.h = (int32_t *)((char *)h->ws + offInitH);
-        const int tiles = (h->npad + BT - 1) / BT;
-        qap_build_m_kernel<<<(unsigned)(tiles * tiles) * (unsigned)batch, 256, np * sizeof(int32_t), st>>>(BP);
-        CU(cudaGetLastError());
-        P.perm32 = SP.perm32; P.start_state = SP.state; P.initM = BP.M; P.initH = BP.h;
-    }
-    kern<<<batch, threads, smem, st>>>(P);
+    // start permutations (+ stream state), then M and h as one batched tiled integer product
+    BuildParams BP;
+    StartParams SP;
+    rc = launch_build(h, w, batch, P.rng, P.force_seq_rng, P.master_seed, P.first_index, P.perms, st, BP, SP);
+    if (rc) return rc;
+    P.perm32 = SP.perm32; P.start_state = SP.state; P.initM = BP.M; P.initH = BP.h;
+    kern<<<batch, h->threads, h->smem_bytes, st>>>(P);
     CU(cudaGetLastError());
     CU(cudaEventRecord(h->ev1, st));
     h->have_timing = 1;
@@ -558,40 +568,23 @@ extern "C" int qapb_all_deltas(qapb_handle *h, const int64_t *perms, int batch, 
     int rc = check_common(h, batch);
     if (rc) return rc;
     if (!perms || !deltas) return fail(QAPB_ERR_INVALID, "NULL buffer");
-    if (h->storage == 3) {
-        // int32 plans: the full evaluator as a tiled contraction (qap_build_m_kernel) + emission
-        cudaStream_t st = (cudaStream_t)stream;
-        const size_t np = (size_t)h->npad;
-        const size_t szPerm = (np * 4 * batch + 255) / 256 * 256, szState = ((size_t)8 * batch + 255) / 256 * 256;
-        rc = ensure_ws(h, 2 * szPerm + szState + np * np * 4 * batch + 256);
-        if (rc) return rc;
-        StartParams SP;
-        SP.n = h->n; SP.npad = h->npad; SP.rng = 0; SP.force_seq_rng = 0; SP.master_seed = 0; SP.first_index = 0;
-        SP.perms = perms;
-        SP.perm32 = (int32_t *)h->ws;
-        SP.state = (unsigned long long *)((char *)h->ws + szPerm);
-        BuildParams BP;
-        BP.n = h->n; BP.npad = h->npad; BP.symmetric = h->symmetric;
-        BP.F = h->dF; BP.FT = h->dFT; BP.D = h->dD; BP.DT = h->dDT; BP.fd = h->dfd; BP.dd = h->ddd;
-        BP.perm32 = SP.perm32;
-        BP.h = (int32_t *)((char *)h->ws + szPerm + szState);
-        BP.M = (int32_t *)((char *)h->ws + 2 * szPerm + szState);
-        CU(cudaEventRecord(h->ev0, st));
-        qap_start_kernel<<<batch, 128, 2 * np * sizeof(int32_t), st>>>(SP);
-        const int tiles = (h->npad + BT - 1) / BT;
-        qap_build_m_kernel<<<(unsigned)(tiles * tiles) * (unsigned)batch, 256, np * sizeof(int32_t), st>>>(BP);
-        qap_emit_deltas_kernel<<<dim3(batch, std::min(h->n - 1, 64)), 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
-        CU(cudaGetLastError());
-        CU(cudaEventRecord(h->ev1, st));
-        h->have_timing = 1;
-        return QAPB_OK;
-    }
-    SearchParams P;
-    base_params(h, P);
-    P.mode = MODE_ALL_DELTAS;
-    P.perms = perms;
-    P.out_deltas = deltas;
-    return launch_search(h, P, batch, 0, (cudaStream_t)stream);
+    // the full evaluator as a tiled contraction (qap_build_m_kernel) + emission
+    cudaStream_t st = (cudaStream_t)stream;
+    const WsPlan w = plan_ws(h, batch, 0);
+    rc = ensure_ws(h, w.total);
+    if (rc) return rc;
+    CU(cudaEventRecord(h->ev0, st));
+    BuildParams BP;
+    StartParams SP;
+    rc = launch_build(h, w, batch, 0, 0, 0, 0, perms, st, BP, SP);
+    if (rc) return rc;
+    const dim3 grid(batch, std::min(h->n - 1, 64));
+    if (h->acc_bits == 64) qap_emit_deltas_kernel<int64_t><<<grid, 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
+    else qap_emit_deltas_kernel<int32_t><<<grid, 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(h->ev1, st));
+    h->have_timing = 1;
+    return QAPB_OK;
 }
 
 extern "C" int qapb_two_opt(qapb_handle *h, const int64_t *perms, int batch, int iterations, int64_t *best,
@@ -656,8 +649,6 @@ extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, u
     const size_t head = 2 * perm_bytes + (size_t)count * sizeof(int64_t);
     SearchParams P;
     base_params(h, P);
-    rc = ensure_ws(h, head + 256);  // make h->ws valid before taking addresses; launch_search may regrow
-    if (rc) return rc;
     P.mode = algo == QAPB_ALGO_TABU ? MODE_TABU : MODE_TWO_OPT;
     P.rng = 1;
     P.iterations = iterations;
@@ -665,22 +656,9 @@ extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, u
     P.first_index = first_index;
     P.ten_lo = ten_low;
     P.ten_hi = ten_high;
-    // compute total need first so the head pointers stay valid
-    {
-        const size_t acc_bytes = h->acc_bits / 8;
-        const size_t m_elems = (size_t)h->upt * 8 * h->threads * 4, t_elems = (size_t)h->upt * 4 * h->threads * 4;
-        size_t need = (head + 255) / 256 * 256;
-        if (h->storage == 1 || h->storage == 2) need += m_elems * acc_bytes * count;
-        if (h->storage == 2) need += t_elems * sizeof(int32_t) * count;
-        if (h->storage == 3 && !h->exp_in_smem) need += (size_t)h->nunits * 16 * sizeof(int32_t) * count;
-        if (h->storage == 3) {
-            const size_t np = (size_t)h->npad;
-            need = (need + 255) / 256 * 256;
-            need += 2 * ((np * 4 * count + 255) / 256 * 256) + ((size_t)8 * count + 255) / 256 * 256 + np * np * 4 * count;
-        }
-        rc = ensure_ws(h, need);
-        if (rc) return rc;
-    }
+    // size the whole workspace first so the head pointers stay valid
+    rc = ensure_ws(h, plan_ws(h, count, head).total);
+    if (rc) return rc;
     int64_t *w_best = (int64_t *)h->ws;
     int64_t *w_cur = (int64_t *)((char *)h->ws + perm_bytes);
     int64_t *w_curcost = (int64_t *)((char *)h->ws + 2 * perm_bytes);

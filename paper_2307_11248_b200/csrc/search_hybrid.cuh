@@ -329,7 +329,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     int32_t *sM = reinterpret_cast<int32_t *>(smem_raw + lay.offM);
     unsigned *sTB = reinterpret_cast<unsigned *>(smem_raw + lay.offTB);
     int32_t *sMX = reinterpret_cast<int32_t *>(smem_raw + lay.offMX);
-    constexpr int NPM = SMEMU ? 256 : 128;  // size class of the plan (host: make_hyb_layout)
+    constexpr int NPM = (SMEMU && UR == 2) ? 256 : 128;  // size class of the plan (host: make_hyb_layout)
     Vecs V;
     V.A = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(0, NPM));
     V.C = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(1, NPM));
@@ -385,7 +385,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     for (int i = tid; i < npad; i += T) {
         V.A[i] = 0; V.C[i] = 0; V.B[i] = 0; V.E[i] = 0;
         V.ColR[i] = 0; V.ColS[i] = 0; V.TR[i] = 0; V.TS[i] = 0; V.XR[i] = 0; V.XS[i] = 0;
-        V.H[i] = P.initH[(size_t)b * npad + i];
+        V.H[i] = reinterpret_cast<const int32_t *>(P.initH)[(size_t)b * npad + i];
         sP[i] = P.perm32[(size_t)b * npad + i];
     }
     unsigned long long rng_state = P.rng ? P.start_state[b] : 0ULL;
@@ -407,7 +407,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         __syncthreads();
     }
     int my_pi = tid < n ? sP[tid] : 0;  // unit at location tid, kept in a register (T >= n by plan)
-    const int32_t *__restrict__ Minit = P.initM + (size_t)b * npad * npad;
+    const int32_t *__restrict__ Minit = reinterpret_cast<const int32_t *>(P.initM) + (size_t)b * npad * npad;
 
     // ---- unit ownership.  tb = mask of pairs that are tabu now (pads / non-pairs permanently
     // set, expiry MAXV), mexp = earliest expiry among the clearable bits.

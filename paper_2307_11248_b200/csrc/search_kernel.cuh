@@ -32,7 +32,7 @@
 
 namespace qapb {
 
-enum { MODE_ALL_DELTAS = 0, MODE_TWO_OPT = 1, MODE_TABU = 2 };
+enum { MODE_TWO_OPT = 1, MODE_TABU = 2 };
 enum { TENURE_CHUNK = 256 };  // tenure draws precomputed per refill
 
 // ---- shared-memory layout, shared by host (size) and device (offsets) ------
@@ -51,8 +51,7 @@ __host__ __device__ inline SmemLayout make_layout(int npad, int nunits, int T, i
     L.offM = o;
     if (storage == 0) o += (unsigned)upt * 8u * (unsigned)T * 4u * (unsigned)acc_bytes;
     o = align16(o);
-    L.offT = o;
-    if (storage <= 1) o += (unsigned)upt * 4u * (unsigned)T * 16u;
+    L.offT = o; o += (unsigned)upt * (unsigned)T * 8u;  // per unit: 16-bit tabu mask word + earliest expiry
     o = align16(o);
     L.offA = o; o += 4u * npad;
     L.offC = o; o += 4u * npad;
@@ -63,7 +62,7 @@ __host__ __device__ inline SmemLayout make_layout(int npad, int nunits, int T, i
     L.offP = o; o += 4u * npad;
     L.offJ = o; o += 4u * npad;
     L.offU = o; o += align16(2u * nunits);
-    L.offRedD = o; o += 32u * 8u;
+    L.offRedD = o; o += 32u * 8u + 16u;
     L.offRedK = o; o += 32u * 4u;
     L.offMisc = o; o += 64u;
     L.offTen = o; o += 4u * TENURE_CHUNK;
@@ -91,20 +90,19 @@ struct SearchParams {
     const int64_t *tenures;          // [B,iterations]   (tabu, rng == 0)
     unsigned long long master_seed, first_index;
     long long ten_lo, ten_hi;
-    int64_t *out_deltas;             // [B, n(n-1)/2]    (MODE_ALL_DELTAS)
     int64_t *best, *best_cost, *cur, *cur_cost;
     int64_t *cells;                  // [B,n,n] or null
     int64_t *stopped, *steps;        // [B] or null
     int64_t *tr_i, *tr_j, *tr_d, *tr_tabu;  // [B,iterations] or null
-    void *gM;                        // global placement matrices (storage >= 1)
-    void *gT;                        // global tabu triangles    (storage == 2)
+    void *gM;                        // global placement matrices (storage 1)
+    void *gT;                        // tabu expiry per (unit, slot), int32 (generic kernel; hybrid when not in smem)
     unsigned long long gM_stride, gT_stride;  // elements per start
     long long *dbg;                  // optional phase-cycle counters (development), else null
     SmemLayout lay;                  // generic kernel: offsets live in the constant bank
     HybLayout hlay;                  // hybrid kernel
-    const int32_t *perm32;           // hybrid: [B,npad] start permutations (qap_start_kernel)
-    const unsigned long long *start_state;  // hybrid: [B] SplitMix64 state after the shuffle
-    const int32_t *initM, *initH;    // hybrid: [B,npad,npad], [B,npad] from qap_build_m_kernel
+    const int32_t *perm32;           // [B,npad] start permutations (qap_start_kernel)
+    const unsigned long long *start_state;  // [B] SplitMix64 state after the shuffle
+    const void *initM, *initH;       // [B,npad,npad], [B,npad] from qap_build_m_kernel (int32 or int64 state)
     int toff, us, exp_in_smem;       // hybrid plan: off-diagonal threads, shared-memory units per thread
     int staged;                      // hybrid: int16 copies of D, F (and transposes) staged in shared memory
 };
@@ -275,7 +273,7 @@ __device__ __forceinline__ ElemLoc locate(int x, int y, int nb, int noff, int T)
         w = x & 3; l = y & 3;
     } else if (X > Y) {
         uid = Y * nb - ((Y * (Y + 1)) >> 1) + (X - Y - 1);
-        w = 4 + (x & 3); l = y & 3;
+        w = 4 + (y & 3); l = x & 3;  // the lower block is stored transposed (row u holds L[0..3][u])
     } else {
         uid = noff + X;
         w = x & 3; l = y & 3;
@@ -289,9 +287,29 @@ __device__ __forceinline__ ElemLoc locate(int x, int y, int nb, int noff, int T)
 }
 
 // -----------------------------------------------------------------------------
-// The search kernel.  STORAGE: 0 = M and tabu triangle in shared memory,
-// 1 = M in global (L2-resident), tabu in shared, 2 = both in global.
+// The generic search kernel: any n <= 1020, int32 or int64 state.  STORAGE 0 keeps M in
+// shared memory, STORAGE 1 in an L2-resident workspace.  Start permutation, stream state,
+// M and h come from qap_start_kernel / qap_build_m_kernel (build_kernels.cuh).  M is
+// streamed through registers one row pair at a time (row u of the upper block with row u of
+// the transposed lower block), so eight accumulators are live per thread.  The tabu
+// triangle is a 16-bit mask per unit (pairs that are tabu now) plus the unit's earliest
+// expiry in shared memory; the expiry iterations themselves live in an L2-resident array
+// that is touched only when a pair is set or expires.
 // -----------------------------------------------------------------------------
+__device__ __forceinline__ void expire_unit_bits(unsigned &tb, int32_t &mexp, int c, const int32_t *xp16)
+{
+    unsigned bits = tb;
+    int32_t nm = 0x7fffffff;
+    while (bits) {
+        const int q = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int32_t e = xp16[q];
+        if (e <= c) tb &= ~(1u << q);
+        else if (e != 0x7fffffff) nm = min(nm, e);
+    }
+    mexp = nm;
+}
+
 template <typename acc_t, int STORAGE, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchParams P)
 {
@@ -303,17 +321,17 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
 
     acc_t *M = STORAGE == 0 ? reinterpret_cast<acc_t *>(smem_raw + lay.offM)
                             : reinterpret_cast<acc_t *>(P.gM) + (size_t)b * P.gM_stride;
-    int32_t *Tb = STORAGE <= 1 ? reinterpret_cast<int32_t *>(smem_raw + lay.offT)
-                               : reinterpret_cast<int32_t *>(P.gT) + (size_t)b * P.gT_stride;
+    unsigned *sTB = reinterpret_cast<unsigned *>(smem_raw + lay.offT);  // [upt*T] tabu-now masks
+    int32_t *sMX = reinterpret_cast<int32_t *>(sTB + (size_t)upt * T);  // [upt*T] earliest expiry
+    int32_t *xp = reinterpret_cast<int32_t *>(P.gT) + (size_t)b * P.gT_stride;  // [nunits*16]
     int32_t *sA = reinterpret_cast<int32_t *>(smem_raw + lay.offA);
     int32_t *sC = reinterpret_cast<int32_t *>(smem_raw + lay.offC);
     int32_t *sB = reinterpret_cast<int32_t *>(smem_raw + lay.offB);
     int32_t *sE = reinterpret_cast<int32_t *>(smem_raw + lay.offE);
     acc_t *sH = reinterpret_cast<acc_t *>(smem_raw + lay.offH);
     int32_t *sP = reinterpret_cast<int32_t *>(smem_raw + lay.offP);
-    unsigned *sJ = reinterpret_cast<unsigned *>(smem_raw + lay.offJ);
     uint16_t *sU = reinterpret_cast<uint16_t *>(smem_raw + lay.offU);
-    long long *sRed64 = reinterpret_cast<long long *>(smem_raw + lay.offRedD);  // 32 x 8 B
+    long long *sRed64 = reinterpret_cast<long long *>(smem_raw + lay.offRedD);  // 33 x 8 B
     acc_t *sRedD = reinterpret_cast<acc_t *>(smem_raw + lay.offRedD);
     unsigned *sRedK = reinterpret_cast<unsigned *>(smem_raw + lay.offRedK);
     long long *sMisc = reinterpret_cast<long long *>(smem_raw + lay.offMisc);
@@ -325,53 +343,23 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
     const int32_t *__restrict__ DT = P.DT;
     const bool sym = P.symmetric != 0;
     const acc_t MAXV = Acc<acc_t>::maxv();
+    const int32_t MAXE = 0x7fffffff;
 
     // ---------------------------------------------------------------- setup
+    const acc_t *__restrict__ Hinit = reinterpret_cast<const acc_t *>(P.initH) + (size_t)b * npad;
+    const acc_t *__restrict__ Minit = reinterpret_cast<const acc_t *>(P.initM) + (size_t)b * npad * npad;
     for (int u = tid; u < nunits; u += T) sU[u] = P.unit_ij[u];
     for (int i = tid; i < npad; i += T) {
         sA[i] = 0; sC[i] = 0; sB[i] = 0; sE[i] = 0;
-        sH[i] = 0;
-        sP[i] = (P.rng || i >= n) ? (i < n ? i : 0) : (int32_t)P.perms[(size_t)b * n + i];
+        sH[i] = Hinit[i];
+        sP[i] = P.perm32[(size_t)b * npad + i];
     }
-    unsigned long long rng_state = 0;  // meaningful in thread 0 only
-    if (P.rng) {
-        // multistart.py:88: state = derive_seed(master, index); core.py:81-87 shuffle.
-        const unsigned long long seed = mix64(P.master_seed + QAPB_GAMMA * (P.first_index + (unsigned long long)b + 1ULL));
-        // Draw k (0-based) serves i = n-1-k with bound i+1.  Draws are computed in
-        // parallel assuming no rejection; any rejection (probability ~ n^2/2^64)
-        // falls back to the exact sequential loop.
-        int reject = P.force_seq_rng;
-        for (int k = tid; k < n - 1; k += T) {
-            unsigned long long bound = (unsigned long long)(n - 1 - k) + 1ULL;
-            unsigned long long r = mix64(seed + QAPB_GAMMA * ((unsigned long long)k + 1ULL));
-            unsigned long long rem = (0ULL - bound) % bound;
-            if (r > ~0ULL - rem) reject = 1;
-            sJ[n - 1 - k] = (unsigned)(r % bound);
-        }
-        reject = __syncthreads_or(reject);
-        if (tid == 0) {
-            rng_state = seed;
-            if (reject) {
-                for (int i = n - 1; i >= 1; --i) {
-                    unsigned j = (unsigned)randbelow_seq(rng_state, (unsigned long long)i + 1ULL);
-                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
-                }
-            } else {
-                for (int i = n - 1; i >= 1; --i) {
-                    unsigned j = sJ[i];
-                    int32_t t = sP[i]; sP[i] = sP[j]; sP[j] = t;
-                }
-                rng_state = seed + QAPB_GAMMA * (unsigned long long)(n - 1);
-            }
-            sMisc[2] = (long long)rng_state;
-        }
-    }
+    unsigned long long rng_state = P.rng ? P.start_state[b] : 0ULL;  // stream state after the shuffle
     if (P.cells) {
         int64_t *cz = P.cells + (size_t)b * n * n;
         for (int i = tid; i < n * n; i += T) cz[i] = 0;
     }
     __syncthreads();
-    if (P.rng) rng_state = (unsigned long long)sMisc[2];  // stream state after the shuffle, in every thread
 
     // full cost (_kernels.pyx:18-24), int64, including the diagonal products.
     long long cost;
@@ -387,112 +375,30 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
         __syncthreads();
     }
 
-    // h[i]
-    for (int i = tid; i < n; i += T) {
-        int pi = sP[i];
-        acc_t acc = (acc_t)P.dd[i] * (acc_t)P.fd[pi];
-        if (sym) {
-            for (int k = 0; k < n; ++k) acc += (acc_t)2 * ((acc_t)D[i * npad + k] * (acc_t)F[pi * npad + sP[k]]);
-        } else {
-            for (int k = 0; k < n; ++k) {
-                int pk = sP[k];
-                acc += (acc_t)D[i * npad + k] * (acc_t)F[pi * npad + pk] + (acc_t)DT[i * npad + k] * (acc_t)FT[pi * npad + pk];
-            }
-        }
-        sH[i] = acc;
-    }
-    __syncthreads();
-
-    // M (and tabu triangle) per unit
+    // units into the spill layout (lower block transposed); tabu masks: pads and non-pairs are
+    // permanently set with expiry MAXE
     for (int k = 0; k < upt; ++k) {
         const int uid = tid + k * T;
-        if (uid >= nunits) break;
+        if (uid >= nunits) { sTB[k * T + tid] = 0xffffu; sMX[k * T + tid] = MAXE; continue; }
         const int I = sU[uid] & 0xff, J = sU[uid] >> 8;
-        int pI[4], pJ[4];
+        unsigned dead = 0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) { pI[u] = sP[4 * I + u]; pJ[u] = sP[4 * J + u]; }
-        acc_t U[4][4], L[4][4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) { U[u][v] = 0; L[u][v] = 0; }
-        for (int kk = 0; kk < n; ++kk) {
-            const int pk = sP[kk];
-            int32_t dI[4], dJ[4], fI[4], fJ[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                dI[u] = D[(4 * I + u) * npad + kk];
-                dJ[u] = D[(4 * J + u) * npad + kk];
-                fI[u] = F[pI[u] * npad + pk];
-                fJ[u] = F[pJ[u] * npad + pk];
-            }
-            if (sym) {
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        U[u][v] += (acc_t)dI[u] * (acc_t)fJ[v];
-                        L[v][u] += (acc_t)dJ[v] * (acc_t)fI[u];
-                    }
-            } else {
-                int32_t dtI[4], dtJ[4], ftI[4], ftJ[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    dtI[u] = DT[(4 * I + u) * npad + kk];
-                    dtJ[u] = DT[(4 * J + u) * npad + kk];
-                    ftI[u] = FT[pI[u] * npad + pk];
-                    ftJ[u] = FT[pJ[u] * npad + pk];
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        U[u][v] += (acc_t)dI[u] * (acc_t)fJ[v] + (acc_t)dtI[u] * (acc_t)ftJ[v];
-                        L[v][u] += (acc_t)dJ[v] * (acc_t)fI[u] + (acc_t)dtJ[v] * (acc_t)ftI[u];
-                    }
-            }
-        }
-        int32_t Ex[4][4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 4; ++u) {
+            acc_t Ur[4], Lt[4];
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                const int i = 4 * I + u, j = 4 * J + v;
-                if (sym) { U[u][v] *= 2; L[v][u] *= 2; }
-                const acc_t fs = (acc_t)F[pI[u] * npad + pJ[v]] + (acc_t)F[pJ[v] * npad + pI[u]];
-                U[u][v] += (acc_t)D[i * npad + j] * fs + (acc_t)P.dd[i] * (acc_t)P.fd[pJ[v]];
-                L[v][u] += (acc_t)D[j * npad + i] * fs + (acc_t)P.dd[j] * (acc_t)P.fd[pI[u]];
-                const bool pad = (i >= n) || (j >= n);
-                if (pad) { U[u][v] = Acc<acc_t>::bighalf(); L[v][u] = Acc<acc_t>::bighalf(); }
-                if (i == j) { U[u][v] = 0; L[v][u] = 0; }
-                Ex[u][v] = pad ? 0x7fffffff : 0;
+                Ur[v] = Minit[(size_t)(4 * I + u) * npad + 4 * J + v];
+                Lt[v] = Minit[(size_t)(4 * J + v) * npad + 4 * I + u];
+                if (4 * I + u >= n || 4 * J + v >= n || (I == J && u >= v)) dead |= 1u << (u * 4 + v);
             }
-        if (P.mode == MODE_ALL_DELTAS) {
-            acc_t hI[4], hJ[4];
-            ld_h4(sH, I, hI);
-            ld_h4(sH, J, hJ);
-            int64_t *out = P.out_deltas + (size_t)b * ((size_t)n * (n - 1) / 2);
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const int i = 4 * I + u, j = 4 * J + v;
-                    if (i < j && j < n) {
-                        const acc_t d = (I == J) ? U[u][v] + U[v][u] - hI[u] - hI[v]
-                                                 : U[u][v] + L[v][u] - hI[u] - hJ[v];
-                        out[(size_t)i * n - ((size_t)i * (i + 1)) / 2 + (j - i - 1)] = (int64_t)d;
-                    }
-                }
-        } else {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                st_row(M, k * 8 + u, T, tid, U[u]);
-                st_row(M, k * 8 + 4 + u, T, tid, L[u]);
-                reinterpret_cast<int4 *>(Tb)[(k * 4 + u) * T + tid] = make_int4(Ex[u][0], Ex[u][1], Ex[u][2], Ex[u][3]);
-            }
+            st_row(M, k * 8 + u, T, tid, Ur);
+            st_row(M, k * 8 + 4 + u, T, tid, Lt);
         }
+        sTB[k * T + tid] = dead;
+        sMX[k * T + tid] = MAXE;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) xp[(size_t)uid * 16 + q] = ((dead >> q) & 1u) ? MAXE : 0;
     }
-    if (P.mode == MODE_ALL_DELTAS) return;
     __syncthreads();
 
     // ------------------------------------------------------------ iterations
@@ -521,57 +427,51 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
             const int uid = tid + k * T;
             if (uid >= nunits) break;
             const int I = sU[uid] & 0xff, J = sU[uid] >> 8;
-            acc_t cand[16];
+            unsigned tbk = sTB[k * T + tid];
+            if (c >= sMX[k * T + tid]) {  // some pair of this unit stops being tabu now
+                int32_t mx;
+                expire_unit_bits(tbk, mx, c, xp + (size_t)uid * 16);
+                sTB[k * T + tid] = tbk;
+                sMX[k * T + tid] = mx;
+            }
             acc_t m = MAXV;
+            int slot = 0;
             if (I != J) {
-                acc_t U[4][4], L[4][4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    ld_row(M, k * 8 + u, T, tid, U[u]);
-                    ld_row(M, k * 8 + 4 + u, T, tid, L[u]);
-                }
-                if (c > 1) {
-                    int32_t aI[4], bI[4], aJ[4], bJ[4];
-                    ld_vec4(sA, I, aI); ld_vec4(sB, I, bI); ld_vec4(sA, J, aJ); ld_vec4(sB, J, bJ);
-                    if (sym) {  // a pre-doubled: a == c, b == e
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-#pragma unroll
-                            for (int v = 0; v < 4; ++v) {
-                                U[u][v] -= (acc_t)aI[u] * (acc_t)bJ[v];
-                                L[v][u] -= (acc_t)aJ[v] * (acc_t)bI[u];
-                            }
-                    } else {
-                        int32_t cI[4], eI[4], cJ[4], eJ[4];
-                        ld_vec4(sC, I, cI); ld_vec4(sE, I, eI); ld_vec4(sC, J, cJ); ld_vec4(sE, J, eJ);
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-#pragma unroll
-                            for (int v = 0; v < 4; ++v) {
-                                U[u][v] -= (acc_t)aI[u] * (acc_t)bJ[v] + (acc_t)cI[u] * (acc_t)eJ[v];
-                                L[v][u] -= (acc_t)aJ[v] * (acc_t)bI[u] + (acc_t)cJ[v] * (acc_t)eI[u];
-                            }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        st_row(M, k * 8 + u, T, tid, U[u]);
-                        st_row(M, k * 8 + 4 + u, T, tid, L[u]);
-                    }
-                }
-                acc_t hI[4], hJ[4];
-                ld_h4(sH, I, hI);
+                int32_t aJ[4], bJ[4], cJ[4], eJ[4];
+                ld_vec4(sA, J, aJ); ld_vec4(sB, J, bJ);
+                if (!sym) { ld_vec4(sC, J, cJ); ld_vec4(sE, J, eJ); }
+                acc_t hJ[4];
                 ld_h4(sH, J, hJ);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    int32_t ex[4];
-                    ld_vec4(Tb, (k * 4 + u) * T + tid, ex);
+                    acc_t Ur[4], Lr[4];
+                    ld_row(M, k * 8 + u, T, tid, Ur);
+                    ld_row(M, k * 8 + 4 + u, T, tid, Lr);
+                    if (c > 1) {
+                        const int32_t aIu = sA[4 * I + u], bIu = sB[4 * I + u];
+                        if (sym) {  // a pre-doubled: a == c, b == e
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                Ur[v] -= (acc_t)aIu * (acc_t)bJ[v];
+                                Lr[v] -= (acc_t)aJ[v] * (acc_t)bIu;
+                            }
+                        } else {
+                            const int32_t cIu = sC[4 * I + u], eIu = sE[4 * I + u];
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                Ur[v] -= (acc_t)aIu * (acc_t)bJ[v] + (acc_t)cIu * (acc_t)eJ[v];
+                                Lr[v] -= (acc_t)aJ[v] * (acc_t)bIu + (acc_t)cJ[v] * (acc_t)eIu;
+                            }
+                        }
+                        st_row(M, k * 8 + u, T, tid, Ur);
+                        st_row(M, k * 8 + 4 + u, T, tid, Lr);
+                    }
+                    const acc_t hIu = sH[4 * I + u];
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
-                        const acc_t d = U[u][v] + L[v][u] - hI[u] - hJ[v];
-                        const bool adm = (ex[v] <= c) || (d < thr);
-                        const acc_t cd = adm ? d : MAXV;
-                        cand[u * 4 + v] = cd;
-                        m = cd < m ? cd : m;
+                        const acc_t d = Ur[v] + Lr[v] - hIu - hJ[v];
+                        const bool tb = (tbk >> (u * 4 + v)) & 1u;
+                        if ((!tb || d < thr) && d < m) { m = d; slot = u * 4 + v; }
                     }
                 }
             } else {
@@ -594,29 +494,16 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                 acc_t hI[4];
                 ld_h4(sH, I, hI);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    int32_t ex[4];
-                    ld_vec4(Tb, (k * 4 + u) * T + tid, ex);
+                for (int u = 0; u < 3; ++u)
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        acc_t cd = MAXV;
-                        if (u < v) {
-                            const acc_t d = U[u][v] + U[v][u] - hI[u] - hI[v];
-                            const bool adm = (ex[v] <= c) || (d < thr);
-                            cd = adm ? d : MAXV;
-                        }
-                        cand[u * 4 + v] = cd;
-                        m = cd < m ? cd : m;
+                    for (int v = u + 1; v < 4; ++v) {
+                        const acc_t d = U[u][v] + U[v][u] - hI[u] - hI[v];
+                        const bool tb = (tbk >> (u * 4 + v)) & 1u;
+                        if ((!tb || d < thr) && d < m) { m = d; slot = u * 4 + v; }
                     }
-                }
             }
             if (m != MAXV && m <= bd) {
-                int slot = 15;
-#pragma unroll
-                for (int q = 14; q >= 0; --q) slot = (cand[q] == m) ? q : slot;
-                const int u = slot >> 2, v = slot & 3;
-                const int32_t ex = Tb[((size_t)((k * 4 + u) * T + tid)) * 4 + v];
-                const unsigned key = pair_key(4 * I + u, 4 * J + v, ex > c ? 1 : 0);
+                const unsigned key = pair_key(4 * I + (slot >> 2), 4 * J + (slot & 3), (tbk >> slot) & 1u);
                 if (m < bd || key < bkey) { bd = m; bkey = key; }
             }
         }
@@ -676,7 +563,11 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                         const int R = r >> 2, S = s >> 2;
                         const int uid = (R < S) ? R * nb - ((R * (R + 1)) >> 1) + (S - R - 1) : noff + R;
                         const int kq = uid / T, tq = uid - kq * T;
-                        Tb[((size_t)((kq * 4 + (r & 3)) * T + tq)) * 4 + (s & 3)] = (int32_t)(c + ten);
+                        const int q = (r & 3) * 4 + (s & 3);
+                        const int32_t new_exp = (int32_t)(c + ten);
+                        sTB[kq * T + tq] |= 1u << q;
+                        sMX[kq * T + tq] = min(sMX[kq * T + tq], new_exp);
+                        xp[(size_t)uid * 16 + q] = new_exp;
                         if (P.cells) {
                             int64_t *cz = P.cells + (size_t)b * n * n;
                             cz[(size_t)r * n + s] = (int64_t)c + ten;

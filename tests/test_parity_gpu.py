@@ -309,3 +309,48 @@ def test_tabu_not_worse_than_two_opt_and_dominance(q):
     large = q.run_multistart(inst, q.SearchConfig(algorithm="tabu", n_starts=64, iterations=80, master_seed=4))
     assert large.best.cost <= small.best.cost
     assert np.array_equal(large.per_start_costs[:16], small.per_start_costs)
+
+
+@pytest.mark.parametrize("storage", ["0", "1"])
+@pytest.mark.parametrize("shape", ["rand23", "tai30a", "tai45b"])
+def test_generic_kernel_storage_modes(q, orc, monkeypatch, shape, storage):
+    """Both placements of the generic kernel's state (M in shared memory / M in L2), int32 (rand,
+    tai*a) and int64 (tai*b) state."""
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    monkeypatch.setenv("QAPB_FORCE_GENERIC", "1")
+    if storage != "0":
+        monkeypatch.setenv("QAPB_FORCE_STORAGE", storage)
+    inst = shapes.by_name(shape)
+    n, iters = inst.n, 50
+    di = DeviceInstance(inst.flow, inst.distance)
+    try:
+        assert di.info["storage"] == int(storage)
+        assert di.info["acc_bits"] == (64 if shape.endswith("b") else 32)
+        lo, hi = orc.tenure_bounds(n)
+        perms, tens = [], []
+        for b in range(3):
+            r = orc.Rng(orc.derive_seed(17, b))
+            perms.append(r.permutation(n))
+            tens.append(r.tenures(lo, hi, iters))
+        perms, tens = np.stack(perms), np.stack(tens)
+        best, bc, cur, cc, cz, stop, steps, tr, _ = di.tabu(perms, iters, tens)
+        b2, bc2, cur2, cc2, mi, mj, md = di.two_opt(perms, iters)
+        deltas = di.all_deltas(perms)
+        for b in range(3):
+            want = orc.tabu_run(inst.flow, inst.distance, perms[b], iters, tens[b])
+            assert np.array_equal(best[b], want[0]) and bc[b] == want[1]
+            assert np.array_equal(cur[b], want[2]) and cc[b] == want[3]
+            assert np.array_equal(cz[b], want[4]) and steps[b] == want[6]
+            for a in range(4):
+                assert np.array_equal(tr[a][b, : want[6]], want[7][a])
+            w2 = orc.two_opt_run(inst.flow, inst.distance, perms[b], iters)
+            for g, w in zip((b2[b], bc2[b], cur2[b], cc2[b], mi[b], mj[b], md[b]), w2):
+                assert np.array_equal(g, w)
+            assert np.array_equal(deltas[b], orc.all_deltas(inst.flow, inst.distance, perms[b]))
+        costs, kbest, kidx, kperm = di.multistart("tabu", 21, 0, 6, iters, lo, hi)
+        wc, wbc, wbi, wbp = orc.multistart(inst.flow, inst.distance, "tabu", 21, 6, iters, threads=orc.max_threads())
+        assert np.array_equal(costs, wc) and (kbest, kidx) == (wbc, wbi) and np.array_equal(kperm, wbp)
+    finally:
+        di.close()
