@@ -71,13 +71,14 @@ static kern_t pick_hybrid_kernel(int symmetric, int packed, int plan)
     // plan 0: register-only (n <= 128), 80 registers/thread (two 352-thread CTAs per SM at n = 100)
     // plan 1: the same with int16 copies of D and F staged in shared memory
     // plan 2: two register units + shared-memory units per thread, 128 registers (n <= 256)
+    // plan 3/4: two register units per thread on half the threads, 112 registers (109 <= n <= 120:
+    //           two CTAs per SM where plan 0/1 would fit only one), without / with int16 staging
 #define KH(S, PK) {(kern_t) qap_search_hybrid_kernel<S, PK, 1, false, false, 80>, \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, true, 80>,  \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128>,  \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, false, 112>, \
-                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, true, 112>, \
-                   (kern_t) qap_search_hybrid_kernel<S, PK, 1, true, false, 80>}
-    static kern_t tab[2][2][6] = {{KH(false, false), KH(false, true)}, {KH(true, false), KH(true, true)}};
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, true, 112>}
+    static kern_t tab[2][2][5] = {{KH(false, false), KH(false, true)}, {KH(true, false), KH(true, true)}};
 #undef KH
     return tab[symmetric != 0][packed != 0][plan];
 }
@@ -85,28 +86,17 @@ static kern_t handle_kernel(const qapb_handle *h)
 {
     // packed (delta, slot) keys need |delta|*16 + 15 < 2^31
     const int packed = h->delta_bound < ((1LL << 27) - 1);
-    return h->storage == 3 ? pick_hybrid_kernel(h->symmetric, packed, h->us > 0 ? (h->upt == 2 ? 2 : 5) : (h->upt == 2 ? (h->staged ? 4 : 3) : (h->staged ? 1 : 0)))
+    return h->storage == 3 ? pick_hybrid_kernel(h->symmetric, packed, h->us > 0 ? 2 : (h->upt == 2 ? (h->staged ? 4 : 3) : (h->staged ? 1 : 0)))
                            : pick_kernel(h->acc_bits, h->storage, h->lb_class);
 }
 
 // Split of the off-diagonal units of one search between registers (UR per thread) and shared
 // memory (US per thread) for the hybrid kernel.  Returns false if the instance does not fit.
-static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
+static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff, int us)
 {
-    const int nb = h->nb, noff = h->noff, dw = (nb + 31) / 32;
-    int ur = 1, toff = (noff + 31) / 32 * 32, us = 0;
-    if (nb > 32) {                 // n <= 256: two register units per thread, the rest in shared memory
-        ur = 2;
-        toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
-        us = std::max(0, (noff - ur * toff + toff - 1) / toff);
-    }
-    if (const char *pl = getenv("QAPB_PLAN")) {  // development override: "UR,Toff,US"
-        int a, b, c;
-        if (sscanf(pl, "%d,%d,%d", &a, &b, &c) == 3 && (a == 1 || a == 2) && b % 32 == 0 && b >= 0 && c >= 0 &&
-            (long long)(a + c) * b >= noff)
-            ur = a, toff = b, us = c;
-    }
+    const int nb = h->nb, dw = (nb + 31) / 32;
     const int threads = toff + 32 * dw;
+    if ((long long)(ur + us) * toff < h->noff) return false;
     if (threads > 1024 || (us > 0 && threads > 512) || (us == 0 && ur == 2 && threads > 608)) return false;
     int exp_in_smem = 1;
     HybLayout L = make_hyb_layout(h->npad, nb, toff, us, 1);
@@ -118,10 +108,10 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
     if (L.total > smem_cap) return false;
     if (threads < h->n) return false;  // the publish phase maps one location per thread
     if (h->npad > 128 && !(us > 0 && ur == 2)) return false;  // layout size class 256 is tied to the (2 + smem) shape
-    if (h->npad <= 128 && us > 0 && ur != 1) return false;
+    if (h->npad <= 128 && us > 0) return false;
     int staged = 0;
     if (us == 0 && h->fits_i16 && !getenv("QAPB_NO_STAGE")) {
-        // stage while two CTAs per SM still fit (the register file allows no more at 80 regs x 352 threads)
+        // stage while two CTAs per SM still fit
         HybLayout Ls = make_hyb_layout(h->npad, nb, toff, us, exp_in_smem, 1, h->symmetric);
         if (Ls.total <= std::min(smem_cap, 110u * 1024u)) { staged = 1; L = Ls; }
     }
@@ -130,6 +120,47 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
     h->threads = threads;
     h->lb_class = 0;
     h->smem_bytes = L.total;
+    return true;
+}
+
+static int hybrid_occupancy(const qapb_handle *h)
+{
+    int occ = 0;
+    const void *k = (const void *)handle_kernel(h);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, h->threads, h->smem_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return occ;
+}
+
+// Split of the off-diagonal units of one search between registers (UR per thread) and shared
+// memory (US per thread) for the hybrid kernel.  Returns false if the instance does not fit.
+//   n <= 128: one register unit per thread (80 registers) if two such CTAs fit an SM (n <= 108),
+//             else two register units per thread on half the threads (112 registers) if THAT
+//             gives two CTAs per SM (n <= 120), else one unit per thread;
+//   n <= 256: two register units + shared-memory units per thread, one CTA per SM.
+static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
+{
+    const int nb = h->nb, noff = h->noff;
+    h->storage = 3;  // handle_kernel() dispatches on it
+    if (const char *pl = getenv("QAPB_PLAN")) {  // development override: "UR,Toff,US"
+        int a, b, c;
+        if (sscanf(pl, "%d,%d,%d", &a, &b, &c) == 3 && (a == 1 || a == 2) && b % 32 == 0 && b >= 0 && c >= 0)
+            return try_hybrid_plan(h, smem_cap, a, b, c);
+    }
+    if (nb > 32) {
+        const int toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
+        const int us = std::max(0, (noff - 2 * toff + toff - 1) / toff);
+        return try_hybrid_plan(h, smem_cap, 2, toff, us);
+    }
+    const int t1 = (noff + 31) / 32 * 32, t2 = ((noff + 1) / 2 + 31) / 32 * 32;
+    if (!try_hybrid_plan(h, smem_cap, 1, t1, 0)) return false;
+    if (hybrid_occupancy(h) >= 2 || t2 < 32) return true;
+    const qapb_handle one = *h;
+    if (try_hybrid_plan(h, smem_cap, 2, t2, 0) && hybrid_occupancy(h) >= 2) return true;
+    *h = one;
     return true;
 }
 
