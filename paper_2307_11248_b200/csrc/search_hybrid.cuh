@@ -34,8 +34,8 @@ namespace qapb {
 // depend only on the size class NPADMAX (128 or 256), so the kernel addresses them with immediates
 // (HYB_* below) instead of recomputing bases from the constant bank in every phase; the big,
 // rarely-addressed regions (expiries, staged matrices, shared-memory units) follow at runtime offsets.
-#define HYB_VEC(k, NPM) ((k) * 4 * (NPM))               /* A,C,B,E,H,ColR,ColS,TR,TS,XR,XS,P,J: k = 0..12 */
-#define HYB_REDD(NPM) (13 * 4 * (NPM))
+#define HYB_VEC(k, NPM) ((k) * 4 * (NPM))               /* A,C,B,E,H,ColR,ColS,TR,TS,XR,XS,P,HI,HJ: k = 0..13 */
+#define HYB_REDD(NPM) (14 * 4 * (NPM))
 #define HYB_REDK(NPM) (HYB_REDD(NPM) + 32 * 8 + 16)
 #define HYB_MISC(NPM) (HYB_REDK(NPM) + 32 * 4)
 #define HYB_TEN(NPM) (HYB_MISC(NPM) + 64)
@@ -69,6 +69,7 @@ __host__ __device__ inline HybLayout make_hyb_layout(int npad, int nb, int toff,
 
 struct Vecs {
     int32_t *A, *C, *B, *E, *H, *ColR, *ColS, *TR, *TS, *XR, *XS;
+    int32_t *HI, *HJ;  // packed-key forms of h: HI[i] = -16 h[i] + 4 (i & 3), HJ[i] = -16 h[i] + (i & 3)
 };
 
 __device__ __forceinline__ int32_t pick16(const int32_t (&A)[4][4], int slot)
@@ -83,9 +84,11 @@ __device__ __forceinline__ void st_vec4(int32_t *arr, int blk, int32_t a, int32_
     reinterpret_cast<int4 *>(arr)[blk] = make_int4(a, b, c, d);
 }
 
-// One unit from the row-major M of qap_build_m_kernel; dead = mask of pad pairs.
+// One unit from the row-major M of qap_build_m_kernel; dead = mask of pad pairs.  Pad entries are
+// set to `padv`: large enough that a pad pair never aspirates, small enough that its packed key
+// 16 delta + slot stays below 2^31 (2^25 with packed keys, where |M|, |h| < 2^25 is host-proven).
 __device__ __forceinline__ void load_unit(const int32_t *__restrict__ Mi, int npad, int n, int I, int J,
-                                          int32_t (&U)[4][4], int32_t (&L)[4][4], unsigned &dead)
+                                          int32_t (&U)[4][4], int32_t (&L)[4][4], unsigned &dead, int32_t padv)
 {
     dead = 0;
 #pragma unroll
@@ -94,10 +97,15 @@ __device__ __forceinline__ void load_unit(const int32_t *__restrict__ Mi, int np
         const int4 c = *reinterpret_cast<const int4 *>(Mi + (size_t)(4 * J + u) * npad + 4 * I);
         U[u][0] = a.x; U[u][1] = a.y; U[u][2] = a.z; U[u][3] = a.w;
         L[u][0] = c.x; L[u][1] = c.y; L[u][2] = c.z; L[u][3] = c.w;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v)
-            if (4 * I + u >= n || 4 * J + v >= n) dead |= 1u << (u * 4 + v);
-    }
+            if (4 * I + u >= n || 4 * J + v >= n) {
+                dead |= 1u << (u * 4 + v);
+                if (I != J || u != v) { U[u][v] = padv; L[v][u] = padv; }
+            }
 }
 
 #define QAPB_SWITCH4(idx, BODY)            \
@@ -115,13 +123,14 @@ __device__ __forceinline__ void unit_update(int32_t (&U)[4][4], int32_t (&L)[4][
 {
     int32_t aI[4], bI[4], aJ[4], bJ[4];
     ld_vec4(V.A, Ik, aI); ld_vec4(V.B, Ik, bI); ld_vec4(V.A, Jk, aJ); ld_vec4(V.B, Jk, bJ);
+    // V.A and V.C hold the NEGATED difference vectors, so the update is a plain multiply-add
     if (SYM) {  // a is pre-doubled: a == c, b == e
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                U[u][v] -= aI[u] * bJ[v];
-                L[v][u] -= aJ[v] * bI[u];
+                U[u][v] += aI[u] * bJ[v];
+                L[v][u] += aJ[v] * bI[u];
             }
     } else {
         int32_t cI[4], eI[4], cJ[4], eJ[4];
@@ -130,8 +139,8 @@ __device__ __forceinline__ void unit_update(int32_t (&U)[4][4], int32_t (&L)[4][
         for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                U[u][v] -= aI[u] * bJ[v] + cI[u] * eJ[v];
-                L[v][u] -= aJ[v] * bI[u] + cJ[v] * eI[u];
+                U[u][v] += aI[u] * bJ[v] + cI[u] * eJ[v];
+                L[v][u] += aJ[v] * bI[u] + cJ[v] * eI[u];
             }
     }
     // Rows / columns r and s.  Block row I == R holds row r in U and column r in L; block column
@@ -182,32 +191,59 @@ _Pragma("unroll")
 // 1 and 16: they issue as IMAD on the FMA pipe.  PACKED: |delta| < 2^27 (host-proven), key =
 // delta*16 + slot orders by (delta, slot), so the running first-minimum is one predicated
 // IMNMX per pair in four independent chains.
+// km = min(km, kd) if the pair is admissible: its tabu bit is clear, or kd < thr16 (aspiration).
+// Written in PTX so that it is LOP3 (bit -> predicate) + ISETP.LT.OR + a predicated VIMNMX.
+template <int BIT>
+__device__ __forceinline__ void admissible_min(int32_t &km, int32_t kd, unsigned tbk, int32_t thr16)
+{
+    asm("{\n\t"
+        ".reg .pred p, q;\n\t"
+        ".reg .b32 t;\n\t"
+        "and.b32 t, %2, %3;\n\t"
+        "setp.eq.u32 q, t, 0;\n\t"
+        "setp.lt.or.s32 p, %1, %4, q;\n\t"
+        "@p min.s32 %0, %0, %1;\n\t"
+        "}"
+        : "+r"(km)
+        : "r"(kd), "r"(tbk), "n"(1u << BIT), "r"(thr16));
+}
+
 template <bool PACKED>
 __device__ __forceinline__ void unit_select(const int32_t (&U)[4][4], const int32_t (&L)[4][4], unsigned tbk, int Ik,
-                                            int Jk, int32_t thr, const int32_t *sH, int one, int sixteen,
+                                            int Jk, int32_t thr, const Vecs &V, int one, int sixteen,
                                             int32_t &dbest, int &sbest)
 {
     const int32_t MAXV = 0x7fffffff;
-    int32_t hI[4], hJ[4];
-    ld_vec4(sH, Ik, hI);
-    ld_vec4(sH, Jk, hJ);
     if (PACKED) {
-        int32_t km[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            km[u] = MAXV;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                const int32_t d = (U[u][v] * one + L[v][u]) - hI[u] - hJ[v];
-                const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
-                const int32_t kd = (int32_t)((uint32_t)d * (uint32_t)sixteen + (uint32_t)(u * 4 + v));
-                if (adm) km[u] = min(km[u], kd);
-            }
-        }
+        // Both pipes of an SMSP issue one warp instruction every two cycles, and the ALU pipe (IADD3 /
+        // LOP3 / ISETP / VIMNMX / SEL) is the busy one in this pass.  The key of a pair,
+        //   kd = 16 delta + slot = (16 U + HI[u]) + (16 L + HJ[v]),   HI = -16 h + 4u,  HJ = -16 h + v,
+        // is therefore three IMADs (FMA pipe; the last one multiplies by the runtime constant 1), and
+        // admissibility + running minimum are exactly three ALU instructions: LOP3 (tabu bit ->
+        // predicate), ISETP.LT.OR (aspiration: kd < 16 thr <=> delta < thr), predicated VIMNMX.
+        int32_t hi[4], hj[4];
+        ld_vec4(V.HI, Ik, hi);
+        ld_vec4(V.HJ, Jk, hj);
+        const int32_t thr16 = max(thr, -(1 << 27)) * 16;  // |delta| < 2^27 (host-proven)
+        int32_t km[4] = {MAXV, MAXV, MAXV, MAXV};
+#define QAPB_PAIR(u, v)                                                             \
+    {                                                                               \
+        const int32_t t1 = U[u][v] * sixteen + hi[u];                               \
+        const int32_t t2 = L[v][u] * sixteen + hj[v];                               \
+        admissible_min<(u) * 4 + (v)>(km[u], t1 * one + t2, tbk, thr16);            \
+    }
+        QAPB_PAIR(0, 0) QAPB_PAIR(0, 1) QAPB_PAIR(0, 2) QAPB_PAIR(0, 3)
+        QAPB_PAIR(1, 0) QAPB_PAIR(1, 1) QAPB_PAIR(1, 2) QAPB_PAIR(1, 3)
+        QAPB_PAIR(2, 0) QAPB_PAIR(2, 1) QAPB_PAIR(2, 2) QAPB_PAIR(2, 3)
+        QAPB_PAIR(3, 0) QAPB_PAIR(3, 1) QAPB_PAIR(3, 2) QAPB_PAIR(3, 3)
+#undef QAPB_PAIR
         const int32_t m = min(min(km[0], km[1]), min(km[2], km[3]));
         dbest = (m == MAXV) ? MAXV : (m >> 4);
         sbest = m & 15;
     } else {
+        int32_t hI[4], hJ[4];
+        ld_vec4(V.H, Ik, hI);
+        ld_vec4(V.H, Jk, hJ);
         int32_t rd[4];
         int rs[4];
 #pragma unroll
@@ -240,7 +276,7 @@ __device__ __forceinline__ void diag_update(int32_t (&U)[4][4], int Ik, int R, i
         for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int v = 0; v < 4; ++v)
-                if (u != v) U[u][v] -= aI[u] * bI[v];
+                if (u != v) U[u][v] += aI[u] * bI[v];
     } else {
         int32_t cI[4], eI[4];
         ld_vec4(V.C, Ik, cI); ld_vec4(V.E, Ik, eI);
@@ -248,7 +284,7 @@ __device__ __forceinline__ void diag_update(int32_t (&U)[4][4], int Ik, int R, i
         for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int v = 0; v < 4; ++v)
-                if (u != v) U[u][v] -= aI[u] * bI[v] + cI[u] * eI[v];
+                if (u != v) U[u][v] += aI[u] * bI[v] + cI[u] * eI[v];
     }
     if (Ik == R) {
         int32_t cs[4], t[4];
@@ -343,6 +379,8 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     V.XR = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(9, NPM));
     V.XS = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(10, NPM));
     int32_t *sP = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(11, NPM));
+    V.HI = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(12, NPM));
+    V.HJ = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(13, NPM));
     long long *sRed64 = reinterpret_cast<long long *>(smem_raw + HYB_REDD(NPM));
     int32_t *sRedD = reinterpret_cast<int32_t *>(smem_raw + HYB_REDD(NPM));
     unsigned *sRedK = reinterpret_cast<unsigned *>(smem_raw + HYB_REDK(NPM));
@@ -385,7 +423,10 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     for (int i = tid; i < npad; i += T) {
         V.A[i] = 0; V.C[i] = 0; V.B[i] = 0; V.E[i] = 0;
         V.ColR[i] = 0; V.ColS[i] = 0; V.TR[i] = 0; V.TS[i] = 0; V.XR[i] = 0; V.XS[i] = 0;
-        V.H[i] = reinterpret_cast<const int32_t *>(P.initH)[(size_t)b * npad + i];
+        const int32_t h0 = reinterpret_cast<const int32_t *>(P.initH)[(size_t)b * npad + i];
+        V.H[i] = h0;
+        V.HI[i] = 4 * (i & 3) - 16 * h0;
+        V.HJ[i] = (i & 3) - 16 * h0;
         sP[i] = P.perm32[(size_t)b * npad + i];
     }
     unsigned long long rng_state = P.rng ? P.start_state[b] : 0ULL;
@@ -427,7 +468,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         if (k == 0 && diag) { I[0] = tid - Toff; J[0] = I[0]; uidv[0] = noff + I[0]; own[0] = true; }
         if (own[k]) {
             unsigned dead;
-            load_unit(Minit, npad, n, I[k], J[k], U[k], L[k], dead);
+            load_unit(Minit, npad, n, I[k], J[k], U[k], L[k], dead, PACKED ? (1 << 25) : (1 << 29));
             if (diag) dead |= 0xF731u;  // slots with u >= v are not pairs of a diagonal block
             tb[k] = dead;
 #pragma unroll
@@ -441,7 +482,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 int32_t Us[4][4], Ls[4][4];
                 unsigned dead;
                 const int Ik = P.unit_ij[uid] & 0xff, Jk = P.unit_ij[uid] >> 8;
-                load_unit(Minit, npad, n, Ik, Jk, Us, Ls, dead);
+                load_unit(Minit, npad, n, Ik, Jk, Us, Ls, dead, PACKED ? (1 << 25) : (1 << 29));
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     st_row(sM, k2 * 8 + u, Toff, tid, Us[u]);
@@ -491,7 +532,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             int sk;
             if (I[k] != J[k]) {
                 if (R >= 0) unit_update<SYM>(U[k], L[k], I[k], J[k], R, S, ru, su, V);
-                unit_select<PACKED>(U[k], L[k], tb[k], I[k], J[k], thr, V.H, one, sixteen, dk, sk);
+                unit_select<PACKED>(U[k], L[k], tb[k], I[k], J[k], thr, V, one, sixteen, dk, sk);
             } else {
                 if (R >= 0) diag_update<SYM>(U[k], I[k], R, S, ru, su, V);
                 diag_select(U[k], tb[k], I[k], thr, V.H, dk, sk);
@@ -523,7 +564,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 }
                 int32_t dk;
                 int sk;
-                unit_select<PACKED>(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V.H, one, sixteen, dk, sk);
+                unit_select<PACKED>(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V, one, sixteen, dk, sk);
                 if (dk != MAXV) {
                     const unsigned key = pair_key(4 * Ik + (sk >> 2), 4 * Jk + (sk & 3), 0);
                     if (dk < my_d || (dk == my_d && key < my_key)) { my_d = dk; my_key = key; my_which = UR + k2; my_slot = sk; }
@@ -569,12 +610,14 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 const int32_t Fpspi = ldF(ps, pi), Fprpi = ldF(pr, pi);
                 const int32_t a = mid ? Dsi - Dri : 0, bb = mid ? Fpspi - Fprpi : 0;
                 const int32_t a2 = 2 * a, b2 = 2 * bb;
-                V.A[i] = a2;
+                V.A[i] = -a2;
                 V.B[i] = bb;
                 V.XR[i] = b2 * ((mid ? Dri : 0) - Drs);
                 V.XS[i] = b2 * (Drs - (mid ? Dsi : 0));
                 if (mid) {
-                    V.H[i] -= a2 * bb;
+                    const int32_t hn = V.H[i] - a2 * bb;
+                    V.H[i] = hn;
+                    if (PACKED) { V.HI[i] = 4 * (i & 3) - 16 * hn; V.HJ[i] = (i & 3) - 16 * hn; }
                     V.TR[i] = a2 * (Fpspr - Fpspi);
                     V.TS[i] = a2 * (Fprpi - Fpspr);
                 } else if (i == r) {
@@ -592,14 +635,16 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 const int32_t a = mid ? Dis - Dir : 0, cc = mid ? Dsi - Dri : 0;
                 const int32_t bb = mid ? Fpips - Fpipr : 0, e = mid ? Fpspi - Fprpi : 0;
                 const int32_t be = bb + e;
-                V.A[i] = a;
+                V.A[i] = -a;
                 V.B[i] = bb;
-                V.C[i] = cc;
+                V.C[i] = -cc;
                 V.E[i] = e;
                 V.XR[i] = -Drs * bb - Dsr * e + (mid ? Dri : 0) * be;
                 V.XS[i] = Dsr * bb + Drs * e - (mid ? Dsi : 0) * be;
                 if (mid) {
-                    V.H[i] -= a * bb + cc * e;
+                    const int32_t hn = V.H[i] - (a * bb + cc * e);
+                    V.H[i] = hn;
+                    if (PACKED) { V.HI[i] = 4 * (i & 3) - 16 * hn; V.HJ[i] = (i & 3) - 16 * hn; }
                     V.TR[i] = a * (Fpspr - (Fpips + Fpspi)) + cc * Fprps;
                     V.TS[i] = a * ((Fpipr + Fprpi) - Fprps) - cc * Fpspr;
                 } else if (i == r) {
@@ -646,8 +691,13 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             const int32_t hr = V.H[r], hs = V.H[s];
             V.TS[r] = hr + (Drs - Dsr) * Fpspr;  // M'[r][s]
             V.TR[s] = hs + (Dsr - Drs) * Fprps;  // M'[s][r]
-            V.H[r] = mrs + (Dsr - Drs) * Fprps;
-            V.H[s] = msr + (Drs - Dsr) * Fpspr;
+            const int32_t hrn = mrs + (Dsr - Drs) * Fprps, hsn = msr + (Drs - Dsr) * Fpspr;
+            V.H[r] = hrn;
+            V.H[s] = hsn;
+            if (PACKED) {
+                V.HI[r] = 4 * ru - 16 * hrn; V.HJ[r] = ru - 16 * hrn;
+                V.HI[s] = 4 * su - 16 * hsn; V.HJ[s] = su - 16 * hsn;
+            }
             if (P.tr_i) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
                 const size_t o = (size_t)b * iters + (c - 1);
                 P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
