@@ -151,15 +151,16 @@ __device__ __forceinline__ void unit_update(int32_t (&U)[4][4], int32_t (&L)[4][
         const bool hI = Ik == R, hJ = Jk == R;
         if (hI | hJ) {
             const int o = hI ? Jk : Ik;
+            const int fI = hI ? 1 : 0, fJ = hJ ? 1 : 0;  // row increments as IMADs (FMA pipe), not SEL + IADD
             int32_t x[4], cs[4], t[4];
             ld_vec4(V.XR, o, x); ld_vec4(V.ColS, o, cs); ld_vec4(V.TR, o, t);
             QAPB_SWITCH4(ru, {
 _Pragma("unroll")
                 for (int w = 0; w < 4; ++w) {
                     const int32_t nv = cs[w] + t[w];
-                    U[q][w] += hI ? x[w] : 0;
+                    U[q][w] += x[w] * fI;
                     L[w][q] = hI ? nv : L[w][q];
-                    L[q][w] += hJ ? x[w] : 0;
+                    L[q][w] += x[w] * fJ;
                     U[w][q] = hJ ? nv : U[w][q];
                 }
             })
@@ -169,15 +170,16 @@ _Pragma("unroll")
         const bool hI = Ik == S, hJ = Jk == S;
         if (hI | hJ) {
             const int o = hI ? Jk : Ik;
+            const int fI = hI ? 1 : 0, fJ = hJ ? 1 : 0;
             int32_t x[4], cr[4], t[4];
             ld_vec4(V.XS, o, x); ld_vec4(V.ColR, o, cr); ld_vec4(V.TS, o, t);
             QAPB_SWITCH4(su, {
 _Pragma("unroll")
                 for (int w = 0; w < 4; ++w) {
                     const int32_t nv = cr[w] + t[w];
-                    U[q][w] += hI ? x[w] : 0;
+                    U[q][w] += x[w] * fI;
                     L[w][q] = hI ? nv : L[w][q];
-                    L[q][w] += hJ ? x[w] : 0;
+                    L[q][w] += x[w] * fJ;
                     U[w][q] = hJ ? nv : U[w][q];
                 }
             })
