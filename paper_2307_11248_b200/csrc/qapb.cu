@@ -248,10 +248,14 @@ static int ensure_ws(qapb_handle *h, size_t bytes)
     return QAPB_OK;
 }
 
-// Upper bound on |M[a][b]| and |h[a]| over all permutations: rearrangement
-// inequality on sorted absolute rows/columns, plus the direct and diagonal terms.
+// Upper bound on |M[a][b]| and |h[a]| over all permutations: rearrangement inequality on sorted
+// absolute rows/columns, plus the direct and diagonal terms.
+//   level 0: 2 n max|D| max|F|                                   O(n^2)
+//   level 1: sorted row/column of D against the elementwise maximum ("envelope") of the
+//            sorted rows/columns of F                            O(n^2 log n)
+//   level 2: sorted row/column of D against every sorted row/column of F      O(n^3)
 static double placement_bound(int n, const std::vector<long long> &F0, const std::vector<long long> &D0,
-                              const std::vector<long long> &fd, const std::vector<long long> &dd, bool refined)
+                              const std::vector<long long> &fd, const std::vector<long long> &dd, int level)
 {
     long long maxF = 0, maxD = 0, maxfd = 0, maxdd = 0;
     for (long long v : F0) maxF = std::max(maxF, std::llabs(v));
@@ -259,7 +263,7 @@ static double placement_bound(int n, const std::vector<long long> &F0, const std
     for (long long v : fd) maxfd = std::max(maxfd, std::llabs(v));
     for (long long v : dd) maxdd = std::max(maxdd, std::llabs(v));
     double extra = 2.0 * (double)maxD * (double)maxF + (double)maxfd * (double)maxdd;
-    if (!refined) return 2.0 * n * (double)maxD * (double)maxF + extra;
+    if (level == 0) return 2.0 * n * (double)maxD * (double)maxF + extra;
     std::vector<std::vector<double>> dr(n), dc(n), fr(n), fc(n);
     for (int a = 0; a < n; ++a) {
         dr[a].resize(n); dc[a].resize(n); fr[a].resize(n); fc[a].resize(n);
@@ -275,6 +279,17 @@ static double placement_bound(int n, const std::vector<long long> &F0, const std
         std::sort(fc[a].begin(), fc[a].end(), std::greater<double>());
     }
     double best = 0;
+    if (level == 1) {
+        std::vector<double> er(n, 0.0), ec(n, 0.0);
+        for (int u = 0; u < n; ++u)
+            for (int k = 0; k < n; ++k) { er[k] = std::max(er[k], fr[u][k]); ec[k] = std::max(ec[k], fc[u][k]); }
+        for (int a = 0; a < n; ++a) {
+            double s = 0;
+            for (int k = 0; k < n; ++k) s += dr[a][k] * er[k] + dc[a][k] * ec[k];
+            best = std::max(best, s);
+        }
+        return best + extra;
+    }
     for (int a = 0; a < n; ++a)
         for (int u = 0; u < n; ++u) {
             double s = 0;
@@ -319,8 +334,10 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
 
     // accumulator width: |delta| <= 4 * bound must stay below 2^31-1 for the int32 state
     const double lim32 = 2147483647.0 / 4.0 - 8.0;
-    double bnd = placement_bound(n, F0, D0, fd, dd, false);
-    if (bnd >= lim32) bnd = placement_bound(n, F0, D0, fd, dd, true);
+    // the cheap envelope bound also decides packed selection keys (|delta| < 2^27); the O(n^3) one
+    // is only worth its time when it can still rescue the int32 state
+    double bnd = std::min(placement_bound(n, F0, D0, fd, dd, 0), placement_bound(n, F0, D0, fd, dd, 1));
+    if (bnd >= lim32) bnd = std::min(bnd, placement_bound(n, F0, D0, fd, dd, 2));
     h->acc_bits = bnd < lim32 ? 32 : 64;
     if (bnd >= 9.0e18 / 4.0) {
         delete h;
