@@ -339,6 +339,34 @@ def run_ours(args) -> None:
                 gap[f"time_to_{g}pct_s"] = hit["seconds"]
                 if cpu:
                     gap[f"cpu_time_to_{g}pct_s_est"] = STARTS_PER_GPU * hit["iterations"] * npairs / cpu["value"]
+        # other QAPLIB shapes of BASELINE.json (configs 1, 3, 4 and the north_star's shape list), same
+        # multistart entry, full waves of starts, device time of the whole start+build+search+pick pipeline
+        shapes_tbl = None
+        if not args.no_shapes:
+            from paper_2307_11248_b200 import shapes as shp
+
+            shapes_tbl = []
+            for name, algo, starts, its in (("nug12", "2opt", 1776, 48), ("tai30a", "tabu", 1, 1000),
+                                            ("tai30a", "tabu", 1776, 240), ("tai64c", "tabu", 1184, 512),
+                                            ("tai100a", "2opt", 1184, 400), ("sko100", "tabu", 1184, 800),
+                                            ("rand100", "tabu", 1184, 800), ("tai150b", "tabu", 296, 1200),
+                                            ("tai256c", "2opt", 148, 1024), ("tai256c", "tabu", 148, 2048)):
+                try:
+                    si = shp.by_name(name)
+                    sd = device_instance(si.flow, si.distance, local)
+                    st_ = q.tenure_bounds(si.n)
+                    ms = None
+                    for rep in range(2):
+                        sd.multistart(algo, rep, 0, starts, its, st_.low, st_.high)
+                        t_ms = sd.last_kernel_ms()
+                        ms = t_ms if ms is None else min(ms, t_ms)
+                    ev = starts * its * si.n * (si.n - 1) // 2
+                    shapes_tbl.append({"shape": name, "n": si.n, "algo": algo, "starts": starts, "iterations": its,
+                                       "ms": ms, "evals_per_s": ev / (ms * 1e-3), "acc_bits": sd.info["acc_bits"],
+                                       "kernel": "hybrid" if sd.info["storage"] == 3 else "generic",
+                                       "threads": sd.info["threads"], "ctas_per_sm": sd.info["ctas_per_sm"]})
+                except Exception as exc:  # pragma: no cover
+                    shapes_tbl.append({"shape": name, "error": repr(exc)})
         print(json.dumps({
             "metric": "swap_move_evals_per_sec", "value": value, "unit": "evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
@@ -353,7 +381,7 @@ def run_ours(args) -> None:
             "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "run_multistart(inst, cfg) with a fresh instance upload per step"},
             "gpu_launches": 4 * args.steps,  # start, build-M, search, pick-best per step
-            "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "time_to_gap": gap, "full_evaluator": full_eval, "result_check": ok,
+            "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "time_to_gap": gap, "full_evaluator": full_eval, "shapes": shapes_tbl, "result_check": ok,
         }))
     if world > 1:
         dist.destroy_process_group()
@@ -377,6 +405,7 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-time-to-gap", action="store_true")
+    ap.add_argument("--no-shapes", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -119,6 +119,16 @@ int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, uint64_t fir
                     int64_t *per_start_costs, int64_t *best_key, int64_t *best_perm,
                     void *stream);
 
+/* The same map for an explicit list of starts: start b runs from the SplitMix64 state
+ * seeds[b] (what rng.py:62-70 `derive_seed(master, index)` returns), so one launch can serve
+ * several (master_seed, index range) runs at once -- the repetitions `master_seed + rep` of
+ * cli.py:113-115 and the seeds axis `+ 7919 * idx` of cli.py:168-175.  No reduction is done:
+ *   per_start_costs: [count]    best cost of each start
+ *   best_perms:      [count,n]  best permutation of each start */
+int qapb_multistart_seeds(qapb_handle *h, int algo, const uint64_t *seeds, int count, int iterations,
+                          int64_t ten_low, int64_t ten_high, int64_t *per_start_costs,
+                          int64_t *best_perms, void *stream);
+
 /* Host-buffer variants (synchronous; copies inside). */
 int qapb_full_cost_host(qapb_handle *h, const int64_t *perms, int batch, int64_t *costs);
 int qapb_all_deltas_host(qapb_handle *h, const int64_t *perms, int batch, int64_t *deltas);
@@ -133,6 +143,10 @@ int qapb_tabu_host(qapb_handle *h, const int64_t *perms, int batch, int iteratio
 int qapb_multistart_host(qapb_handle *h, int algo, uint64_t master_seed, uint64_t first_index,
                          int count, int iterations, int64_t ten_low, int64_t ten_high,
                          int64_t *per_start_costs, int64_t *best_key, int64_t *best_perm);
+
+int qapb_multistart_seeds_host(qapb_handle *h, int algo, const uint64_t *seeds, int count,
+                               int iterations, int64_t ten_low, int64_t ten_high,
+                               int64_t *per_start_costs, int64_t *best_perms);
 
 /* Time of the most recent search-kernel launch sequence on this handle, in
  * milliseconds between CUDA events recorded on the launching stream

@@ -126,6 +126,20 @@ class DeviceInstance:
             ten_low, ten_high, _addr(costs), _addr(key), _addr(perm)))
         return costs, int(key[0]), int(key[1]), perm
 
+    def multistart_seeds(self, algorithm: str, seeds, iterations: int, ten_low: int = 1, ten_high: int = 1):
+        """Host-buffer multistart over explicit per-start SplitMix64 states (`derive_seed` values):
+        (per_start_costs[count], best_perms[count, n]).  One launch for any mix of master seeds."""
+        sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+        if sd.ndim != 1 or sd.size < 1:
+            raise DomainError("seeds must be a non-empty 1-d array")
+        count = int(sd.size)
+        costs = np.empty(count, _i64)
+        perms = np.empty((count, self.n), _i64)
+        algo = _lib.ALGO_TABU if algorithm == "tabu" else _lib.ALGO_2OPT
+        _lib.check(_lib.lib().qapb_multistart_seeds_host(
+            self._h, algo, _addr(sd), count, iterations, ten_low, ten_high, _addr(costs), _addr(perms)))
+        return costs, perms
+
     def multistart_device(self, algorithm: str, master_seed: int, first_index: int, count: int,
                           iterations: int, ten_low: int, ten_high: int,
                           costs_ptr: int, key_ptr: int, perm_ptr: int, stream: int = 0) -> None:

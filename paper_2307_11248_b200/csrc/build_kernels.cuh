@@ -19,6 +19,7 @@ namespace qapb {
 struct StartParams {
     int n, npad, rng, force_seq_rng;
     unsigned long long master_seed, first_index;
+    const unsigned long long *seeds; // [B] explicit per-start states (rng == 1), or null: derive_seed(master, first + b)
     const int64_t *perms;            // [B,n] (rng == 0)
     int32_t *perm32;                 // [B,npad] out
     unsigned long long *state;       // [B] out: SplitMix64 state after the shuffle
@@ -36,7 +37,8 @@ __global__ void __launch_bounds__(128) qap_start_kernel(const StartParams P)
     if (P.rng) {
         // draws computed in parallel assuming no rejection; a rejection (probability ~ n^2/2^64)
         // falls back to the exact sequential loop
-        const unsigned long long seed = mix64(P.master_seed + QAPB_GAMMA * (P.first_index + (unsigned long long)b + 1ULL));
+        const unsigned long long seed =
+            P.seeds ? P.seeds[b] : mix64(P.master_seed + QAPB_GAMMA * (P.first_index + (unsigned long long)b + 1ULL));
         int reject = P.force_seq_rng;
         for (int k = tid; k < n - 1; k += T) {
             unsigned long long bound = (unsigned long long)(n - 1 - k) + 1ULL;

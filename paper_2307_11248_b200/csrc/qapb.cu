@@ -125,13 +125,25 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
 
 static int hybrid_occupancy(const qapb_handle *h)
 {
-    int occ = 0;
+    // the answer depends only on (kernel, CTA size, shared memory, device): remember it, the query
+    // costs more than packing a small instance
+    struct Key { const void *k; int threads; unsigned smem; int device; int occ; };
+    static std::mutex mu;
+    static std::vector<Key> seen;
     const void *k = (const void *)handle_kernel(h);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const Key &e : seen)
+            if (e.k == k && e.threads == h->threads && e.smem == h->smem_bytes && e.device == h->device) return e.occ;
+    }
+    int occ = 0;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes) != cudaSuccess ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, h->threads, h->smem_bytes) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
+    std::lock_guard<std::mutex> lk(mu);
+    seen.push_back({k, h->threads, h->smem_bytes, h->device, occ});
     return occ;
 }
 
@@ -336,7 +348,8 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     const double lim32 = 2147483647.0 / 4.0 - 8.0;
     // the cheap envelope bound also decides packed selection keys (|delta| < 2^27); the O(n^3) one
     // is only worth its time when it can still rescue the int32 state
-    double bnd = std::min(placement_bound(n, F0, D0, fd, dd, 0), placement_bound(n, F0, D0, fd, dd, 1));
+    double bnd = placement_bound(n, F0, D0, fd, dd, 0);
+    if (4.0 * bnd >= (double)((1LL << 27) - 1)) bnd = std::min(bnd, placement_bound(n, F0, D0, fd, dd, 1));
     if (bnd >= lim32) bnd = std::min(bnd, placement_bound(n, F0, D0, fd, dd, 2));
     h->acc_bits = bnd < lim32 ? 32 : 64;
     if (bnd >= 9.0e18 / 4.0) {
@@ -536,12 +549,12 @@ static WsPlan plan_ws(const qapb_handle *h, int batch, size_t head)
 
 // qap_start_kernel + qap_build_m_kernel for `batch` permutations (caller-provided or device-drawn)
 static int launch_build(qapb_handle *h, const WsPlan &w, int batch, int rng, int force_seq, unsigned long long master_seed,
-                        unsigned long long first_index, const int64_t *perms, cudaStream_t st, BuildParams &BP,
-                        StartParams &SP)
+                        unsigned long long first_index, const unsigned long long *seeds, const int64_t *perms,
+                        cudaStream_t st, BuildParams &BP, StartParams &SP)
 {
     const size_t np = (size_t)h->npad;
     SP.n = h->n; SP.npad = h->npad; SP.rng = rng; SP.force_seq_rng = force_seq;
-    SP.master_seed = master_seed; SP.first_index = first_index; SP.perms = perms;
+    SP.master_seed = master_seed; SP.first_index = first_index; SP.seeds = seeds; SP.perms = perms;
     SP.perm32 = (int32_t *)((char *)h->ws + w.offPerm);
     SP.state = (unsigned long long *)((char *)h->ws + w.offState);
     qap_start_kernel<<<batch, 128, 2 * np * sizeof(int32_t), st>>>(SP);
@@ -582,7 +595,7 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     // start permutations (+ stream state), then M and h as one batched tiled integer product
     BuildParams BP;
     StartParams SP;
-    rc = launch_build(h, w, batch, P.rng, P.force_seq_rng, P.master_seed, P.first_index, P.perms, st, BP, SP);
+    rc = launch_build(h, w, batch, P.rng, P.force_seq_rng, P.master_seed, P.first_index, P.seeds, P.perms, st, BP, SP);
     if (rc) return rc;
     P.perm32 = SP.perm32; P.start_state = SP.state; P.initM = BP.M; P.initH = BP.h;
     kern<<<batch, h->threads, h->smem_bytes, st>>>(P);
@@ -624,7 +637,7 @@ extern "C" int qapb_all_deltas(qapb_handle *h, const int64_t *perms, int batch, 
     CU(cudaEventRecord(h->ev0, st));
     BuildParams BP;
     StartParams SP;
-    rc = launch_build(h, w, batch, 0, 0, 0, 0, perms, st, BP, SP);
+    rc = launch_build(h, w, batch, 0, 0, 0, 0, nullptr, perms, st, BP, SP);
     if (rc) return rc;
     const dim3 grid(batch, std::min(h->n - 1, 64));
     if (h->acc_bits == 64) qap_emit_deltas_kernel<int64_t><<<grid, 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
@@ -717,6 +730,44 @@ extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, u
     CU(cudaGetLastError());
     CU(cudaEventRecord(h->ev1, (cudaStream_t)stream));
     return QAPB_OK;
+}
+
+static int check_multistart_args(int algo, int iterations, int64_t ten_low, int64_t ten_high)
+{
+    if (algo != QAPB_ALGO_2OPT && algo != QAPB_ALGO_TABU) return fail(QAPB_ERR_INVALID, "unknown algorithm " + std::to_string(algo));
+    if (iterations < 1) return fail(QAPB_ERR_INVALID, "iterations must be >= 1, got " + std::to_string(iterations));
+    if (algo == QAPB_ALGO_TABU && !(1 <= ten_low && ten_low <= ten_high))
+        return fail(QAPB_ERR_INVALID, "invalid tenure interval [" + std::to_string(ten_low) + ", " + std::to_string(ten_high) + "]");
+    if (algo == QAPB_ALGO_TABU && (double)iterations + (double)ten_high >= 2147483647.0)
+        return fail(QAPB_ERR_UNSUPPORTED, "iterations + tenure must fit int32");
+    return QAPB_OK;
+}
+
+extern "C" int qapb_multistart_seeds(qapb_handle *h, int algo, const uint64_t *seeds, int count, int iterations,
+                                     int64_t ten_low, int64_t ten_high, int64_t *per_start_costs, int64_t *best_perms,
+                                     void *stream)
+{
+    int rc = check_common(h, count);
+    if (rc) return rc;
+    rc = check_multistart_args(algo, iterations, ten_low, ten_high);
+    if (rc) return rc;
+    if (!seeds || !per_start_costs || !best_perms) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    // workspace head: cur perms [count,n], cur costs [count]
+    const size_t perm_bytes = (size_t)count * h->n * sizeof(int64_t);
+    const size_t head = perm_bytes + (size_t)count * sizeof(int64_t);
+    rc = ensure_ws(h, plan_ws(h, count, head).total);
+    if (rc) return rc;
+    SearchParams P;
+    base_params(h, P);
+    P.mode = algo == QAPB_ALGO_TABU ? MODE_TABU : MODE_TWO_OPT;
+    P.rng = 1;
+    P.iterations = iterations;
+    P.seeds = (const unsigned long long *)seeds;
+    P.ten_lo = ten_low;
+    P.ten_hi = ten_high;
+    P.best = best_perms; P.best_cost = per_start_costs;
+    P.cur = (int64_t *)h->ws; P.cur_cost = (int64_t *)((char *)h->ws + perm_bytes);
+    return launch_search(h, P, count, head, (cudaStream_t)stream);
 }
 
 extern "C" int qapb_last_kernel_ms(qapb_handle *h, float *ms)
@@ -854,6 +905,26 @@ extern "C" int qapb_multistart_host(qapb_handle *h, int algo, uint64_t master_se
     memcpy(per_start_costs, host.data(), (size_t)count * 8);
     memcpy(best_key, host.data() + count, 16);
     memcpy(best_perm, host.data() + count + 2, (size_t)h->n * 8);
+    return QAPB_OK;
+}
+
+extern "C" int qapb_multistart_seeds_host(qapb_handle *h, int algo, const uint64_t *seeds, int count, int iterations,
+                                          int64_t ten_low, int64_t ten_high, int64_t *per_start_costs,
+                                          int64_t *best_perms)
+{
+    int rc = check_common(h, count);
+    if (rc) return rc;
+    if (!seeds || !per_start_costs || !best_perms) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    const size_t cb = (size_t)count * 8, pb = (size_t)count * h->n * 8;
+    DevBuf buf;  // [seeds | costs | perms]
+    CU(buf.alloc(2 * cb + pb));
+    char *d = buf.as<char>();
+    H2D(d, seeds, cb);
+    rc = qapb_multistart_seeds(h, algo, (const uint64_t *)d, count, iterations, ten_low, ten_high, (int64_t *)(d + cb),
+                               (int64_t *)(d + 2 * cb), nullptr);
+    if (rc) return rc;
+    D2H(per_start_costs, d + cb, cb);
+    D2H(best_perms, d + 2 * cb, pb);
     return QAPB_OK;
 }
 

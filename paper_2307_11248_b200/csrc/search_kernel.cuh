@@ -89,6 +89,7 @@ struct SearchParams {
     const int64_t *perms;            // [B,n]            (rng == 0)
     const int64_t *tenures;          // [B,iterations]   (tabu, rng == 0)
     unsigned long long master_seed, first_index;
+    const unsigned long long *seeds;  // [B] explicit per-start SplitMix64 states (rng == 1) or null
     long long ten_lo, ten_hi;
     int64_t *best, *best_cost, *cur, *cur_cost;
     int64_t *cells;                  // [B,n,n] or null

@@ -214,3 +214,57 @@ def test_product_never_imports_oracle():
                 text = open(os.path.join(dirpath, fn)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", text, re.M), fn
                 assert "liboracle" not in text, fn
+
+
+def test_derive_seeds_vectorised_matches_scalar():
+    from paper_2307_11248_b200.sweep import derive_seeds
+
+    for master in (0, 7, 2**63 + 5, 2**64 - 1):
+        got = derive_seeds(master, 3, 40)
+        want = [q.derive_seed(master, i) for i in range(3, 43)]
+        assert [int(x) for x in got] == want
+
+
+def test_make_sweep_validation_and_expand():
+    """tuner.py:90-122 rules: axis names, non-empty strictly increasing positive values, powers of
+    two <= 1024 on the instances axis; expand yields (value, rep, master_seed + rep)."""
+    base = q.SearchConfig(algorithm="2opt", n_starts=4, master_seed=10)
+    for bad in (("nope", [1]), ("seeds", []), ("seeds", [0, 1]), ("seeds", [2, 1]), ("instances", [3]),
+                ("instances", [2048])):
+        with pytest.raises(q.DomainError):
+            q.make_sweep(bad[0], bad[1], base)
+    plan = q.make_sweep("instances", [2, 8], base)
+    assert list(q.expand(plan, 2)) == [(2, 0, 10), (2, 1, 11), (8, 0, 10), (8, 1, 11)]
+
+
+def test_run_multistart_many_groups_and_splits():
+    """Grouping by (algorithm, iterations, tenure), concatenated seeds, per-run split, first-minimum
+    tie rule -- with a fake seed runner (cost = seed-derived number), no GPU."""
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.sweep import derive_seeds, run_multistart_many
+
+    inst = shapes.rand(6, 3)
+    calls = []
+
+    def fake(inst_, algorithm, seeds, iterations, low, high):
+        calls.append((algorithm, iterations, low, high, len(seeds)))
+        costs = (seeds % np.uint64(5)).astype(np.int64)  # many ties
+        perms = np.tile(np.arange(inst_.n, dtype=np.int64), (len(seeds), 1))
+        perms[:, 0] = (seeds % np.uint64(1000)).astype(np.int64)  # tag each row with its seed
+        return costs, perms
+
+    cfgs = [q.SearchConfig(algorithm="tabu", n_starts=5, iterations=9, master_seed=1),
+            q.SearchConfig(algorithm="2opt", n_starts=3, iterations=9, master_seed=1),
+            q.SearchConfig(algorithm="tabu", n_starts=7, iterations=9, master_seed=2),
+            q.SearchConfig(algorithm="tabu", n_starts=2, iterations=4, master_seed=1)]
+    res = run_multistart_many(inst, cfgs, _seed_runner=fake)
+    assert sorted(c[4] for c in calls) == [2, 3, 12] and len(calls) == 3  # the two 9-iteration tabu runs share a launch
+    for cfg, r in zip(cfgs, res):
+        seeds = derive_seeds(cfg.master_seed, 0, cfg.n_starts)
+        costs = (seeds % np.uint64(5)).astype(np.int64)
+        assert np.array_equal(r.per_start_costs, costs)
+        k = int(np.flatnonzero(costs == costs.min())[0])
+        assert r.best_start_index == k and r.best.cost == int(costs[k])
+        assert r.best.permutation[0] == int(seeds[k] % np.uint64(1000))
+        assert r.best.seed == q.derive_seed(cfg.master_seed, k)
+        assert r.config_digest == q.config_digest(inst, cfg)

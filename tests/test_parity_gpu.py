@@ -354,3 +354,31 @@ def test_generic_kernel_storage_modes(q, orc, monkeypatch, shape, storage):
         assert np.array_equal(costs, wc) and (kbest, kidx) == (wbc, wbi) and np.array_equal(kperm, wbp)
     finally:
         di.close()
+
+
+def test_batched_runs_equal_separate_calls(q):
+    """sweep.run_multistart_many / run_repetitions / run_sweep: one launch per (algorithm, iterations,
+    tenure) group gives the MultiStartResult of separate run_multistart calls (cli.py:109-116,162-175)."""
+    from dataclasses import replace
+
+    from paper_2307_11248_b200 import shapes
+
+    inst = shapes.rand(23, 6)
+    base = q.SearchConfig(algorithm="tabu", n_starts=12, iterations=40, master_seed=3)
+    cfgs = [base, replace(base, master_seed=4), replace(base, algorithm="2opt", iterations=25),
+            replace(base, n_starts=5, master_seed=3 + 7919), replace(base, iterations=17)]
+    many = q.run_multistart_many(inst, cfgs)
+    for cfg, got in zip(cfgs, many):
+        want = q.run_multistart(inst, cfg)
+        assert np.array_equal(got.per_start_costs, want.per_start_costs)
+        assert (got.best.cost, got.best_start_index, got.best.seed) == (want.best.cost, want.best_start_index, want.best.seed)
+        assert np.array_equal(got.best.permutation, want.best.permutation)
+        assert got.config_digest == want.config_digest
+    reps = q.run_repetitions(inst, base, 3)
+    assert [r.best.cost for r in reps] == [q.run_multistart(inst, replace(base, master_seed=3 + k)).best.cost for k in range(3)]
+    rows = q.run_sweep(inst, q.make_sweep("seeds", [1, 3], base), 2)
+    for value, rep, cost in rows:
+        want = min(q.run_multistart(inst, replace(base, master_seed=3 + rep + 7919 * idx)).best.cost for idx in range(value))
+        assert cost == want
+    rows = q.run_sweep(inst, q.make_sweep("neighborhoods", [10, 30], base), 1)
+    assert [c for _, _, c in rows] == [q.run_multistart(inst, replace(base, iterations=v)).best.cost for v in (10, 30)]
