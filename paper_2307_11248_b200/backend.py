@@ -16,6 +16,7 @@ from __future__ import annotations
 import ctypes
 import hashlib
 import threading
+import weakref
 from collections import OrderedDict
 
 import numpy as np
@@ -161,26 +162,52 @@ _CACHE_LOCK = threading.Lock()
 _CACHE_MAX = 8
 
 
+# read-only matrices (every `Instance` freezes its arrays, instance.py:47) are recognised by identity, so
+# repeated calls on one instance do not re-hash 2 n^2 words: (id(flow), id(dist), device) -> weak refs + handle
+_ID_CACHE: dict = {}
+
+
+def _frozen(a) -> bool:
+    return isinstance(a, np.ndarray) and a.dtype == _i64 and a.flags.c_contiguous and not a.flags.writeable
+
+
+_SERIAL = [0]
+
+
 def device_instance(flow, dist, device: int = 0) -> DeviceInstance:
-    """Cached `DeviceInstance` keyed by matrix contents (not identity)."""
-    f, d = _mat(flow), _mat(dist)
-    digest = hashlib.blake2b(f.tobytes() + d.tobytes(), digest_size=16).digest()
-    key = (f.shape, digest, device)
+    """Cached `DeviceInstance`: by identity for frozen arrays (no hashing), else keyed by matrix contents.
+    Both kinds live in one LRU that closes evicted handles."""
+    by_id = _frozen(flow) and _frozen(dist)
     with _CACHE_LOCK:
-        hit = _CACHE.get(key)
-        if hit is not None:
+        if by_id:
+            hit = _ID_CACHE.get((id(flow), id(dist), device))
+            if hit is not None and hit[0]() is flow and hit[1]() is dist and hit[2]._h:
+                return hit[2]
+            _SERIAL[0] += 1
+            key = ("id", _SERIAL[0])
+            f, d = flow, dist
+        else:
+            f, d = _mat(flow), _mat(dist)
+            key = (f.shape, hashlib.blake2b(f.tobytes() + d.tobytes(), digest_size=16).digest(), device)
+        inst = _CACHE.get(key)
+        if inst is not None:
             _CACHE.move_to_end(key)
-            return hit
+            return inst
         inst = DeviceInstance(f, d, device)
         _CACHE[key] = inst
         while len(_CACHE) > _CACHE_MAX:
             _, old = _CACHE.popitem(last=False)
             old.close()
+        if by_id:
+            for k in [k for k, v in _ID_CACHE.items() if v[0]() is None or v[1]() is None or not v[2]._h]:
+                del _ID_CACHE[k]
+            _ID_CACHE[(id(flow), id(dist), device)] = (weakref.ref(flow), weakref.ref(dist), inst)
         return inst
 
 
 def clear_cache() -> None:
     with _CACHE_LOCK:
+        _ID_CACHE.clear()
         while _CACHE:
             _, old = _CACHE.popitem()
             old.close()

@@ -122,9 +122,12 @@ def _cuda_shard_runner(inst: Instance, cfg: SearchConfig, first_index: int, coun
         raise QapError("no CUDA device: the multi-start path has no CPU fallback")
     dev = torch.cuda.current_device()
     device = torch.device("cuda", dev)
-    costs = torch.empty(count, dtype=torch.int64, device=device)
-    key = torch.full((2,), _I64_MAX, dtype=torch.int64, device=device)
-    perm = torch.zeros(inst.n, dtype=torch.int64, device=device)
+    # one device block [costs | key | perm]: a single read-back on the single-GPU path
+    block = torch.empty(count + 2 + inst.n, dtype=torch.int64, device=device)
+    costs, key, perm = block[:count], block[count:count + 2], block[count + 2:]
+    if count == 0:
+        key.fill_(_I64_MAX)
+        perm.zero_()
     if count > 0:
         ten = cfg.resolved_tenure(inst.n)
         di = device_instance(inst.flow, inst.distance, dev)
@@ -196,6 +199,10 @@ def run_multistart(inst: Instance, cfg: SearchConfig, *, group=None, _shard_runn
             parts[r][: shard_bounds(cfg.n_starts, world, r)[1] - shard_bounds(cfg.n_starts, world, r)[0]].cpu().numpy()
             for r in range(world)])
     else:
+        base = costs._base
+        if base is not None and base is key._base and base is perm._base and base.numel() == hi - lo + 2 + inst.n:
+            host = base.cpu()  # [costs | key | perm] in one transfer
+            costs, key, perm = host[:hi - lo], host[hi - lo:hi - lo + 2], host[hi - lo + 2:]
         key_h = key.cpu()
         best_cost, best_index = int(key_h[0]), int(key_h[1])
         per_start = costs.cpu().numpy()
