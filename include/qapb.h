@@ -59,6 +59,7 @@ typedef struct qapb_info {
     int32_t threads;        /* CTA size of the search kernel                          */
     int32_t units_per_thread;
     int32_t storage;        /* 0: placement matrix in shared memory, 1: in L2/global,
+                               2: placement matrix and tabu masks in L2/global,
                                3: hybrid kernel (registers + shared memory)           */
     int32_t smem_bytes;     /* dynamic shared memory per CTA                          */
     int32_t ctas_per_sm;    /* resident searches per SM (occupancy query)             */

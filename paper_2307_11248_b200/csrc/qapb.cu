@@ -58,9 +58,11 @@ typedef void (*kern_t)(const SearchParams);
 static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
 {
 #define K(A, S, MT, MB) (kern_t) qap_search_kernel<A, S, MT, MB>
-    static kern_t tab[2][2][2] = {
-        {{K(int32_t, 0, 384, 2), K(int32_t, 0, 512, 1)}, {K(int32_t, 1, 384, 2), K(int32_t, 1, 512, 1)}},
-        {{K(int64_t, 0, 384, 1), K(int64_t, 0, 512, 1)}, {K(int64_t, 1, 384, 1), K(int64_t, 1, 512, 1)}},
+    static kern_t tab[2][3][2] = {
+        {{K(int32_t, 0, 384, 2), K(int32_t, 0, 512, 1)}, {K(int32_t, 1, 384, 2), K(int32_t, 1, 512, 1)},
+         {K(int32_t, 2, 384, 2), K(int32_t, 2, 512, 1)}},
+        {{K(int64_t, 0, 384, 1), K(int64_t, 0, 512, 1)}, {K(int64_t, 1, 384, 1), K(int64_t, 1, 512, 1)},
+         {K(int64_t, 2, 384, 1), K(int64_t, 2, 512, 1)}},
     };
 #undef K
     return tab[acc_bits == 64][storage][lb_class];
@@ -384,10 +386,11 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     if (h->acc_bits == 32 && nb <= 64 && !(force && force[0] == '1') && plan_hybrid(h, smem_cap)) {
         storage = 3;
     } else {
-        // generic kernel: M in shared memory when it fits, else in an L2-resident workspace
-        const char *fs = getenv("QAPB_FORCE_STORAGE");  // development: 1
+        // generic kernel: M in shared memory when it fits, else in an L2-resident workspace, else
+        // (n > ~700) the per-unit tabu masks too
+        const char *fs = getenv("QAPB_FORCE_STORAGE");  // development: 1 or 2
         storage = -1;
-        for (int k = (fs && fs[0] == '1') ? 1 : 0; k < 2; ++k) {
+        for (int k = (fs && (fs[0] == '1' || fs[0] == '2')) ? fs[0] - '0' : 0; k < 3; ++k) {
             SmemLayout L = make_layout(npad, h->nunits, threads, upt, acc_bytes, k);
             if (L.total <= smem_cap) { h->smem_bytes = L.total; storage = k; break; }
         }
@@ -533,10 +536,10 @@ static WsPlan plan_ws(const qapb_handle *h, int batch, size_t head)
     const size_t acc_bytes = h->acc_bits / 8, np = (size_t)h->npad;
     WsPlan w;
     w.m_elems = (size_t)h->upt * 8 * h->threads * 4;
-    w.x_elems = (size_t)h->nunits * 16;
+    w.x_elems = (size_t)h->nunits * 16 + (h->storage == 2 ? (size_t)2 * h->upt * h->threads : 0);
     size_t o = up(head);
     w.offM = o;
-    if (h->storage == 1) o += up(w.m_elems * acc_bytes * batch);
+    if (h->storage == 1 || h->storage == 2) o += up(w.m_elems * acc_bytes * batch);
     w.offT = o;
     if (h->storage != 3 || !h->exp_in_smem) o += up(w.x_elems * sizeof(int32_t) * batch);
     w.offPerm = o;  o += up(np * 4 * batch);

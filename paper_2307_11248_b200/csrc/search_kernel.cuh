@@ -51,7 +51,8 @@ __host__ __device__ inline SmemLayout make_layout(int npad, int nunits, int T, i
     L.offM = o;
     if (storage == 0) o += (unsigned)upt * 8u * (unsigned)T * 4u * (unsigned)acc_bytes;
     o = align16(o);
-    L.offT = o; o += (unsigned)upt * (unsigned)T * 8u;  // per unit: 16-bit tabu mask word + earliest expiry
+    L.offT = o;
+    if (storage <= 1) o += (unsigned)upt * (unsigned)T * 8u;  // per unit: 16-bit tabu mask word + earliest expiry
     o = align16(o);
     L.offA = o; o += 4u * npad;
     L.offC = o; o += 4u * npad;
@@ -289,7 +290,8 @@ __device__ __forceinline__ ElemLoc locate(int x, int y, int nb, int noff, int T)
 
 // -----------------------------------------------------------------------------
 // The generic search kernel: any n <= 1020, int32 or int64 state.  STORAGE 0 keeps M in
-// shared memory, STORAGE 1 in an L2-resident workspace.  Start permutation, stream state,
+// shared memory, STORAGE 1 in an L2-resident workspace, STORAGE 2 (n > ~700) also keeps the
+// per-unit tabu masks there.  Start permutation, stream state,
 // M and h come from qap_start_kernel / qap_build_m_kernel (build_kernels.cuh).  M is
 // streamed through registers one row pair at a time (row u of the upper block with row u of
 // the transposed lower block), so eight accumulators are live per thread.  The tabu
@@ -322,9 +324,10 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
 
     acc_t *M = STORAGE == 0 ? reinterpret_cast<acc_t *>(smem_raw + lay.offM)
                             : reinterpret_cast<acc_t *>(P.gM) + (size_t)b * P.gM_stride;
-    unsigned *sTB = reinterpret_cast<unsigned *>(smem_raw + lay.offT);  // [upt*T] tabu-now masks
+    int32_t *xp = reinterpret_cast<int32_t *>(P.gT) + (size_t)b * P.gT_stride;  // [nunits*16] (+ masks, STORAGE 2)
+    unsigned *sTB = STORAGE <= 1 ? reinterpret_cast<unsigned *>(smem_raw + lay.offT)  // [upt*T] tabu-now masks
+                                 : reinterpret_cast<unsigned *>(xp + (size_t)nunits * 16);
     int32_t *sMX = reinterpret_cast<int32_t *>(sTB + (size_t)upt * T);  // [upt*T] earliest expiry
-    int32_t *xp = reinterpret_cast<int32_t *>(P.gT) + (size_t)b * P.gT_stride;  // [nunits*16]
     int32_t *sA = reinterpret_cast<int32_t *>(smem_raw + lay.offA);
     int32_t *sC = reinterpret_cast<int32_t *>(smem_raw + lay.offC);
     int32_t *sB = reinterpret_cast<int32_t *>(smem_raw + lay.offB);

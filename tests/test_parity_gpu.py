@@ -311,11 +311,11 @@ def test_tabu_not_worse_than_two_opt_and_dominance(q):
     assert np.array_equal(large.per_start_costs[:16], small.per_start_costs)
 
 
-@pytest.mark.parametrize("storage", ["0", "1"])
+@pytest.mark.parametrize("storage", ["0", "1", "2"])
 @pytest.mark.parametrize("shape", ["rand23", "tai30a", "tai45b"])
 def test_generic_kernel_storage_modes(q, orc, monkeypatch, shape, storage):
-    """Both placements of the generic kernel's state (M in shared memory / M in L2), int32 (rand,
-    tai*a) and int64 (tai*b) state."""
+    """Every placement of the generic kernel's state (M in shared memory / M in L2 / M and the tabu
+    masks in L2), int32 (rand, tai*a) and int64 (tai*b) state."""
     from paper_2307_11248_b200 import shapes
     from paper_2307_11248_b200.backend import DeviceInstance
 
@@ -382,3 +382,41 @@ def test_batched_runs_equal_separate_calls(q):
         assert cost == want
     rows = q.run_sweep(inst, q.make_sweep("neighborhoods", [10, 30], base), 1)
     assert [c for _, _, c in rows] == [q.run_multistart(inst, replace(base, iterations=v)).best.cost for v in (10, 30)]
+
+
+@pytest.mark.parametrize("n,iters", [(257, 6), (400, 4), (1020, 2)])
+def test_sizes_beyond_the_hybrid_plans(q, orc, n, iters):
+    """n > 256 runs in the generic kernel with M in the L2-resident workspace; n = 1020 is the largest
+    supported size.  Few iterations: the oracle is O(n^3) per iteration."""
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.backend import device_instance
+
+    inst = shapes.rand(n, 77)
+    info = device_instance(inst.flow, inst.distance).info
+    assert info["storage"] == (2 if n > 700 else 1) and info["acc_bits"] == 32
+    rng = orc.Rng(orc.derive_seed(5, n))
+    perm = rng.permutation(n)
+    lo, hi = orc.tenure_bounds(n)
+    ten = rng.tenures(lo, hi, iters)
+    assert np.array_equal(q.kernels.all_deltas(inst.flow, inst.distance, perm), orc.all_deltas(inst.flow, inst.distance, perm))
+    got = q.kernels.tabu_run(inst.flow, inst.distance, perm, iters, ten)
+    want = orc.tabu_run(inst.flow, inst.distance, perm, iters, ten)
+    for idx, (g, w) in enumerate(zip(got[:7], want[:7])):
+        assert np.array_equal(g, w), f"n={n} tabu output {idx}"
+    for idx, (g, w) in enumerate(zip(got[7], want[7])):
+        assert np.array_equal(g, w), f"n={n} trail {idx}"
+
+
+def test_unsupported_sizes_and_values(q):
+    """n > 1020 and |entry| >= 2^30 are refused with QapError (status QAPB_ERR_UNSUPPORTED), not computed wrongly."""
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    big = np.zeros((1021, 1021), np.int64)
+    with pytest.raises(q.QapError):
+        DeviceInstance(big, big)
+    f = np.zeros((4, 4), np.int64)
+    f[0, 1] = 1 << 30
+    with pytest.raises(q.QapError):
+        DeviceInstance(f, np.ones((4, 4), np.int64))
+    with pytest.raises(q.DomainError):
+        DeviceInstance(np.zeros((1, 1), np.int64), np.zeros((1, 1), np.int64))
