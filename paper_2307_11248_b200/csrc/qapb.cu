@@ -40,6 +40,7 @@ struct qapb_handle {
     int lb_class = 0;  // 0: <=384 threads, 2 CTAs/SM register budget; 1: <=512 threads
     int toff = 0, us = 0, exp_in_smem = 1;         // hybrid plan
     int staged = 0, fits_i16 = 0;                  // int16 copies of D/F staged in shared memory
+    int dsm = 0;                                   // hybrid: diagonal blocks in shared memory (no dedicated warps)
     unsigned smem_bytes = 0;
     int ctas_per_sm = 0, sm_count = 0;
     long long delta_bound = 0;
@@ -75,12 +76,14 @@ static kern_t pick_hybrid_kernel(int symmetric, int packed, int plan)
     // plan 2: two register units + shared-memory units per thread, 128 registers (n <= 256)
     // plan 3/4: two register units per thread on half the threads, 112 registers (109 <= n <= 120:
     //           two CTAs per SM where plan 0/1 would fit only one), without / with int16 staging
+    // plan 5: plan 2 with the diagonal blocks in shared memory (no dedicated diagonal warps)
 #define KH(S, PK) {(kern_t) qap_search_hybrid_kernel<S, PK, 1, false, false, 80>, \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, true, 80>,  \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128>,  \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, false, 112>, \
-                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, true, 112>}
-    static kern_t tab[2][2][5] = {{KH(false, false), KH(false, true)}, {KH(true, false), KH(true, true)}};
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, true, 112>, \
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128, true>}
+    static kern_t tab[2][2][6] = {{KH(false, false), KH(false, true)}, {KH(true, false), KH(true, true)}};
 #undef KH
     return tab[symmetric != 0][packed != 0][plan];
 }
@@ -88,24 +91,29 @@ static kern_t handle_kernel(const qapb_handle *h)
 {
     // packed (delta, slot) keys need |delta|*16 + 15 < 2^31
     const int packed = h->delta_bound < ((1LL << 27) - 1);
-    return h->storage == 3 ? pick_hybrid_kernel(h->symmetric, packed, h->us > 0 ? 2 : (h->upt == 2 ? (h->staged ? 4 : 3) : (h->staged ? 1 : 0)))
+    int plan = h->us > 0 ? 2 : (h->upt == 2 ? (h->staged ? 4 : 3) : (h->staged ? 1 : 0));
+    if (h->dsm) plan = 5;
+    return h->storage == 3 ? pick_hybrid_kernel(h->symmetric, packed, plan)
                            : pick_kernel(h->acc_bits, h->storage, h->lb_class);
 }
 
 // Split of the off-diagonal units of one search between registers (UR per thread) and shared
 // memory (US per thread) for the hybrid kernel.  Returns false if the instance does not fit.
-static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff, int us)
+static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff, int us, int dsm = 0,
+                            unsigned smem_target = 0)
 {
     const int nb = h->nb, dw = (nb + 31) / 32;
-    const int threads = toff + 32 * dw;
+    const int threads = dsm ? toff : toff + 32 * dw;
+    if (dsm && !(ur == 2 && us > 0)) return false;  // the instantiated shape
+    if (dsm && threads < nb) return false;
     if ((long long)(ur + us) * toff < h->noff) return false;
     if (threads > 1024 || (us > 0 && threads > 512) || (us == 0 && ur == 2 && threads > 608)) return false;
     int exp_in_smem = 1;
-    HybLayout L = make_hyb_layout(h->npad, nb, toff, us, 1);
+    HybLayout L = make_hyb_layout(h->npad, nb, toff, us, 1, 0, 1, dsm);
     // keep the expiry array in shared memory only while it does not cost a resident CTA
-    if (L.total > smem_cap && us > 0) {
+    if (L.total > (smem_target ? smem_target : smem_cap) && us > 0) {
         exp_in_smem = 0;
-        L = make_hyb_layout(h->npad, nb, toff, us, 0);
+        L = make_hyb_layout(h->npad, nb, toff, us, 0, 0, 1, dsm);
     }
     if (L.total > smem_cap) return false;
     if (threads < h->n) return false;  // the publish phase maps one location per thread
@@ -114,10 +122,11 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     int staged = 0;
     if (us == 0 && h->fits_i16 && !getenv("QAPB_NO_STAGE")) {
         // stage while two CTAs per SM still fit
-        HybLayout Ls = make_hyb_layout(h->npad, nb, toff, us, exp_in_smem, 1, h->symmetric);
-        if (Ls.total <= std::min(smem_cap, 110u * 1024u)) { staged = 1; L = Ls; }
+        HybLayout Ls = make_hyb_layout(h->npad, nb, toff, us, exp_in_smem, 1, h->symmetric, dsm);
+        if (Ls.total <= std::min(smem_cap, (dsm ? 74u : 110u) * 1024u)) { staged = 1; L = Ls; }
     }
     h->staged = staged;
+    h->dsm = dsm;
     h->upt = ur; h->toff = toff; h->us = us; h->exp_in_smem = exp_in_smem;
     h->threads = threads;
     h->lb_class = 0;
@@ -160,11 +169,23 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
     const int nb = h->nb, noff = h->noff;
     h->storage = 3;  // handle_kernel() dispatches on it
     if (const char *pl = getenv("QAPB_PLAN")) {  // development override: "UR,Toff,US"
-        int a, b, c;
-        if (sscanf(pl, "%d,%d,%d", &a, &b, &c) == 3 && (a == 1 || a == 2) && b % 32 == 0 && b >= 0 && c >= 0)
-            return try_hybrid_plan(h, smem_cap, a, b, c);
+        int a, b, c, d = 0, e = 0;
+        if (sscanf(pl, "%d,%d,%d,%d,%d", &a, &b, &c, &d, &e) >= 3 && (a == 1 || a == 2) && b % 32 == 0 && b >= 0 && c >= 0)
+            return try_hybrid_plan(h, smem_cap, a, b, c, d, (unsigned)e * 1024u);
     }
     if (nb > 32) {
+        // n = 129..256: every warp on off-diagonal units (two in registers + the rest in shared memory per
+        // thread), the diagonal blocks in shared memory with the last nb threads (DSM).  Preferred: 256
+        // threads with the expiry array in L2 if that keeps TWO searches resident per SM (n <= ~190:
+        // 545 / 559 / 616 G evals/s at n = 144 / 160 / 180 against 420 / 376 / 442 for the dedicated-
+        // diagonal-warp plan); else all 512 threads on one search (4 units per thread at n = 256
+        // instead of 4 or 5 on 14 of 16 warps: 710 -> 750 G evals/s).
+        if (!getenv("QAPB_NO_DSM")) {
+            const int us2 = std::max(1, (noff - 2 * 256 + 255) / 256);
+            if (try_hybrid_plan(h, smem_cap, 2, 256, us2, 1, 113u * 1024u) && hybrid_occupancy(h) >= 2) return true;
+            const int us1 = std::max(1, (noff - 2 * 512 + 511) / 512);
+            if (try_hybrid_plan(h, smem_cap, 2, 512, us1, 1)) return true;
+        }
         const int toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
         const int us = std::max(0, (noff - 2 * toff + toff - 1) / toff);
         return try_hybrid_plan(h, smem_cap, 2, toff, us);
@@ -588,8 +609,8 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     P.gT_stride = w.x_elems;
     kern_t kern = handle_kernel(h);
     if (h->storage == 3) {
-        P.hlay = make_hyb_layout(h->npad, h->nb, h->toff, h->us, h->exp_in_smem, h->staged, h->symmetric);
-        P.staged = h->staged;
+        P.hlay = make_hyb_layout(h->npad, h->nb, h->toff, h->us, h->exp_in_smem, h->staged, h->symmetric, h->dsm);
+        P.staged = h->staged; P.dsm = h->dsm;
         P.toff = h->toff; P.us = h->us; P.exp_in_smem = h->exp_in_smem;
     } else P.lay = make_layout(h->npad, h->nunits, h->threads, h->upt, h->acc_bits / 8, h->storage);
     // several handles share one kernel instantiation: (re)assert this launch's opt-in size

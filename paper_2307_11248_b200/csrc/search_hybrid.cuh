@@ -42,7 +42,7 @@ namespace qapb {
 #define HYB_FIXED_END(NPM) (HYB_TEN(NPM) + 4 * TENURE_CHUNK)
 
 __host__ __device__ inline HybLayout make_hyb_layout(int npad, int nb, int toff, int us, int exp_in_smem,
-                                                     int staged = 0, int symmetric = 1)
+                                                     int staged = 0, int symmetric = 1, int dsm = 0)
 {
     HybLayout L;
     const unsigned npm = npad <= 128 ? 128u : 256u;
@@ -58,6 +58,8 @@ __host__ __device__ inline HybLayout make_hyb_layout(int npad, int nb, int toff,
     L.offM = o; o += (unsigned)us * 8u * (unsigned)toff * 16u;
     L.offTB = o; o += align16(4u * (unsigned)us * (unsigned)toff);
     L.offMX = o; o += align16(4u * (unsigned)us * (unsigned)toff);
+    L.offDG = o;   // diagonal blocks in shared memory (DSM plans): 16 words + mask + earliest expiry each
+    if (dsm) o += 64u * (unsigned)nb + align16(8u * (unsigned)nb);
     const unsigned m16 = staged ? align16(2u * (unsigned)npad * (unsigned)npad) : 0u;
     L.offD16 = o; o += m16;
     L.offF16 = o; o += m16;
@@ -354,7 +356,7 @@ __device__ __forceinline__ void expire_bits(unsigned &tb, int32_t &mexp, int c, 
     mexp = nm;
 }
 
-template <bool SYM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG>
+template <bool SYM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG, bool DSM = false>
 __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -455,7 +457,15 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     // ---- unit ownership.  tb = mask of pairs that are tabu now (pads / non-pairs permanently
     // set, expiry MAXV), mexp = earliest expiry among the clearable bits.
     const bool offt = tid < Toff;
-    const bool diag = tid >= Toff && (tid - Toff) < nb;
+    // diagonal blocks: one per thread of the last warps in registers, or (DSM) in shared memory, owned by
+    // the last nb threads of the CTA in addition to their off-diagonal units
+    const bool diag = !DSM && tid >= Toff && (tid - Toff) < nb;
+    const bool dsm_owner = DSM && tid >= T - nb;
+    const int dsmI = T - 1 - tid;  // diagonal block of a DSM owner
+    int32_t *sDG = reinterpret_cast<int32_t *>(smem_raw + lay.offDG);              // [nb][16]
+    unsigned *sDGtb = reinterpret_cast<unsigned *>(smem_raw + lay.offDG) + 16 * nb;  // [nb]
+    int32_t *sDGmx = reinterpret_cast<int32_t *>(sDGtb + nb);                        // [nb]
+    constexpr int WHICH_DIAG = 1000;
     int I[UR], J[UR], uidv[UR];
     bool own[UR];
     int32_t U[UR][4][4], L[UR][4][4];
@@ -476,6 +486,18 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
 #pragma unroll
             for (int q = 0; q < 16; ++q) xp[uidv[k] * 16 + q] = ((dead >> q) & 1u) ? MAXV : 0;
         }
+    }
+    if (dsm_owner) {
+        int32_t Ud[4][4], Ld[4][4];
+        unsigned dead;
+        load_unit(Minit, npad, n, dsmI, dsmI, Ud, Ld, dead, PACKED ? (1 << 25) : (1 << 29));
+        dead |= 0xF731u;  // slots with u >= v are not pairs of a diagonal block
+#pragma unroll
+        for (int u = 0; u < 4; ++u) st_vec4(sDG + 16 * dsmI, u, Ud[u][0], Ud[u][1], Ud[u][2], Ud[u][3]);
+        sDGtb[dsmI] = dead;
+        sDGmx[dsmI] = MAXV;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) xp[(noff + dsmI) * 16 + q] = ((dead >> q) & 1u) ? MAXV : 0;
     }
     if (SMEMU && offt) {
         for (int k2 = 0; k2 < US; ++k2) {
@@ -573,6 +595,23 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 }
             }
         }
+        if (dsm_owner) {
+            int32_t Ud[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) ld_vec4(sDG + 16 * dsmI + 4 * u, 0, Ud[u]);
+            if (R >= 0) {
+                diag_update<SYM>(Ud, dsmI, R, S, ru, su, V);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) st_vec4(sDG + 16 * dsmI, u, Ud[u][0], Ud[u][1], Ud[u][2], Ud[u][3]);
+            }
+            int32_t dk;
+            int sk;
+            diag_select(Ud, sDGtb[dsmI], dsmI, thr, V.H, dk, sk);
+            if (dk != MAXV) {
+                const unsigned key = pair_key(4 * dsmI + (sk >> 2), 4 * dsmI + (sk & 3), 0);
+                if (dk < my_d || (dk == my_d && key < my_key)) { my_d = dk; my_key = key; my_which = WHICH_DIAG; my_slot = sk; }
+            }
+        }
 
         if (timing) tB = clock64();
         int32_t bd = my_d;
@@ -665,7 +704,16 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             const int32_t new_exp = (int32_t)(c + ten);
             int32_t mrs = 0, msr = 0;
             unsigned was = 0;
-            if (!SMEMU || my_which < UR) {
+            if (DSM && my_which == WHICH_DIAG) {
+                mrs = sDG[16 * dsmI + ru * 4 + su];
+                msr = sDG[16 * dsmI + su * 4 + ru];
+                was = (sDGtb[dsmI] >> my_slot) & 1u;
+                if (tabu) {
+                    sDGtb[dsmI] |= 1u << my_slot;
+                    sDGmx[dsmI] = min(sDGmx[dsmI], new_exp);
+                    xp[(noff + dsmI) * 16 + my_slot] = new_exp;
+                }
+            } else if (!SMEMU || my_which < UR) {
 #pragma unroll
                 for (int k = 0; k < UR; ++k) {
                     if (k != my_which) continue;
@@ -758,6 +806,20 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                     sTB[k2 * Toff + tid] = tbv;
                     sMX[k2 * Toff + tid] = mx;
                 }
+            }
+        }
+        if (dsm_owner) {
+            const int32_t *dg = sDG + 16 * dsmI;
+            if (dsmI == R)
+                st_vec4(V.ColR, dsmI, ru == 0 ? 0 : dg[0 + ru], ru == 1 ? 0 : dg[4 + ru], ru == 2 ? 0 : dg[8 + ru], ru == 3 ? 0 : dg[12 + ru]);
+            if (dsmI == S)
+                st_vec4(V.ColS, dsmI, su == 0 ? 0 : dg[0 + su], su == 1 ? 0 : dg[4 + su], su == 2 ? 0 : dg[8 + su], su == 3 ? 0 : dg[12 + su]);
+            int32_t mx = sDGmx[dsmI];
+            if (c + 1 >= mx) {
+                unsigned tbv = sDGtb[dsmI];
+                expire_bits(tbv, mx, c + 1, xp + (noff + dsmI) * 16);
+                sDGtb[dsmI] = tbv;
+                sDGmx[dsmI] = mx;
             }
         }
         if (timing) tF = clock64();

@@ -73,7 +73,7 @@ __host__ __device__ inline SmemLayout make_layout(int npad, int nunits, int T, i
 
 struct HybLayout {  // search_hybrid.cuh
     unsigned offM, offTB, offMX, offA, offC, offB, offE, offH, offColR, offColS, offTR, offTS, offXR, offXS;
-    unsigned offP, offJ, offRedD, offRedK, offMisc, offTen, offExp, offD16, offF16, offDT16, offFT16, total;
+    unsigned offP, offJ, offRedD, offRedK, offMisc, offTen, offExp, offD16, offF16, offDT16, offFT16, offDG, total;
 };
 
 struct SearchParams {
@@ -107,6 +107,7 @@ struct SearchParams {
     const void *initM, *initH;       // [B,npad,npad], [B,npad] from qap_build_m_kernel (int32 or int64 state)
     int toff, us, exp_in_smem;       // hybrid plan: off-diagonal threads, shared-memory units per thread
     int staged;                      // hybrid: int16 copies of D, F (and transposes) staged in shared memory
+    int dsm;                         // hybrid: diagonal blocks in shared memory, owned by the last nb threads
 };
 
 // ---- accumulator traits -----------------------------------------------------
