@@ -74,12 +74,25 @@ struct Vecs {
     int32_t *HI, *HJ;  // packed-key forms of h: HI[i] = -16 h[i] + 4 (i & 3), HJ[i] = -16 h[i] + (i & 3)
 };
 
-__device__ __forceinline__ int32_t pick16(const int32_t (&A)[4][4], int slot)
+template <int A>
+__device__ __forceinline__ int32_t pick_row(const int32_t (&M)[4][4], int v)
 {
-    int32_t r = A[0][0];
-#pragma unroll
-    for (int q = 1; q < 16; ++q) r = (slot == q) ? A[q >> 2][q & 3] : r;
-    return r;
+    switch (v) {
+        case 0: return M[A][0];
+        case 1: return M[A][1];
+        case 2: return M[A][2];
+        default: return M[A][3];
+    }
+}
+// M[u][v] for warp-uniform u, v (in-block indices of the accepted move)
+__device__ __forceinline__ int32_t pick_uniform(const int32_t (&M)[4][4], int u, int v)
+{
+    switch (u) {
+        case 0: return pick_row<0>(M, v);
+        case 1: return pick_row<1>(M, v);
+        case 2: return pick_row<2>(M, v);
+        default: return pick_row<3>(M, v);
+    }
 }
 __device__ __forceinline__ void st_vec4(int32_t *arr, int blk, int32_t a, int32_t b, int32_t c, int32_t d)
 {
@@ -536,14 +549,8 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     for (int c = 1; c <= iters; ++c) {
         long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0;
         if (timing) tA = clock64();
-        long long ten = 0;
-        if (tabu) {
-            if (!P.rng) {
-                ten = P.tenures[(size_t)b * iters + (c - 1)];
-            } else if (((c - 1) & (TENURE_CHUNK - 1)) == 0) {
-                fill_tenure_chunk(rng_state, P.ten_lo, P.ten_hi, P.force_seq_rng, sTen, sMisc, tid, T);
-            }
-        }
+        if (tabu && P.rng && ((c - 1) & (TENURE_CHUNK - 1)) == 0)
+            fill_tenure_chunk(rng_state, P.ten_lo, P.ten_hi, P.force_seq_rng, sTen, sMisc, tid, T);
 
         // ---------------- pass: update + select over this thread's units
         int32_t my_d = MAXV;
@@ -631,10 +638,12 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         const bool improved = cost < best_cost;
         if (improved) best_cost = cost;
         thr = Acc<int32_t>::clamp_thr(best_cost - cost);
-        if (tabu && P.rng) ten = sTen[(c - 1) & (TENURE_CHUNK - 1)];
         steps_done = c;
         R = r >> 2; S = s >> 2; ru = r & 3; su = s & 3;
-        const int pr = sP[r], ps = sP[s];
+        // only the publish threads and the owner of the winning pair need the two units
+        const bool is_winner = my_key == bkey;
+        int pr = 0, ps = 0;
+        if (tid < n || is_winner) { pr = sP[r]; ps = sP[s]; }
         if (timing) tC = clock64() + (pr & 0);
 
         // ---------------- publish: difference vectors of the move (old permutation), additive
@@ -698,9 +707,12 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         }
         if (timing) tD = clock64();
         // ---- the thread owning the winning pair: corners, h[r], h[s], tabu memory, trail
-        if (my_key == bkey) {
+        if (is_winner) {
             const int32_t Drs = ldD(r, s), Dsr = ldD(s, r);
             const int32_t Fpspr = ldF(ps, pr), Fprps = ldF(pr, ps);
+            // the tenure of this move (tabu.py:184-186): drawn on the device or provided by the caller
+            const long long ten = !tabu ? 0 : (P.rng ? (long long)sTen[(c - 1) & (TENURE_CHUNK - 1)]
+                                                     : (long long)P.tenures[(size_t)b * iters + (c - 1)]);
             const int32_t new_exp = (int32_t)(c + ten);
             int32_t mrs = 0, msr = 0;
             unsigned was = 0;
@@ -717,8 +729,9 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
 #pragma unroll
                 for (int k = 0; k < UR; ++k) {
                     if (k != my_which) continue;
-                    mrs = pick16(U[k], ru * 4 + su);
-                    msr = (I[k] != J[k]) ? pick16(L[k], su * 4 + ru) : pick16(U[k], su * 4 + ru);
+                    // ru, su are uniform: two uniform switches instead of two 15-deep select chains
+                    mrs = pick_uniform(U[k], ru, su);
+                    msr = (I[k] != J[k]) ? pick_uniform(L[k], su, ru) : pick_uniform(U[k], su, ru);
                     was = (tb[k] >> my_slot) & 1u;
                     if (tabu) {
                         tb[k] |= 1u << my_slot;
