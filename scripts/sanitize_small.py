@@ -1,21 +1,31 @@
 """Small runs of every kernel path for compute-sanitizer (memcheck / racecheck)."""
-import sys
+import os, sys
 sys.path.insert(0, ".")
 import numpy as np
 import paper_2307_11248_b200 as q
 from paper_2307_11248_b200 import shapes
-for name in ("rand12", "tai30a", "rand23"):
-    inst = shapes.by_name(name)
-    res = q.run_multistart(inst, q.SearchConfig(algorithm="tabu", n_starts=4, iterations=40, master_seed=1))
-    res2 = q.run_multistart(inst, q.SearchConfig(algorithm="2opt", n_starts=4, iterations=20, master_seed=1))
-    rec, trail = q.run_tabu(inst, 3, 30)
-    q.all_deltas(inst, rec.permutation)
-    print(name, res.best.cost, res2.best.cost, rec.cost)
-import os
-os.environ["QAPB_FORCE_GENERIC"] = "1"
 from paper_2307_11248_b200.backend import clear_cache
-clear_cache()
-for name in ("rand12", "tai30a"):
+
+def run(name, starts=3, iters=12):
     inst = shapes.by_name(name)
-    res = q.run_multistart(inst, q.SearchConfig(algorithm="tabu", n_starts=4, iterations=40, master_seed=1))
-    print("generic", name, res.best.cost)
+    res = q.run_multistart(inst, q.SearchConfig(algorithm="tabu", n_starts=starts, iterations=iters, master_seed=1))
+    res2 = q.run_multistart(inst, q.SearchConfig(algorithm="2opt", n_starts=starts, iterations=iters, master_seed=1))
+    rec, trail = q.run_tabu(inst, 3, iters)
+    q.all_deltas(inst, rec.permutation)
+    many = q.run_repetitions(inst, q.SearchConfig(algorithm="tabu", n_starts=2, iterations=iters, master_seed=1), 2)
+    info = q.backend.device_instance(inst.flow, inst.distance).info
+    print(name, res.best.cost, res2.best.cost, rec.cost, many[1].best.cost, "storage", info["storage"], "threads", info["threads"], "acc", info["acc_bits"])
+
+# hybrid plans: one register unit (+ staging), asymmetric, two register units (n = 112), two CTAs with
+# shared-memory units and diagonal blocks in shared memory (n = 132), one CTA (n = 200)
+for name in ("rand12", "tai30a", "rand23", "tai112a", "rand132", "tai200a"):
+    run(name)
+# generic kernel: int64 state (tai*b), forced int32, M in L2, masks in L2
+run("tai45b")
+os.environ["QAPB_FORCE_GENERIC"] = "1"
+clear_cache()
+run("tai30a")
+for st in ("1", "2"):
+    os.environ["QAPB_FORCE_STORAGE"] = st
+    clear_cache()
+    run("rand23")
