@@ -287,6 +287,8 @@ def run_ours(args) -> None:
             "achieved": achieved / 1e12, "peak": int_peak / 1e12, "unit": "Tint-op/s",
             "frac": achieved / int_peak, "traffic": dram_bytes,
             "ops_per_eval": ops_survey, "ops_per_eval_source": "SURVEY.md 8(d) incremental evaluator",
+            "frac_note": "algorithmic ops (SURVEY 8d model: the 2n-4 pairs touching r,s recomputed in O(n)) per launch / duration / peak; "
+                         "the placement matrix makes those pairs O(1), so fewer ops are executed -- see frac_executed_ops and DESIGN.md 4",
             "frac_executed_ops": evals_per_launch * ops_exec / (k_ms * 1e-3) / int_peak,
             "executed_ops_per_eval": ops_exec,
             "peak_source": "measured live: qapb_probe_int_peak (IMAD / IADD3 / mixed issue loops on all SMs)",
