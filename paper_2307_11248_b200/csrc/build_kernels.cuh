@@ -77,7 +77,22 @@ struct BuildParams {
     void *h;                         // [B,npad] out
 };
 
-enum { BT = 64, BK = 32 };
+enum { BK = 32 };
+
+// Output tile edge of qap_build_m_kernel: the one of {64, 52, 32} that wastes the least work on
+// npad (n = 100: 2 x 2 tiles of 52 cover 104 instead of 128 columns -- 1.08x instead of 1.64x the
+// useful multiply-adds).  Threads per CTA = (BT / 4)^2, rounded up to a warp multiple.
+__host__ __device__ inline int build_tile(int npad)
+{
+    const int cand[3] = {64, 52, 32};
+    int best = 64;
+    long long best_cost = -1;
+    for (int k = 0; k < 3; ++k) {
+        const long long tiles = (npad + cand[k] - 1) / cand[k], cost = tiles * cand[k];
+        if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = cand[k]; }
+    }
+    return best;
+}
 
 __device__ __forceinline__ void st_acc4(int32_t *dst, const int32_t (&v)[4])
 {
@@ -89,11 +104,13 @@ __device__ __forceinline__ void st_acc4(int64_t *dst, const int64_t (&v)[4])
     reinterpret_cast<longlong2 *>(dst)[1] = make_longlong2(v[2], v[3]);
 }
 
-template <typename acc_t>
+template <typename acc_t, int BT>
 __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
 {
     __shared__ __align__(16) int32_t sA[2][BK][BT];  // [term][k][i]
     __shared__ __align__(16) int32_t sB[2][BK][BT];  // [term][k][j]
+    constexpr int TW = BT / 4;                         // micro-tiles per tile edge
+    const int NT = blockDim.x;
     __shared__ int32_t sPk[BK];
     extern __shared__ __align__(16) unsigned char dyn[];
     int32_t *sPerm = reinterpret_cast<int32_t *>(dyn);  // [npad]
@@ -104,10 +121,11 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
     const int ti = tt / tiles, tj = tt % tiles;
     const int i0 = ti * BT, j0 = tj * BT;
     const int32_t *perm = P.perm32 + (size_t)b * npad;
-    for (int i = tid; i < npad; i += 256) sPerm[i] = perm[i];
+    for (int i = tid; i < npad; i += NT) sPerm[i] = perm[i];
     __syncthreads();
     const bool sym = P.symmetric != 0;
-    const int ty = tid >> 4, tx = tid & 15;  // micro-tile rows 4*ty.., cols 4*tx..
+    const int ty = tid / TW, tx = tid % TW;  // micro-tile rows 4*ty.., cols 4*tx..
+    const bool active = ty < TW;
     acc_t acc[4][4];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
@@ -119,7 +137,7 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
         // gathered at p_j); second term (asymmetric only): A2 = D0[k][i] (row of D), B2 = F0[p_k][p_j]
         if (tid < BK) sPk[tid] = (k0 + tid < n) ? sPerm[k0 + tid] : 0;
         __syncthreads();
-        for (int e = tid; e < BK * BT; e += 256) {
+        for (int e = tid; e < BK * BT; e += NT) {
             const int k = e / BT, x = e % BT;
             const int kk = k0 + k;
             const bool kin = kk < n;
@@ -135,7 +153,7 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
         }
         __syncthreads();
 #pragma unroll 8
-        for (int k = 0; k < BK; ++k) {
+        for (int k = 0; k < BK && active; ++k) {
             const int4 a = *reinterpret_cast<const int4 *>(&sA[0][k][4 * ty]);
             const int4 bq = *reinterpret_cast<const int4 *>(&sB[0][k][4 * tx]);
             const int32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {bq.x, bq.y, bq.z, bq.w};
@@ -161,7 +179,7 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int i = i0 + 4 * ty + u;
-        if (i >= npad) continue;
+        if (i >= npad || !active) continue;
         acc_t out[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
@@ -188,7 +206,7 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
         if (jb < npad) st_acc4(&Mb[(size_t)i * npad + jb], out);
     }
     if (ti == 0 && tj == 0)
-        for (int i = n + tid; i < npad; i += 256) hb[i] = 0;
+        for (int i = n + tid; i < npad; i += NT) hb[i] = 0;
 }
 
 // kernels.all_deltas (_kernels.pyx:58-70) from M and h: out[b][k] = M[i][j] + M[j][i] - h[i] - h[j]

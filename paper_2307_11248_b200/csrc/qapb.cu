@@ -588,10 +588,14 @@ static int launch_build(qapb_handle *h, const WsPlan &w, int batch, int rng, int
     BP.perm32 = SP.perm32;
     BP.M = (char *)h->ws + w.offInitM;
     BP.h = (char *)h->ws + w.offInitH;
-    const int tiles = (h->npad + BT - 1) / BT;
+    const int bt = build_tile(h->npad), tiles = (h->npad + bt - 1) / bt;
     const unsigned grid = (unsigned)(tiles * tiles) * (unsigned)batch;
-    if (h->acc_bits == 64) qap_build_m_kernel<int64_t><<<grid, 256, np * sizeof(int32_t), st>>>(BP);
-    else qap_build_m_kernel<int32_t><<<grid, 256, np * sizeof(int32_t), st>>>(BP);
+    const unsigned nt = (unsigned)(((bt / 4) * (bt / 4) + 31) / 32 * 32);
+    const size_t dyn = np * sizeof(int32_t);
+#define QAPB_BUILD(A, B) qap_build_m_kernel<A, B><<<grid, nt, dyn, st>>>(BP)
+    if (h->acc_bits == 64) { if (bt == 64) QAPB_BUILD(int64_t, 64); else if (bt == 52) QAPB_BUILD(int64_t, 52); else QAPB_BUILD(int64_t, 32); }
+    else { if (bt == 64) QAPB_BUILD(int32_t, 64); else if (bt == 52) QAPB_BUILD(int32_t, 52); else QAPB_BUILD(int32_t, 32); }
+#undef QAPB_BUILD
     CU(cudaGetLastError());
     return QAPB_OK;
 }
