@@ -36,6 +36,7 @@ static int fail(int code, const std::string &msg)
 struct qapb_handle {
     int n = 0, nb = 0, npad = 0, device = 0;
     int acc_bits = 32, symmetric = 0;
+    int sym_mode = 0;  // generic kernel: 0 two products per entry, 1 both symmetric, 2 D only, 3 F only
     int nunits = 0, noff = 0, threads = 0, upt = 0, storage = 0;
     int lb_class = 0;  // 0: <=384 threads, 2 CTAs/SM register budget; 1: <=512 threads
     int toff = 0, us = 0, exp_in_smem = 1;         // hybrid plan
@@ -349,7 +350,8 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
 
     const int nb = (n + 3) / 4, npad = nb * 4;
     std::vector<long long> F0((size_t)n * n), D0((size_t)n * n), fd(n), dd(n);
-    bool sym = true, fits16 = true;
+    bool sym = true, symF = true, symD = true, fits16 = true;
+    long long maxF0 = 0, maxD0 = 0;
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
             long long f = flow[(size_t)i * n + j], d = dist[(size_t)i * n + j];
@@ -359,12 +361,18 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
             if (std::llabs(f) > 32767 || std::llabs(d) > 32767) fits16 = false;
             F0[(size_t)i * n + j] = f;
             D0[(size_t)i * n + j] = d;
-            if (i != j && (flow[(size_t)i * n + j] != flow[(size_t)j * n + i] || dist[(size_t)i * n + j] != dist[(size_t)j * n + i]))
-                sym = false;
+            maxF0 = std::max(maxF0, std::llabs(f));
+            maxD0 = std::max(maxD0, std::llabs(d));
+            if (i != j && flow[(size_t)i * n + j] != flow[(size_t)j * n + i]) symF = false;
+            if (i != j && dist[(size_t)i * n + j] != dist[(size_t)j * n + i]) symD = false;
         }
+    sym = symF && symD;
 
     qapb_handle *h = new qapb_handle();
     h->n = n; h->nb = nb; h->npad = npad; h->device = device; h->symmetric = sym ? 1 : 0;
+    // one symmetric matrix is enough for a single-product rank-2 update: D = D^T gives a == c, so
+    // a[i] b[j] + c[i] e[j] = a[i] (b[j] + e[j]); F = F^T gives b == e.  The summed vector must fit int32.
+    h->sym_mode = sym ? 1 : (symD && maxF0 < (1LL << 29)) ? 2 : (symF && maxD0 < (1LL << 29)) ? 3 : 0;
     h->fits_i16 = fits16 ? 1 : 0;
 
     // accumulator width: |delta| <= 4 * bound must stay below 2^31-1 for the int32 state
@@ -536,7 +544,7 @@ static void base_params(const qapb_handle *h, SearchParams &P)
 {
     memset(&P, 0, sizeof(P));
     P.n = h->n; P.nb = h->nb; P.npad = h->npad; P.nunits = h->nunits; P.noff = h->noff; P.upt = h->upt;
-    P.symmetric = h->symmetric;
+    P.symmetric = h->storage == 3 ? h->symmetric : h->sym_mode;
     P.force_seq_rng = h->force_seq_rng;
     P.one = 1;
     P.sixteen = 16;

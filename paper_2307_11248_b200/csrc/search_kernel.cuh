@@ -81,7 +81,7 @@ struct SearchParams {
     int mode;        // MODE_*
     int rng;         // 1: derive start permutation + tenures on the device (multistart)
     int iterations;
-    int symmetric;
+    int symmetric;   // hybrid: 1 if both matrices are symmetric; generic: 0 none, 1 both, 2 distance only, 3 flow only
     int force_seq_rng;  // test hook: take the sequential (rejection-exact) RNG path
     int one, sixteen;   // runtime constants 1 and 16: multiplying by them keeps adds/shifts on the FMA (IMAD) pipe
     const int32_t *F, *FT, *D, *DT;  // [npad*npad], zero diagonal, zero padded
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
     const int32_t *__restrict__ FT = P.FT;
     const int32_t *__restrict__ D = P.D;
     const int32_t *__restrict__ DT = P.DT;
-    const bool sym = P.symmetric != 0;
+    const bool sym = P.symmetric != 0;  // single-product rank-2 update: at least one symmetric matrix
     const acc_t MAXV = Acc<acc_t>::maxv();
     const int32_t MAXE = 0x7fffffff;
 
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                     ld_row(M, k * 8 + 4 + u, T, tid, Lr);
                     if (c > 1) {
                         const int32_t aIu = sA[4 * I + u], bIu = sB[4 * I + u];
-                        if (sym) {  // a pre-doubled: a == c, b == e
+                        if (sym) {  // one product: the published a, b are pre-combined (see the prep phase)
 #pragma unroll
                             for (int v = 0; v < 4; ++v) {
                                 Ur[v] -= (acc_t)aIu * (acc_t)bJ[v];
@@ -597,8 +597,11 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                     *pis = mir + (acc_t)a * (fs_pr - (acc_t)Fprps) - (acc_t)cc * (acc_t)Fpspr;
                     sH[i] -= (acc_t)a * (acc_t)bb + (acc_t)cc * (acc_t)e;
                 }
-                sA[i] = sym ? 2 * a : a;
-                sC[i] = cc; sB[i] = bb; sE[i] = e;
+                // single-product forms: both symmetric a == c, b == e -> (2a) b; D = D^T only a == c -> a (b + e);
+                // F = F^T only b == e -> (a + c) b
+                sA[i] = P.symmetric == 1 ? 2 * a : P.symmetric == 3 ? a + cc : a;
+                sB[i] = P.symmetric == 2 ? bb + e : bb;
+                sC[i] = cc; sE[i] = e;
             }
         }
         __syncthreads();  // ---------------------------------------------- sync #2

@@ -420,3 +420,42 @@ def test_unsupported_sizes_and_values(q):
         DeviceInstance(f, np.ones((4, 4), np.int64))
     with pytest.raises(q.DomainError):
         DeviceInstance(np.zeros((1, 1), np.int64), np.zeros((1, 1), np.int64))
+
+
+@pytest.mark.parametrize("which,scale", [("dist", 1), ("flow", 1), ("dist", 40000), ("flow", 40000)])
+def test_generic_kernel_one_symmetric_matrix(q, orc, monkeypatch, which, scale):
+    """One symmetric matrix lets the generic kernel's rank-2 update use a single product per entry
+    (a == c or b == e); int32 state (scale 1) and int64 state (large entries)."""
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    monkeypatch.setenv("QAPB_FORCE_GENERIC", "1")
+    rs = np.random.default_rng(31 + scale)
+    n, iters = 27, 40
+    f = rs.integers(0, 60, (n, n)).astype(np.int64)
+    d = rs.integers(0, 60, (n, n)).astype(np.int64)
+    if which == "dist":
+        d = d + d.T
+        f = f * scale
+    else:
+        f = f + f.T
+        d = d * scale
+    np.fill_diagonal(f, rs.integers(0, 9, n))  # non-zero diagonals too
+    di = DeviceInstance(f, d)
+    try:
+        assert di.info["storage"] == 0 and di.info["symmetric"] == 0
+        assert di.info["acc_bits"] == (32 if scale == 1 else 64)
+        lo, hi = orc.tenure_bounds(n)
+        rng = orc.Rng(orc.derive_seed(9, scale))
+        perm = rng.permutation(n)
+        ten = rng.tenures(lo, hi, iters)
+        best, bc, cur, cc, cz, stop, steps, tr, _ = di.tabu(perm, iters, ten)
+        want = orc.tabu_run(f, d, perm, iters, ten)
+        assert np.array_equal(best[0], want[0]) and bc[0] == want[1] and np.array_equal(cur[0], want[2]) and cc[0] == want[3]
+        assert np.array_equal(cz[0], want[4]) and steps[0] == want[6]
+        for a in range(4):
+            assert np.array_equal(tr[a][0, : want[6]], want[7][a])
+        b2 = di.two_opt(perm, iters)
+        for g, w in zip([x[0] for x in b2], orc.two_opt_run(f, d, perm, iters)):
+            assert np.array_equal(g, w)
+    finally:
+        di.close()
