@@ -545,7 +545,13 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     int R = -1, S = -1, ru = 0, su = 0;  // previous move (block and in-block indices)
 
     long long tacc[6] = {0, 0, 0, 0, 0, 0};
+    // phase-cycle counters of CTA 0 (scripts/phase_time.py): compiled in only with -DQAPB_PHASE_TIMING,
+    // the clock reads and their predicates cost ~3 % of the loop otherwise
+#ifdef QAPB_PHASE_TIMING
     const bool timing = P.dbg != nullptr && b == 0 && (tid == 0 || tid == 128 || tid == Toff);
+#else
+    constexpr bool timing = false;
+#endif
     for (int c = 1; c <= iters; ++c) {
         long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0;
         if (timing) tA = clock64();
