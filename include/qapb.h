@@ -149,6 +149,15 @@ int qapb_multistart_seeds_host(qapb_handle *h, int algo, const uint64_t *seeds, 
                                int iterations, int64_t ten_low, int64_t ten_high,
                                int64_t *per_start_costs, int64_t *best_perms);
 
+/* Launch-configuration tuning (the GPU counterpart of the (N, t, b) space of tuner.py:28-78: here a
+ * configuration is how one search is laid out on an SM).  `qapb_plan_candidates` lists the plans of
+ * the register/shared-memory kernel that fit this instance as rows {register units per thread,
+ * threads carrying off-diagonal units, shared-memory units per thread, diagonal blocks in shared
+ * memory (0/1)}; `qapb_set_plan` re-plans the handle with one of them (results are identical under
+ * every plan; only the speed differs).  Instances served by the generic kernel have no candidates. */
+int qapb_plan_candidates(qapb_handle *h, int32_t *plans /* [cap][4] */, int cap, int *count);
+int qapb_set_plan(qapb_handle *h, int reg_units, int unit_threads, int smem_units, int diag_in_smem);
+
 /* Time of the most recent search-kernel launch sequence on this handle, in
  * milliseconds between CUDA events recorded on the launching stream
  * (valid after the stream has been synchronised).  Used by bench.py for the

@@ -84,6 +84,8 @@ SIGNATURES = {
     "qapb_tabu_host": (c_int, [c_void_p, _P, c_int, c_int, _P] + [_P] * 11),
     "qapb_multistart_host": (c_int, [c_void_p, c_int, c_uint64, c_uint64, c_int, c_int, c_int64, c_int64, _P, _P, _P]),
     "qapb_multistart_seeds_host": (c_int, [c_void_p, c_int, _P, c_int, c_int, c_int64, c_int64, _P, _P]),
+    "qapb_plan_candidates": (c_int, [c_void_p, _P, c_int, POINTER(c_int)]),
+    "qapb_set_plan": (c_int, [c_void_p, c_int, c_int, c_int, c_int]),
     "qapb_last_kernel_ms": (c_int, [c_void_p, POINTER(c_float)]),
     "qapb_probe_int_peak": (c_int, [c_int, c_int, POINTER(c_double)]),
 }

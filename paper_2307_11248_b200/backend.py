@@ -150,6 +150,25 @@ class DeviceInstance:
             self._h, algo, master_seed & 0xFFFFFFFFFFFFFFFF, first_index, count, iterations,
             ten_low, ten_high, costs_ptr, key_ptr, perm_ptr, stream or None))
 
+    def _refresh_info(self) -> None:
+        info = _lib.Info()
+        _lib.check(_lib.lib().qapb_get_info(self._h, ctypes.byref(info)))
+        self.info = {name: int(getattr(info, name)) for name, _ in _lib.Info._fields_}
+
+    def plan_candidates(self) -> list[tuple[int, int, int, int]]:
+        """Launch configurations that fit this instance: (register units per thread, threads carrying
+        off-diagonal units, shared-memory units per thread, diagonal blocks in shared memory); the
+        library's default choice first.  Empty for instances served by the generic kernel."""
+        buf = np.zeros((16, 4), np.int32)
+        count = ctypes.c_int(0)
+        _lib.check(_lib.lib().qapb_plan_candidates(self._h, _addr(buf), 16, ctypes.byref(count)))
+        return [tuple(int(x) for x in row) for row in buf[: min(count.value, 16)]]
+
+    def set_plan(self, plan: tuple[int, int, int, int]) -> None:
+        """Re-plan with one of `plan_candidates()`; results do not depend on the plan."""
+        _lib.check(_lib.lib().qapb_set_plan(self._h, *[int(x) for x in plan]))
+        self._refresh_info()
+
     def last_kernel_ms(self) -> float:
         ms = ctypes.c_float(0)
         _lib.check(_lib.lib().qapb_last_kernel_ms(self._h, ctypes.byref(ms)))

@@ -10,6 +10,7 @@
 #include "search_hybrid.cuh"
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -20,6 +21,7 @@
 
 using namespace qapb;
 
+int g_attr_smem(int device);  // opt-in shared memory per block of a device seen by qapb_create
 static thread_local std::string g_err;
 static int fail(int code, const std::string &msg)
 {
@@ -200,6 +202,30 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
     return true;
 }
 
+// Candidate hybrid plans of an instance: {ur, toff, us, dsm} rows, the default choice first.
+static std::vector<std::array<int, 4>> hybrid_candidates(const qapb_handle *h)
+{
+    std::vector<std::array<int, 4>> out;
+    const int nb = h->nb, noff = h->noff;
+    auto add = [&](int ur, int toff, int us, int dsm) {
+        if (toff < 32 && !(toff == 0 && noff == 0)) return;
+        for (const auto &c : out)
+            if (c[0] == ur && c[1] == toff && c[2] == us && c[3] == dsm) return;
+        out.push_back({ur, toff, us, dsm});
+    };
+    if (nb > 32) {
+        for (int t : {256, 384, 512}) add(2, t, std::max(1, (noff - 2 * t + t - 1) / t), 1);
+        const int toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
+        add(2, toff, std::max(0, (noff - 2 * toff + toff - 1) / toff), 0);
+    } else {
+        add(1, (noff + 31) / 32 * 32, 0, 0);
+        add(2, ((noff + 1) / 2 + 31) / 32 * 32, 0, 0);
+    }
+    return out;
+}
+
+static unsigned device_smem_cap(int device) { return (unsigned)g_attr_smem(device); }
+
 extern "C" int qapb_version(void) { return 1; }
 extern "C" const char *qapb_last_error(void) { return g_err.c_str(); }
 extern "C" int qapb_device_count(int *count)
@@ -270,6 +296,7 @@ size_t g_stage_bytes = 0;
 struct DevAttr { int valid = 0, sm_count = 0, smem_optin = 0; };
 DevAttr g_attr[64];
 }  // namespace
+int g_attr_smem(int device) { return g_attr[device & 63].smem_optin; }
 
 static int ensure_ws(qapb_handle *h, size_t bytes)
 {
@@ -804,6 +831,39 @@ extern "C" int qapb_multistart_seeds(qapb_handle *h, int algo, const uint64_t *s
     P.best = best_perms; P.best_cost = per_start_costs;
     P.cur = (int64_t *)h->ws; P.cur_cost = (int64_t *)((char *)h->ws + perm_bytes);
     return launch_search(h, P, count, head, (cudaStream_t)stream);
+}
+
+extern "C" int qapb_plan_candidates(qapb_handle *h, int32_t *plans, int cap, int *count)
+{
+    if (!h || !count || (cap > 0 && !plans)) return fail(QAPB_ERR_INVALID, "NULL argument");
+    *count = 0;
+    if (h->storage != 3) return QAPB_OK;  // generic kernel: one configuration
+    qapb_handle probe = *h;               // try each candidate on a copy (no device state is touched)
+    for (const auto &c : hybrid_candidates(h)) {
+        const unsigned target = (c[3] && c[1] <= 256) ? 113u * 1024u : 0u;
+        if (!try_hybrid_plan(&probe, device_smem_cap(h->device), c[0], c[1], c[2], c[3], target)) continue;
+        if (*count < cap)
+            for (int q = 0; q < 4; ++q) plans[*count * 4 + q] = c[q];
+        ++*count;
+    }
+    return QAPB_OK;
+}
+
+extern "C" int qapb_set_plan(qapb_handle *h, int reg_units, int unit_threads, int smem_units, int diag_in_smem)
+{
+    if (!h) return fail(QAPB_ERR_INVALID, "NULL handle");
+    if (h->storage != 3) return fail(QAPB_ERR_UNSUPPORTED, "this instance runs in the generic kernel: no alternative plans");
+    CU(cudaSetDevice(h->device));
+    if (h->have_timing) CU(cudaEventSynchronize(h->ev1));  // no launch of the old plan in flight
+    qapb_handle probe = *h;
+    const unsigned target = (diag_in_smem && unit_threads <= 256) ? 113u * 1024u : 0u;
+    if ((reg_units != 1 && reg_units != 2) || unit_threads < 0 || unit_threads % 32 != 0 || smem_units < 0 ||
+        !try_hybrid_plan(&probe, device_smem_cap(h->device), reg_units, unit_threads, smem_units, diag_in_smem ? 1 : 0, target))
+        return fail(QAPB_ERR_INVALID, "plan {" + std::to_string(reg_units) + ", " + std::to_string(unit_threads) + ", " +
+                                          std::to_string(smem_units) + ", " + std::to_string(diag_in_smem) + "} does not fit this instance");
+    probe.ctas_per_sm = 0;  // re-queried by qapb_get_info
+    *h = probe;
+    return QAPB_OK;
 }
 
 extern "C" int qapb_last_kernel_ms(qapb_handle *h, float *ms)

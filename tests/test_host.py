@@ -268,3 +268,18 @@ def test_run_multistart_many_groups_and_splits():
         assert r.best.permutation[0] == int(seeds[k] % np.uint64(1000))
         assert r.best.seed == q.derive_seed(cfg.master_seed, k)
         assert r.config_digest == q.config_digest(inst, cfg)
+
+
+def test_thread_config_space():
+    """tuner.py:28-78 known answers (from the reference itself): 1434 configurations in all, six for
+    N = 4096, and the violation messages of an invalid triple."""
+    cfgs = q.enumerate_configs()
+    assert len(cfgs) == 1434 and cfgs[0] == q.ThreadConfig(1024, 32, 32) and cfgs[-1] == q.ThreadConfig(12288, 1024, 12)
+    assert [c.threads_per_block for c in q.enumerate_configs(4096)] == [32, 64, 128, 256, 512, 1024]
+    assert q.enumerate_configs(1000) == []
+    ok, why = q.validate_config(q.ThreadConfig(1000, 33, 2))
+    assert not ok and why == ["n_starts 1000 outside [1024, 12288]", "n_starts 1000 not a multiple of warp size 32",
+                              "threads_per_block 33 not a multiple of warp size 32",
+                              "n_starts 1000 not divisible by threads_per_block 33"]
+    assert q.validate_config(q.ThreadConfig(2048, 64, 32)) == (True, [])
+    assert q.validate_config(q.ThreadConfig(2048, 64, 31))[1] == ["blocks 31 != n_starts / threads_per_block (32)"]

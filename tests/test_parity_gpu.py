@@ -459,3 +459,42 @@ def test_generic_kernel_one_symmetric_matrix(q, orc, monkeypatch, which, scale):
             assert np.array_equal(g, w)
     finally:
         di.close()
+
+
+@pytest.mark.parametrize("shape,iters", [("rand30", 40), ("tai112a", 16), ("rand132", 12), ("tai200a", 8)])
+def test_every_launch_plan_gives_identical_results(q, orc, shape, iters):
+    """tuner: results do not depend on the launch plan (one / two register units, shared-memory units,
+    diagonal blocks in registers or shared memory, one or two searches per SM)."""
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    inst = shapes.by_name(shape)
+    lo, hi = orc.tenure_bounds(inst.n)
+    want = orc.multistart(inst.flow, inst.distance, "tabu", 13, 5, iters, threads=orc.max_threads())
+    di = DeviceInstance(inst.flow, inst.distance)
+    try:
+        plans = di.plan_candidates()
+        assert len(plans) >= 2 and di.info["storage"] == 3
+        for plan in plans:
+            di.set_plan(plan)
+            costs, bc, bi, bp = di.multistart("tabu", 13, 0, 5, iters, lo, hi)
+            assert np.array_equal(costs, want[0]) and (bc, bi) == (want[1], want[2]) and np.array_equal(bp, want[3]), plan
+        with pytest.raises(q.DomainError):
+            di.set_plan((1, 32, 0, 0) if inst.n > 64 else (2, 4096, 0, 0))
+    finally:
+        di.close()
+    # instances of the generic kernel have a single configuration
+    big = shapes.by_name("tai45b")
+    assert DeviceInstance(big.flow, big.distance).plan_candidates() == []
+
+
+def test_autotune_installs_the_fastest_plan(q):
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.backend import device_instance
+
+    inst = shapes.by_name("tai64c")
+    timings = q.autotune(inst, iterations=40)
+    assert timings and all(a.evals_per_second >= b.evals_per_second for a, b in zip(timings, timings[1:]))
+    di = device_instance(inst.flow, inst.distance)
+    assert di.info["threads"] == timings[0].threads
+    assert q.autotune(shapes.by_name("tai45b")) == []
