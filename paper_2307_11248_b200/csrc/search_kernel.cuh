@@ -454,18 +454,18 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                     ld_row(M, k * 8 + 4 + u, T, tid, Lr);
                     if (c > 1) {
                         const int32_t aIu = sA[4 * I + u], bIu = sB[4 * I + u];
-                        if (sym) {  // one product: the published a, b are pre-combined (see the prep phase)
+                        if (sym) {  // one product: the published a, b are pre-combined (and a, c negated; see the prep phase)
 #pragma unroll
                             for (int v = 0; v < 4; ++v) {
-                                Ur[v] -= (acc_t)aIu * (acc_t)bJ[v];
-                                Lr[v] -= (acc_t)aJ[v] * (acc_t)bIu;
+                                Ur[v] += (acc_t)aIu * (acc_t)bJ[v];
+                                Lr[v] += (acc_t)aJ[v] * (acc_t)bIu;
                             }
                         } else {
                             const int32_t cIu = sC[4 * I + u], eIu = sE[4 * I + u];
 #pragma unroll
                             for (int v = 0; v < 4; ++v) {
-                                Ur[v] -= (acc_t)aIu * (acc_t)bJ[v] + (acc_t)cIu * (acc_t)eJ[v];
-                                Lr[v] -= (acc_t)aJ[v] * (acc_t)bIu + (acc_t)cJ[v] * (acc_t)eIu;
+                                Ur[v] += (acc_t)aIu * (acc_t)bJ[v] + (acc_t)cIu * (acc_t)eJ[v];
+                                Lr[v] += (acc_t)aJ[v] * (acc_t)bIu + (acc_t)cJ[v] * (acc_t)eIu;
                             }
                         }
                         st_row(M, k * 8 + u, T, tid, Ur);
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
 #pragma unroll
                         for (int v = 0; v < 4; ++v)
                             if (u != v)
-                                U[u][v] -= sym ? (acc_t)aI[u] * (acc_t)bI[v]
+                                U[u][v] += sym ? (acc_t)aI[u] * (acc_t)bI[v]
                                                : (acc_t)aI[u] * (acc_t)bI[v] + (acc_t)cI[u] * (acc_t)eI[v];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) st_row(M, k * 8 + u, T, tid, U[u]);
@@ -599,9 +599,11 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                 }
                 // single-product forms: both symmetric a == c, b == e -> (2a) b; D = D^T only a == c -> a (b + e);
                 // F = F^T only b == e -> (a + c) b
-                sA[i] = P.symmetric == 1 ? 2 * a : P.symmetric == 3 ? a + cc : a;
+                // a and c are stored NEGATED, so the update is a multiply-add (one IMAD.WIDE per product with
+                // int64 state instead of a product and a 64-bit subtraction)
+                sA[i] = -(P.symmetric == 1 ? 2 * a : P.symmetric == 3 ? a + cc : a);
                 sB[i] = P.symmetric == 2 ? bb + e : bb;
-                sC[i] = cc; sE[i] = e;
+                sC[i] = -cc; sE[i] = e;
             }
         }
         __syncthreads();  // ---------------------------------------------- sync #2
