@@ -1,4 +1,8 @@
-"""Per-phase cycle counters of CTA 0 of the hybrid search kernel (development aid)."""
+"""Per-phase cycle counters of CTA 0 of the hybrid search kernel (development aid).
+
+Needs a library built with the counters compiled in:
+    NVCC_EXTRA=-DQAPB_PHASE_TIMING QAPB_FORCE_BUILD=1 python -c "import __graft_entry__ as g; g.build()"
+(the production build leaves them out: they cost ~6 % of the search loop)."""
 import ctypes, sys
 sys.path.insert(0, ".")
 import numpy as np
