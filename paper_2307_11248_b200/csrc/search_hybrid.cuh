@@ -74,26 +74,6 @@ struct Vecs {
     int32_t *HI, *HJ;  // packed-key forms of h: HI[i] = -16 h[i] + 4 (i & 3), HJ[i] = -16 h[i] + (i & 3)
 };
 
-template <int A>
-__device__ __forceinline__ int32_t pick_row(const int32_t (&M)[4][4], int v)
-{
-    switch (v) {
-        case 0: return M[A][0];
-        case 1: return M[A][1];
-        case 2: return M[A][2];
-        default: return M[A][3];
-    }
-}
-// M[u][v] for warp-uniform u, v (in-block indices of the accepted move)
-__device__ __forceinline__ int32_t pick_uniform(const int32_t (&M)[4][4], int u, int v)
-{
-    switch (u) {
-        case 0: return pick_row<0>(M, v);
-        case 1: return pick_row<1>(M, v);
-        case 2: return pick_row<2>(M, v);
-        default: return pick_row<3>(M, v);
-    }
-}
 __device__ __forceinline__ void st_vec4(int32_t *arr, int blk, int32_t a, int32_t b, int32_t c, int32_t d)
 {
     reinterpret_cast<int4 *>(arr)[blk] = make_int4(a, b, c, d);
@@ -357,15 +337,26 @@ __device__ __forceinline__ void diag_select(const int32_t (&U)[4][4], unsigned t
 // ---- tabu bits of a unit: clear the ones whose expiry has been reached ------------------------
 __device__ __forceinline__ void expire_bits(unsigned &tb, int32_t &mexp, int c, const int32_t *xp16)
 {
-    unsigned bits = tb;
+    // one 128-bit load per block row that has a bit set (a loop over single bits serialises one
+    // load latency per bit -- it was the straggler of the publish phase)
     int32_t nm = 0x7fffffff;
-    while (bits) {
-        const int q = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const int32_t e = xp16[q];
-        if (e <= c) tb &= ~(1u << q);
-        else if (e != 0x7fffffff) nm = min(nm, e);
+    unsigned keep = tb;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        if ((tb >> (4 * u)) & 15u) {
+            const int4 e4 = reinterpret_cast<const int4 *>(xp16)[u];
+            const int32_t e[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const unsigned bit = 1u << (4 * u + v);
+                if (tb & bit) {
+                    if (e[v] <= c) keep &= ~bit;
+                    else if (e[v] != 0x7fffffff) nm = min(nm, e[v]);
+                }
+            }
+        }
     }
+    tb = keep;
     mexp = nm;
 }
 
@@ -652,6 +643,33 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         if (tid < n || is_winner) { pr = sP[r]; ps = sP[s]; }
         if (timing) tC = clock64() + (pr & 0);
 
+        // ---- owners of columns r and s publish them first (colR[r] = colS[s] = 0 by the diagonal lanes):
+        // the owner of the winning pair then reads its corner values M[r][s] = colS[r], M[s][r] = colR[s]
+        // back from shared memory instead of selecting registers by a run-time index
+#pragma unroll
+        for (int k = 0; k < UR; ++k) {
+            if (!own[k]) continue;
+            const int Ik = I[k], Jk = J[k];
+            if (Ik != Jk) {
+                // uniform switch on r & 3 / s & 3 outside, per-thread predicated 128-bit stores inside
+                QAPB_SWITCH4(ru, {
+                    if (Jk == R) st_vec4(V.ColR, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]);
+                    if (Ik == R) st_vec4(V.ColR, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]);
+                })
+                QAPB_SWITCH4(su, {
+                    if (Jk == S) st_vec4(V.ColS, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]);
+                    if (Ik == S) st_vec4(V.ColS, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]);
+                })
+            } else {
+                if (Ik == R) {
+                    QAPB_SWITCH4(ru, { st_vec4(V.ColR, Ik, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
+                }
+                if (Ik == S) {
+                    QAPB_SWITCH4(su, { st_vec4(V.ColS, Ik, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
+                }
+            }
+        }
+
         // ---------------- publish: difference vectors of the move (old permutation), additive
         // terms, h'[i] -- one location per thread
         if (tid < n) {
@@ -735,9 +753,8 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
 #pragma unroll
                 for (int k = 0; k < UR; ++k) {
                     if (k != my_which) continue;
-                    // ru, su are uniform: two uniform switches instead of two 15-deep select chains
-                    mrs = pick_uniform(U[k], ru, su);
-                    msr = (I[k] != J[k]) ? pick_uniform(L[k], su, ru) : pick_uniform(U[k], su, ru);
+                    mrs = V.ColS[r];  // this thread dumped both columns above: M[r][s], M[s][r]
+                    msr = V.ColR[s];
                     was = (tb[k] >> my_slot) & 1u;
                     if (tabu) {
                         tb[k] |= 1u << my_slot;
@@ -779,32 +796,11 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             }
         }
         if (timing) tE = clock64();
-        // ---- owners of columns r and s publish them (colR[r] = colS[s] = 0 by the diagonal lanes),
-        // and tabu bits that expire at the next iteration are cleared here, off the critical path
+        // ---- tabu bits that expire at the next iteration are cleared here; shared-memory units and
+        // shared-memory diagonal blocks publish their parts of columns r and s
 #pragma unroll
-        for (int k = 0; k < UR; ++k) {
-            if (!own[k]) continue;
-            const int Ik = I[k], Jk = J[k];
-            if (Ik != Jk) {
-                // uniform switch on r & 3 / s & 3 outside, per-thread predicated 128-bit stores inside
-                QAPB_SWITCH4(ru, {
-                    if (Jk == R) st_vec4(V.ColR, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]);
-                    if (Ik == R) st_vec4(V.ColR, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]);
-                })
-                QAPB_SWITCH4(su, {
-                    if (Jk == S) st_vec4(V.ColS, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]);
-                    if (Ik == S) st_vec4(V.ColS, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]);
-                })
-            } else {
-                if (Ik == R) {
-                    QAPB_SWITCH4(ru, { st_vec4(V.ColR, Ik, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
-                }
-                if (Ik == S) {
-                    QAPB_SWITCH4(su, { st_vec4(V.ColS, Ik, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
-                }
-            }
-            if (c + 1 >= mexp[k]) expire_bits(tb[k], mexp[k], c + 1, xp + uidv[k] * 16);
-        }
+        for (int k = 0; k < UR; ++k)
+            if (own[k] && c + 1 >= mexp[k]) expire_bits(tb[k], mexp[k], c + 1, xp + uidv[k] * 16);
         if (SMEMU && offt) {
 #pragma unroll 1
             for (int k2 = 0; k2 < US; ++k2) {
