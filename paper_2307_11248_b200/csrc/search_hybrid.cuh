@@ -732,8 +732,15 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         if (timing) tD = clock64();
         // ---- the thread owning the winning pair: corners, h[r], h[s], tabu memory, trail
         if (is_winner) {
-            const int32_t Drs = ldD(r, s), Dsr = ldD(s, r);
-            const int32_t Fpspr = ldF(ps, pr), Fprps = ldF(pr, ps);
+            // corner terms (D[r][s] - D[s][r]) F[ps][pr] and (D[s][r] - D[r][s]) F[pr][ps]: zero when both
+            // matrices are symmetric, so that case loads nothing here
+            int32_t kr = 0, ks = 0;
+            if (!SYM) {
+                const int32_t Drs = ldD(r, s), Dsr = ldD(s, r);
+                const int32_t Fpspr = ldF(ps, pr), Fprps = ldF(pr, ps);
+                kr = (Drs - Dsr) * Fpspr;
+                ks = (Dsr - Drs) * Fprps;
+            }
             // the tenure of this move (tabu.py:184-186): drawn on the device or provided by the caller
             const long long ten = !tabu ? 0 : (P.rng ? (long long)sTen[(c - 1) & (TENURE_CHUNK - 1)]
                                                      : (long long)P.tenures[(size_t)b * iters + (c - 1)]);
@@ -775,9 +782,9 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 }
             }
             const int32_t hr = V.H[r], hs = V.H[s];
-            V.TS[r] = hr + (Drs - Dsr) * Fpspr;  // M'[r][s]
-            V.TR[s] = hs + (Dsr - Drs) * Fprps;  // M'[s][r]
-            const int32_t hrn = mrs + (Dsr - Drs) * Fprps, hsn = msr + (Drs - Dsr) * Fpspr;
+            V.TS[r] = hr + kr;  // M'[r][s]
+            V.TR[s] = hs + ks;  // M'[s][r]
+            const int32_t hrn = mrs + ks, hsn = msr + kr;
             V.H[r] = hrn;
             V.H[s] = hsn;
             if (PACKED) {
