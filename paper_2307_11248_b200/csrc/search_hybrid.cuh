@@ -651,15 +651,22 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             if (!own[k]) continue;
             const int Ik = I[k], Jk = J[k];
             if (Ik != Jk) {
-                // uniform switch on r & 3 / s & 3 outside, per-thread predicated 128-bit stores inside
-                QAPB_SWITCH4(ru, {
-                    if (Jk == R) st_vec4(V.ColR, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]);
-                    if (Ik == R) st_vec4(V.ColR, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]);
-                })
-                QAPB_SWITCH4(su, {
-                    if (Jk == S) st_vec4(V.ColS, Ik, U[k][0][q], U[k][1][q], U[k][2][q], U[k][3][q]);
-                    if (Ik == S) st_vec4(V.ColS, Jk, L[k][0][q], L[k][1][q], L[k][2][q], L[k][3][q]);
-                })
+                // ONE uniform 16-way switch on (r & 3, s & 3) (a jump table: one indirect branch on the serial
+                // path instead of two two-level trees), per-thread predicated 128-bit stores inside
+#define QAPB_DUMP(a, b)                                                                                    \
+    case (a) * 4 + (b):                                                                                    \
+        if (Jk == R) st_vec4(V.ColR, Ik, U[k][0][a], U[k][1][a], U[k][2][a], U[k][3][a]);                  \
+        if (Ik == R) st_vec4(V.ColR, Jk, L[k][0][a], L[k][1][a], L[k][2][a], L[k][3][a]);                  \
+        if (Jk == S) st_vec4(V.ColS, Ik, U[k][0][b], U[k][1][b], U[k][2][b], U[k][3][b]);                  \
+        if (Ik == S) st_vec4(V.ColS, Jk, L[k][0][b], L[k][1][b], L[k][2][b], L[k][3][b]);                  \
+        break;
+                switch (ru * 4 + su) {
+                    QAPB_DUMP(0, 0) QAPB_DUMP(0, 1) QAPB_DUMP(0, 2) QAPB_DUMP(0, 3)
+                    QAPB_DUMP(1, 0) QAPB_DUMP(1, 1) QAPB_DUMP(1, 2) QAPB_DUMP(1, 3)
+                    QAPB_DUMP(2, 0) QAPB_DUMP(2, 1) QAPB_DUMP(2, 2) QAPB_DUMP(2, 3)
+                    QAPB_DUMP(3, 0) QAPB_DUMP(3, 1) QAPB_DUMP(3, 2) QAPB_DUMP(3, 3)
+                }
+#undef QAPB_DUMP
             } else {
                 if (Ik == R) {
                     QAPB_SWITCH4(ru, { st_vec4(V.ColR, Ik, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
