@@ -386,6 +386,7 @@ def run_ours(args) -> None:
             "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "time_to_gap": gap, "full_evaluator": full_eval, "shapes": shapes_tbl, "result_check": ok,
         }))
     if world > 1:
+        dist.barrier()  # rank 0 finishes its report (roofline probes, shapes table) before the group goes away
         dist.destroy_process_group()
 
 
