@@ -7,13 +7,15 @@
 //   * a further US units per thread in SHARED MEMORY in a spill layout (row w of slot k of
 //     thread t at ((k*8+w)*Toff + t)*16 bytes: every access is a conflict-free 128-bit
 //     LDS/STS) that are streamed through registers once per iteration.
-// The last DW warps own the nb diagonal 4x4 blocks (registers).  The tabu triangle is a
-// 16-bit mask per unit (pairs that are tabu now); expiry iterations live in an array that
-// is only touched when a pair is set or expires (shared memory when it fits, else L2).
-// The split is chosen per instance on the host (qapb.cu, plan_hybrid): n = 100 runs 3
-// searches per SM (160 units in registers + 140 in shared memory per search), n = 256 runs
-// one search per SM with 896 units in registers and 1120 in 140 KB of shared memory --
-// neither memory alone can hold the 256 KB of state of an n = 256 search.
+// The nb diagonal 4x4 blocks live in registers of the last DW warps (n <= 128) or, for the plans
+// with shared-memory units, in shared memory with the last nb threads (DSM), so that every warp
+// carries off-diagonal units.  The tabu triangle is a 16-bit mask per unit (pairs that are tabu
+// now); expiry iterations live in an array that is only touched when a pair is set or expires
+// (shared memory when it fits, else L2).  The split is chosen per instance on the host (qapb.cu,
+// plan_hybrid): n = 100 runs two searches per SM with one register unit per thread (352 threads),
+// n = 160 two searches per SM with 2 register + 2 shared-memory units per thread (256 threads),
+// n = 256 one search per SM on 512 threads with 1024 units in registers and 992 in 124 KB of
+// shared memory -- neither memory alone can hold the 256 KB of state of an n = 256 search.
 //
 // After move (r,s) the 4n entries on rows/columns r,s do not follow the rank-2 rule.  They
 // are fixed at the start of the next pass from six n-vectors published between the two
