@@ -651,7 +651,10 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
         P.hlay = make_hyb_layout(h->npad, h->nb, h->toff, h->us, h->exp_in_smem, h->staged, h->symmetric, h->dsm);
         P.staged = h->staged; P.dsm = h->dsm;
         P.toff = h->toff; P.us = h->us; P.exp_in_smem = h->exp_in_smem;
-    } else P.lay = make_layout(h->npad, h->nunits, h->threads, h->upt, h->acc_bits / 8, h->storage);
+    } else {
+        P.lay = make_layout(h->npad, h->nunits, h->threads, h->upt, h->acc_bits / 8, h->storage);
+        P.inv_t = (unsigned)(((1ULL << 32) + (unsigned)h->threads - 1) / (unsigned)h->threads);
+    }
     // several handles share one kernel instantiation: (re)assert this launch's opt-in size
     CU(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes));
     CU(cudaEventRecord(h->ev0, st));

@@ -105,6 +105,7 @@ struct SearchParams {
     const int32_t *perm32;           // [B,npad] start permutations (qap_start_kernel)
     const unsigned long long *start_state;  // [B] SplitMix64 state after the shuffle
     const void *initM, *initH;       // [B,npad,npad], [B,npad] from qap_build_m_kernel (int32 or int64 state)
+    unsigned inv_t;                  // generic: ceil(2^32 / threads), for uid / T without a division
     int toff, us, exp_in_smem;       // hybrid plan: off-diagonal threads, shared-memory units per thread
     int staged;                      // hybrid: int16 copies of D, F (and transposes) staged in shared memory
     int dsm;                         // hybrid: diagonal blocks in shared memory, owned by the last nb threads
@@ -268,7 +269,7 @@ __device__ __forceinline__ unsigned pair_key(int i, int j, int flag)
 // Locate element M[x][y] (x != y) in the spill layout: returns row index
 // (k*8 + w) and owning thread / lane.
 struct ElemLoc { int row, t, lane4; };
-__device__ __forceinline__ ElemLoc locate(int x, int y, int nb, int noff, int T)
+__device__ __forceinline__ ElemLoc locate(int x, int y, int nb, int noff, int T, unsigned inv_t)
 {
     int X = x >> 2, Y = y >> 2, uid, w, l;
     if (X < Y) {
@@ -281,7 +282,7 @@ __device__ __forceinline__ ElemLoc locate(int x, int y, int nb, int noff, int T)
         uid = noff + X;
         w = x & 3; l = y & 3;
     }
-    int k = uid / T;
+    int k = (int)__umulhi((unsigned)uid, inv_t);  // uid / T by the host's ceil(2^32 / T): exact for uid * T < 2^32
     ElemLoc e;
     e.t = uid - k * T;
     e.row = k * 8 + w;
@@ -302,15 +303,26 @@ __device__ __forceinline__ ElemLoc locate(int x, int y, int nb, int noff, int T)
 // -----------------------------------------------------------------------------
 __device__ __forceinline__ void expire_unit_bits(unsigned &tb, int32_t &mexp, int c, const int32_t *xp16)
 {
-    unsigned bits = tb;
+    // one 128-bit load per block row that has a bit set: the rows are independent, so their L2 latencies
+    // overlap (a loop over single bits pays one latency per bit)
     int32_t nm = 0x7fffffff;
-    while (bits) {
-        const int q = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const int32_t e = xp16[q];
-        if (e <= c) tb &= ~(1u << q);
-        else if (e != 0x7fffffff) nm = min(nm, e);
+    unsigned keep = tb;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        if ((tb >> (4 * u)) & 15u) {
+            const int4 e4 = reinterpret_cast<const int4 *>(xp16)[u];
+            const int32_t e[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const unsigned bit = 1u << (4 * u + v);
+                if (tb & bit) {
+                    if (e[v] <= c) keep &= ~bit;
+                    else if (e[v] != 0x7fffffff) nm = min(nm, e[v]);
+                }
+            }
+        }
     }
+    tb = keep;
     mexp = nm;
 }
 
@@ -554,7 +566,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                 if (improved) best_out[i] = (i == r) ? ps : (i == s) ? pr : pi;
                 if (i == r) {
                     // corners and h[r], h[s]
-                    ElemLoc lrs = locate(r, s, nb, noff, T), lsr = locate(s, r, nb, noff, T);
+                    ElemLoc lrs = locate(r, s, nb, noff, T, P.inv_t), lsr = locate(s, r, nb, noff, T, P.inv_t);
                     acc_t *prs = elem_ptr(M, lrs.row, T, lrs.t, lrs.lane4);
                     acc_t *psr = elem_ptr(M, lsr.row, T, lsr.t, lsr.lane4);
                     const acc_t mrs = *prs, msr = *psr, hr = sH[r], hs = sH[s];
@@ -567,7 +579,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                     if (tabu) {  // cells[bi][bj] = c + t; cells[bj][bi] += 1  (_kernels.pyx:176-178)
                         const int R = r >> 2, S = s >> 2;
                         const int uid = (R < S) ? R * nb - ((R * (R + 1)) >> 1) + (S - R - 1) : noff + R;
-                        const int kq = uid / T, tq = uid - kq * T;
+                        const int kq = (int)__umulhi((unsigned)uid, P.inv_t), tq = uid - kq * T;
                         const int q = (r & 3) * 4 + (s & 3);
                         const int32_t new_exp = (int32_t)(c + ten);
                         sTB[kq * T + tq] |= 1u << q;
@@ -581,8 +593,8 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                     }
                     a = 0; cc = 0; bb = 0; e = 0;
                 } else {
-                    ElemLoc lri = locate(r, i, nb, noff, T), lsi = locate(s, i, nb, noff, T);
-                    ElemLoc lir = locate(i, r, nb, noff, T), lis = locate(i, s, nb, noff, T);
+                    ElemLoc lri = locate(r, i, nb, noff, T, P.inv_t), lsi = locate(s, i, nb, noff, T, P.inv_t);
+                    ElemLoc lir = locate(i, r, nb, noff, T, P.inv_t), lis = locate(i, s, nb, noff, T, P.inv_t);
                     acc_t *pri = elem_ptr(M, lri.row, T, lri.t, lri.lane4);
                     acc_t *psi = elem_ptr(M, lsi.row, T, lsi.t, lsi.lane4);
                     acc_t *pir = elem_ptr(M, lir.row, T, lir.t, lir.lane4);
