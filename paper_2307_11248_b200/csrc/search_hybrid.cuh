@@ -439,7 +439,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         V.HJ[i] = (i & 3) - 16 * h0;
         sP[i] = P.perm32[(size_t)b * npad + i];
     }
-    unsigned long long rng_state = P.rng ? P.start_state[b] : 0ULL;
+    if (tid == 0) sMisc[4] = P.rng ? (long long)P.start_state[b] : 0LL;  // SplitMix64 state after the shuffle
     if (P.cells) {
         int64_t *cz = P.cells + (size_t)b * n * n;
         for (int i = tid; i < n * n; i += T) cz[i] = 0;
@@ -548,8 +548,12 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     for (int c = 1; c <= iters; ++c) {
         long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0;
         if (timing) tA = clock64();
-        if (tabu && P.rng && ((c - 1) & (TENURE_CHUNK - 1)) == 0)
-            fill_tenure_chunk(rng_state, P.ten_lo, P.ten_hi, P.force_seq_rng, sTen, sMisc, tid, T);
+        if (tabu && P.rng && ((c - 1) & (TENURE_CHUNK - 1)) == 0) {
+            // the stream state lives in shared memory between refills (two registers less in the loop)
+            unsigned long long st = (unsigned long long)sMisc[4];
+            fill_tenure_chunk(st, P.ten_lo, P.ten_hi, P.force_seq_rng, sTen, sMisc, tid, T);
+            if (tid == 0) sMisc[4] = (long long)st;
+        }
 
         // ---------------- pass: update + select over this thread's units
         int32_t my_d = MAXV;
