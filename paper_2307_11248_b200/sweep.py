@@ -8,7 +8,8 @@ so all runs that share (algorithm, iterations, tenure) are concatenated into a s
 `qapb_multistart_seeds` launch -- start `index` of a run with master seed `m` still uses
 `derive_seed(m, index)` (multistart.py:88), so each run's `MultiStartResult` is bit-identical
 to a separate `run_multistart` call.  `SweepPlan`, `make_sweep` and `expand` keep the
-reference's names and validation rules (tuner.py:83-131).
+reference's names and validation rules (tuner.py:83-131).  The batch runs on the calling rank's
+GPU; sharding over ranks is `run_multistart`'s job (one config at a time).
 """
 
 from __future__ import annotations

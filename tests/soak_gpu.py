@@ -1,6 +1,6 @@
 """Randomised differential soak: GPU multistart / tabu_run / two_opt_run vs the C oracle on random
 instances (sizes, value ranges, symmetry, diagonals), every launch plan of each instance.
-Usage: python scripts/soak.py [seconds] [seed]   (development aid; the oracle is the checker)"""
+Usage: python tests/soak_gpu.py [seconds] [seed]   (development aid; the oracle is the checker)"""
 import sys, time
 sys.path.insert(0, ".")
 import numpy as np
