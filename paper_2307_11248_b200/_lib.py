@@ -43,11 +43,25 @@ def _sources() -> list[str]:
     ]
 
 
+def _source_digest() -> str:
+    """sha256 over the sources and the compiler flags: decides whether the in-tree library is current
+    (file times do not survive being copied to another machine)."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(NVCC_FLAGS + os.environ.get("NVCC_EXTRA", "").split()).encode())
+    for path in _sources():
+        with open(path, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def build_library(force: bool = False, verbose: bool = False) -> str:
     """nvcc -gencode arch=compute_100a,code=sm_100a ... -> paper_2307_11248_b200/libqapb.so"""
-    newest = max(os.path.getmtime(p) for p in _sources())
-    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
-        return LIB_PATH
+    digest, stamp = _source_digest(), LIB_PATH + ".hash"
+    if not force and os.path.exists(LIB_PATH) and os.path.exists(stamp):
+        with open(stamp) as fh:
+            if fh.read().strip() == digest:
+                return LIB_PATH
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = [nvcc, *NVCC_FLAGS, *os.environ.get("NVCC_EXTRA", "").split(), "-o", LIB_PATH, os.path.join(_SRC, "qapb.cu")]
     if verbose:
@@ -55,6 +69,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise QapError(f"nvcc failed:\n{proc.stdout}\n{proc.stderr}")
+    with open(stamp, "w") as fh:
+        fh.write(digest + "\n")
     if verbose:
         print(proc.stderr)
     return LIB_PATH
