@@ -27,8 +27,9 @@
  *     a ctypes/NumPy binding of `kernels.*` calls.
  *   - There is no CPU fallback: without a CUDA device every call fails with
  *     QAPB_ERR_CUDA.
- *   - A handle is bound to one device and must not be used from two threads at
- *     the same time (it owns a scratch workspace).
+ *   - A handle is bound to one device and owns a scratch workspace: it must not be
+ *     used from two threads at the same time, nor have launches in flight on two
+ *     streams at once (create one handle per stream for that).
  */
 #ifndef QAPB_H
 #define QAPB_H
