@@ -72,8 +72,9 @@ static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
     return tab[acc_bits == 64][storage][lb_class];
 }
 
-static kern_t pick_hybrid_kernel(int symmetric, int packed, int plan)
+static kern_t pick_hybrid_kernel(int symm, int packed, int plan)
 {
+    // symm: 0 both matrices asymmetric, 1 both symmetric, 2 exactly one symmetric (plans 0, 1, 5 only)
     // plan 0: register-only (n <= 128), 80 registers/thread (two 352-thread CTAs per SM at n = 100)
     // plan 1: the same with int16 copies of D and F staged in shared memory
     // plan 2: two register units + shared-memory units per thread, 128 registers (n <= 256)
@@ -86,9 +87,15 @@ static kern_t pick_hybrid_kernel(int symmetric, int packed, int plan)
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, false, 112>, \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, true, 112>, \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128, true>}
-    static kern_t tab[2][2][6] = {{KH(false, false), KH(false, true)}, {KH(true, false), KH(true, true)}};
+#define KH2(PK) {(kern_t) qap_search_hybrid_kernel<2, PK, 1, false, false, 80>, \
+                 (kern_t) qap_search_hybrid_kernel<2, PK, 1, false, true, 80>,  \
+                 nullptr, nullptr, nullptr,                                     \
+                 (kern_t) qap_search_hybrid_kernel<2, PK, 2, true, false, 128, true>}
+    static kern_t tab[3][2][6] = {{KH(0, false), KH(0, true)}, {KH(1, false), KH(1, true)}, {KH2(false), KH2(true)}};
 #undef KH
-    return tab[symmetric != 0][packed != 0][plan];
+#undef KH2
+    kern_t k = tab[symm][packed != 0][plan];
+    return k ? k : tab[0][packed != 0][plan];  // no one-symmetric-matrix instantiation of this plan: two products
 }
 static kern_t handle_kernel(const qapb_handle *h)
 {
@@ -96,7 +103,8 @@ static kern_t handle_kernel(const qapb_handle *h)
     const int packed = h->delta_bound < ((1LL << 27) - 1);
     int plan = h->us > 0 ? 2 : (h->upt == 2 ? (h->staged ? 4 : 3) : (h->staged ? 1 : 0));
     if (h->dsm) plan = 5;
-    return h->storage == 3 ? pick_hybrid_kernel(h->symmetric, packed, plan)
+    const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
+    return h->storage == 3 ? pick_hybrid_kernel(symm, packed, plan)
                            : pick_kernel(h->acc_bits, h->storage, h->lb_class);
 }
 
@@ -571,7 +579,7 @@ static void base_params(const qapb_handle *h, SearchParams &P)
 {
     memset(&P, 0, sizeof(P));
     P.n = h->n; P.nb = h->nb; P.npad = h->npad; P.nunits = h->nunits; P.noff = h->noff; P.upt = h->upt;
-    P.symmetric = h->storage == 3 ? h->symmetric : h->sym_mode;
+    P.symmetric = h->sym_mode;  // 0 none, 1 both, 2 distance only, 3 flow only
     P.force_seq_rng = h->force_seq_rng;
     P.one = 1;
     P.sixteen = 16;

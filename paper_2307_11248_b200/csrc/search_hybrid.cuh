@@ -362,9 +362,15 @@ __device__ __forceinline__ void expire_bits(unsigned &tb, int32_t &mexp, int c, 
     mexp = nm;
 }
 
-template <bool SYM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG, bool DSM = false>
+// SYMM: 0 = both matrices asymmetric (two products per entry in the rank-2 update), 1 = both symmetric,
+// 2 = exactly one symmetric: the update is still ONE product per entry (D = D^T => a == c, so
+// a_i b_j + c_i e_j = a_i (b_j + e_j); F = F^T => b == e), the publish phase uses the general formulas
+// and stores the combined vector (P.symmetric: 2 = distance symmetric, 3 = flow symmetric).
+template <int SYMM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG, bool DSM = false>
 __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams P)
 {
+    constexpr bool SYM = SYMM != 0;       // single-product pass
+    constexpr bool FULLSYM = SYMM == 1;   // symmetric closed forms in the publish phase, no transposes
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
     const int b = blockIdx.x;
@@ -411,8 +417,8 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     // publish phase between the barriers never waits on an L1/L2 miss
     const int16_t *sD16 = reinterpret_cast<const int16_t *>(smem_raw + lay.offD16);
     const int16_t *sF16 = reinterpret_cast<const int16_t *>(smem_raw + lay.offF16);
-    const int16_t *sDT16 = SYM ? sD16 : reinterpret_cast<const int16_t *>(smem_raw + lay.offDT16);
-    const int16_t *sFT16 = SYM ? sF16 : reinterpret_cast<const int16_t *>(smem_raw + lay.offFT16);
+    const int16_t *sDT16 = FULLSYM ? sD16 : reinterpret_cast<const int16_t *>(smem_raw + lay.offDT16);
+    const int16_t *sFT16 = FULLSYM ? sF16 : reinterpret_cast<const int16_t *>(smem_raw + lay.offFT16);
     auto ldD = [&](int a, int c2) -> int32_t { return STG ? (int32_t)sD16[a * npad + c2] : D[a * npad + c2]; };
     auto ldF = [&](int a, int c2) -> int32_t { return STG ? (int32_t)sF16[a * npad + c2] : F[a * npad + c2]; };
     auto ldDT = [&](int a, int c2) -> int32_t { return STG ? (int32_t)sDT16[a * npad + c2] : DT[a * npad + c2]; };
@@ -421,7 +427,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         int16_t *wD = reinterpret_cast<int16_t *>(smem_raw + lay.offD16);
         int16_t *wF = reinterpret_cast<int16_t *>(smem_raw + lay.offF16);
         for (int e = tid; e < npad * npad; e += T) { wD[e] = (int16_t)D[e]; wF[e] = (int16_t)F[e]; }
-        if (!SYM) {
+        if (!FULLSYM) {
             int16_t *wDT = reinterpret_cast<int16_t *>(smem_raw + lay.offDT16);
             int16_t *wFT = reinterpret_cast<int16_t *>(smem_raw + lay.offFT16);
             for (int e = tid; e < npad * npad; e += T) { wDT[e] = (int16_t)DT[e]; wFT[e] = (int16_t)FT[e]; }
@@ -690,7 +696,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             const int pi = my_pi;
             const bool mid = (i != r) && (i != s);
             if (improved) best_out[i] = (i == r) ? ps : (i == s) ? pr : pi;
-            if (SYM) {
+            if (FULLSYM) {
                 // D = D^T, F = F^T: a = c, b = e, and the closed forms collapse
                 const int32_t Drs = ldD(r, s), Fpspr = ldF(ps, pr);
                 const int32_t Dsi = ldD(s, i), Dri = ldD(r, i);
@@ -722,10 +728,15 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 const int32_t a = mid ? Dis - Dir : 0, cc = mid ? Dsi - Dri : 0;
                 const int32_t bb = mid ? Fpips - Fpipr : 0, e = mid ? Fpspi - Fprpi : 0;
                 const int32_t be = bb + e;
-                V.A[i] = -a;
-                V.B[i] = bb;
-                V.C[i] = -cc;
-                V.E[i] = e;
+                if (SYMM == 2) {  // one symmetric matrix: combined vectors for the single-product update
+                    V.A[i] = -(P.symmetric == 3 ? a + cc : a);
+                    V.B[i] = P.symmetric == 2 ? bb + e : bb;
+                } else {
+                    V.A[i] = -a;
+                    V.B[i] = bb;
+                    V.C[i] = -cc;
+                    V.E[i] = e;
+                }
                 V.XR[i] = -Drs * bb - Dsr * e + (mid ? Dri : 0) * be;
                 V.XS[i] = Dsr * bb + Drs * e - (mid ? Dsi : 0) * be;
                 if (mid) {
@@ -748,7 +759,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             // corner terms (D[r][s] - D[s][r]) F[ps][pr] and (D[s][r] - D[r][s]) F[pr][ps]: zero when both
             // matrices are symmetric, so that case loads nothing here
             int32_t kr = 0, ks = 0;
-            if (!SYM) {
+            if (!FULLSYM) {
                 const int32_t Drs = ldD(r, s), Dsr = ldD(s, r);
                 const int32_t Fpspr = ldF(ps, pr), Fprps = ldF(pr, ps);
                 kr = (Drs - Dsr) * Fpspr;

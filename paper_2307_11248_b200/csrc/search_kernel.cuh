@@ -81,7 +81,7 @@ struct SearchParams {
     int mode;        // MODE_*
     int rng;         // 1: derive start permutation + tenures on the device (multistart)
     int iterations;
-    int symmetric;   // hybrid: 1 if both matrices are symmetric; generic: 0 none, 1 both, 2 distance only, 3 flow only
+    int symmetric;   // which matrices are symmetric: 0 none, 1 both, 2 distance only, 3 flow only
     int force_seq_rng;  // test hook: take the sequential (rejection-exact) RNG path
     int one, sixteen;   // runtime constants 1 and 16: multiplying by them keeps adds/shifts on the FMA (IMAD) pipe
     const int32_t *F, *FT, *D, *DT;  // [npad*npad], zero diagonal, zero padded

@@ -60,6 +60,14 @@ def _cases():
     out.append(("fuzz-unpacked-sym23",) + _fuzz_instance(23, 8, symmetric=True, diag=False, lo=0, hi=800))
     big = _fuzz_instance(30, 9, lo=0, hi=6)
     out.append(("fuzz-nostage-asym30", big[0] * 9000, big[1]))
+    # exactly one symmetric matrix: single-product update with combined vectors (hybrid SYMM = 2)
+    for n, which in ((23, "dist"), (30, "flow"), (12, "dist")):
+        f, d = _fuzz_instance(n, 40 + n, lo=0, hi=70)
+        if which == "dist":
+            d = d + d.T
+        else:
+            f = f + f.T
+        out.append((f"fuzz-one-sym-{which}{n}", f, d))
     return out
 
 
