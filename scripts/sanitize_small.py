@@ -20,6 +20,16 @@ def run(name, starts=3, iters=12):
 # shared-memory units and diagonal blocks in shared memory (n = 132), one CTA (n = 200)
 for name in ("rand12", "tai30a", "rand23", "tai112a", "rand132", "tai200a"):
     run(name)
+# exactly one symmetric matrix (hybrid single-product update with combined vectors)
+from paper_2307_11248_b200.instance import Instance
+_rs = np.random.default_rng(5)
+for _n, _which in ((23, "dist"), (40, "flow"), (132, "dist")):
+    _f = _rs.integers(0, 60, (_n, _n)).astype(np.int64); _d = _rs.integers(0, 60, (_n, _n)).astype(np.int64)
+    if _which == "dist": _d = _d + _d.T
+    else: _f = _f + _f.T
+    _inst = Instance(f"onesym{_n}{_which}", _n, _f, _d)
+    _res = q.run_multistart(_inst, q.SearchConfig(algorithm="tabu", n_starts=3, iterations=12, master_seed=1))
+    print(_inst.name, _res.best.cost, q.backend.device_instance(_f, _d).info["threads"])
 # generic kernel: int64 state (tai*b), forced int32, M in L2, masks in L2
 run("tai45b")
 os.environ["QAPB_FORCE_GENERIC"] = "1"
