@@ -207,7 +207,7 @@ __device__ __forceinline__ void admissible_min(int32_t &km, int32_t kd, unsigned
         : "r"(kd), "r"(tbk), "n"(1u << BIT), "r"(thr16));
 }
 
-template <bool PACKED>
+template <bool PACKED, bool NOTABU>
 __device__ __forceinline__ void unit_select(const int32_t (&U)[4][4], const int32_t (&L)[4][4], unsigned tbk, int Ik,
                                             int Jk, int32_t thr, const Vecs &V, int one, int sixteen,
                                             int32_t &dbest, int &sbest)
@@ -225,6 +225,23 @@ __device__ __forceinline__ void unit_select(const int32_t (&U)[4][4], const int3
         ld_vec4(V.HJ, Jk, hj);
         const int32_t thr16 = max(thr, -(1 << 27)) * 16;  // |delta| < 2^27 (host-proven)
         int32_t km[4] = {MAXV, MAXV, MAXV, MAXV};
+        if (NOTABU && tbk == 0) {
+            // 2opt instantiation, no pad slot in this unit: the running minimum alone, one ALU instruction
+            // per pair.  (Compiled out of the tabu kernels: there most warps would hold both kinds of
+            // units and execute both paths, and the extra code costs them 2-8 %.)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int32_t t1 = U[u][v] * sixteen + hi[u];
+                    const int32_t t2 = L[v][u] * sixteen + hj[v];
+                    km[u] = min(km[u], t1 * one + t2);
+                }
+            const int32_t m0 = min(min(km[0], km[1]), min(km[2], km[3]));
+            dbest = m0 >> 4;
+            sbest = m0 & 15;
+            return;
+        }
 #define QAPB_PAIR(u, v)                                                             \
     {                                                                               \
         const int32_t t1 = U[u][v] * sixteen + hi[u];                               \
@@ -366,7 +383,7 @@ __device__ __forceinline__ void expire_bits(unsigned &tb, int32_t &mexp, int c, 
 // 2 = exactly one symmetric: the update is still ONE product per entry (D = D^T => a == c, so
 // a_i b_j + c_i e_j = a_i (b_j + e_j); F = F^T => b == e), the publish phase uses the general formulas
 // and stores the combined vector (P.symmetric: 2 = distance symmetric, 3 = flow symmetric).
-template <int SYMM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG, bool DSM = false>
+template <int SYMM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG, bool DSM = false, bool NOTABU = false>
 __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams P)
 {
     constexpr bool SYM = SYMM != 0;       // single-product pass
@@ -572,7 +589,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             int sk;
             if (I[k] != J[k]) {
                 if (R >= 0) unit_update<SYM>(U[k], L[k], I[k], J[k], R, S, ru, su, V);
-                unit_select<PACKED>(U[k], L[k], tb[k], I[k], J[k], thr, V, one, sixteen, dk, sk);
+                unit_select<PACKED, NOTABU>(U[k], L[k], tb[k], I[k], J[k], thr, V, one, sixteen, dk, sk);
             } else {
                 if (R >= 0) diag_update<SYM>(U[k], I[k], R, S, ru, su, V);
                 diag_select(U[k], tb[k], I[k], thr, V.H, dk, sk);
@@ -604,7 +621,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 }
                 int32_t dk;
                 int sk;
-                unit_select<PACKED>(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V, one, sixteen, dk, sk);
+                unit_select<PACKED, NOTABU>(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V, one, sixteen, dk, sk);
                 if (dk != MAXV) {
                     const unsigned key = pair_key(4 * Ik + (sk >> 2), 4 * Jk + (sk & 3), 0);
                     if (dk < my_d || (dk == my_d && key < my_key)) { my_d = dk; my_key = key; my_which = UR + k2; my_slot = sk; }
