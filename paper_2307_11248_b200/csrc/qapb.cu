@@ -97,28 +97,29 @@ static kern_t pick_hybrid_kernel(int symm, int packed, int plan)
     kern_t k = tab[symm][packed != 0][plan];
     return k ? k : tab[0][packed != 0][plan];  // no one-symmetric-matrix instantiation of this plan: two products
 }
-// 2opt-only instantiations (selection without tabu bits) of the two plans the benchmarks use: the staged
-// one-register-unit plan and the shared-memory plan with DSM, packed keys, symmetric or not; null = use
-// the common kernel.
-static kern_t two_opt_kernel(int symm, int packed, int plan)
+// Multi-start instantiations of the two plans the benchmarks use (the staged one-register-unit plan and
+// the shared-memory plan with DSM; packed keys; both matrices symmetric or neither): no trail / cells
+// code, and for 2opt a selection without tabu bits.  null = use the common kernel.
+static kern_t multistart_kernel(int symm, int packed, int plan, int two_opt)
 {
     if (!packed || symm > 1) return nullptr;
-    if (plan == 1) return symm ? (kern_t) qap_search_hybrid_kernel<1, true, 1, false, true, 80, false, true>
-                               : (kern_t) qap_search_hybrid_kernel<0, true, 1, false, true, 80, false, true>;
-    if (plan == 5) return symm ? (kern_t) qap_search_hybrid_kernel<1, true, 2, true, false, 128, true, true>
-                               : (kern_t) qap_search_hybrid_kernel<0, true, 2, true, false, 128, true, true>;
-    return nullptr;
+#define KM(S, NT) (plan == 1 ? (kern_t) qap_search_hybrid_kernel<S, true, 1, false, true, 80, false, NT, false> \
+                             : (kern_t) qap_search_hybrid_kernel<S, true, 2, true, false, 128, true, NT, false>)
+    if (plan != 1 && plan != 5) return nullptr;
+    if (two_opt) return symm ? KM(1, true) : KM(0, true);
+    return symm ? KM(1, false) : KM(0, false);
+#undef KM
 }
 
-static kern_t handle_kernel(const qapb_handle *h, int two_opt = 0)
+static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_opt = 0)
 {
     // packed (delta, slot) keys need |delta|*16 + 15 < 2^31
     const int packed = h->delta_bound < ((1LL << 27) - 1);
     int plan = h->us > 0 ? 2 : (h->upt == 2 ? (h->staged ? 4 : 3) : (h->staged ? 1 : 0));
     if (h->dsm) plan = 5;
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
-    if (two_opt && h->storage == 3)
-        if (kern_t k2 = two_opt_kernel(symm, packed, plan)) return k2;
+    if (multistart && h->storage == 3)
+        if (kern_t k2 = multistart_kernel(symm, packed, plan, two_opt)) return k2;
     return h->storage == 3 ? pick_hybrid_kernel(symm, packed, plan)
                            : pick_kernel(h->acc_bits, h->storage, h->lb_class);
 }
@@ -669,7 +670,8 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     P.gT = (char *)h->ws + w.offT;
     P.gM_stride = w.m_elems;
     P.gT_stride = w.x_elems;
-    kern_t kern = handle_kernel(h, P.mode == MODE_TWO_OPT);
+    const bool records = P.tr_i || P.cells;
+    kern_t kern = handle_kernel(h, P.rng && !records, P.mode == MODE_TWO_OPT);
     if (h->storage == 3) {
         P.hlay = make_hyb_layout(h->npad, h->nb, h->toff, h->us, h->exp_in_smem, h->staged, h->symmetric, h->dsm);
         P.staged = h->staged; P.dsm = h->dsm;

@@ -383,7 +383,10 @@ __device__ __forceinline__ void expire_bits(unsigned &tb, int32_t &mexp, int c, 
 // 2 = exactly one symmetric: the update is still ONE product per entry (D = D^T => a == c, so
 // a_i b_j + c_i e_j = a_i (b_j + e_j); F = F^T => b == e), the publish phase uses the general formulas
 // and stores the combined vector (P.symmetric: 2 = distance symmetric, 3 = flow symmetric).
-template <int SYMM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG, bool DSM = false, bool NOTABU = false>
+// REC: the run may record a trail / the tabu memory `cells` (the single-run entries); the multi-start
+// entries never do, and their instantiations leave that code out of the winner's serial chain.
+template <int SYMM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG, bool DSM = false, bool NOTABU = false,
+          bool REC = true>
 __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams P)
 {
     constexpr bool SYM = SYMM != 0;       // single-product pass
@@ -832,12 +835,12 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 V.HI[r] = 4 * ru - 16 * hrn; V.HJ[r] = ru - 16 * hrn;
                 V.HI[s] = 4 * su - 16 * hsn; V.HJ[s] = su - 16 * hsn;
             }
-            if (P.tr_i) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
+            if (REC && P.tr_i) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
                 const size_t o = (size_t)b * iters + (c - 1);
                 P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
                 if (P.tr_tabu) P.tr_tabu[o] = (int64_t)was;
             }
-            if (tabu && P.cells) {
+            if (REC && tabu && P.cells) {
                 int64_t *cz = P.cells + (size_t)b * n * n;
                 cz[(size_t)r * n + s] = (int64_t)c + ten;
                 cz[(size_t)s * n + r] += 1;
