@@ -283,3 +283,39 @@ def test_thread_config_space():
                               "n_starts 1000 not divisible by threads_per_block 33"]
     assert q.validate_config(q.ThreadConfig(2048, 64, 32)) == (True, [])
     assert q.validate_config(q.ThreadConfig(2048, 64, 31))[1] == ["blocks 31 != n_starts / threads_per_block (32)"]
+
+
+def test_report_accuracy_and_bench_report():
+    """report.py:16-49 semantics: exact rational gap on the minimum over repetitions, six-decimal
+    formatting, DomainError for a non-positive best-known cost; bench_report batches the
+    repetitions (master seeds seed + rep, cli.py:113-115) through run_multistart_many."""
+    from fractions import Fraction
+
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.sweep import derive_seeds
+
+    assert q.accuracy(110, 100) == Fraction(1, 10) and q.accuracy(100, 100) == 0
+    assert q.format_accuracy(Fraction(1, 3)) == "0.333333" and q.format_accuracy(Fraction(0)) == "0.000000"
+    with pytest.raises(q.DomainError):
+        q.accuracy(5, 0)
+
+    inst = shapes.rand(6, 3)
+    seen = []
+
+    def fake(inst_, algorithm, seeds, iterations, low, high):
+        seen.append(np.asarray(seeds).copy())
+        costs = (seeds % np.uint64(97)).astype(np.int64) + 50
+        return costs, np.tile(np.arange(inst_.n, dtype=np.int64), (len(seeds), 1))
+
+    cfg = q.SearchConfig(algorithm="tabu", n_starts=4, iterations=5, master_seed=11)
+    reg = q.BestKnownRegistry({inst.name: 40})
+    rep = q.bench_report(inst, cfg, 3, reg, _seed_runner=fake)
+    assert len(seen) == 1 and len(seen[0]) == 12  # one launch for the three repetitions
+    want = [int(((derive_seeds(11 + r, 0, 4) % np.uint64(97)).astype(np.int64) + 50).min()) for r in range(3)]
+    assert rep.per_run_costs == want and rep.best_cost == min(want)
+    assert rep.accuracy == Fraction(min(want) - 40, 40)
+    row = rep.row()
+    assert row[:2] == [inst.name, "tabu"] and row[2] == q.format_accuracy(rep.accuracy) and row[3:5] == [min(want), 40]
+    assert q.bench_report(inst, cfg, 1, None, _seed_runner=fake).row()[2] == "no-best-known"
+    with pytest.raises(q.DomainError):
+        q.bench_report(inst, cfg, 0, reg, _seed_runner=fake)
