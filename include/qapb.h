@@ -96,6 +96,8 @@ int qapb_two_opt(qapb_handle *h, const int64_t *perms, int batch, int iterations
 
 /* kernels.tabu_run (_kernels.pyx:121-197), batched.  tenures: [batch, iterations]
  * (tenures[b, c-1] belongs to the move accepted at iteration c, tabu.py:182-186).
+ * Any int64 tenure with |c + tenure| < 2^31 is honoured (zero / negative: the cell
+ * is never tabu); qapb_tabu_host refuses others, the device entry does not look.
  * cells: [batch, n, n] or NULL (upper triangle expiry, lower triangle counts);
  * stopped_early/steps_done: [batch] (0/1 and count);
  * trail_*: [batch, iterations] or NULL together; entries past steps_done are

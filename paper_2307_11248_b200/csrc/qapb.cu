@@ -987,6 +987,13 @@ extern "C" int qapb_tabu_host(qapb_handle *h, const int64_t *perms, int batch, i
     if (!perms || !tenures || !best || !best_cost || !cur || !cur_cost) return fail(QAPB_ERR_INVALID, "NULL buffer");
     const bool tr = trail_i && trail_j && trail_delta && trail_tabu;
     const int n = h->n;
+    // expiry iterations c + tenure are int32 on the device
+    for (int b = 0; b < batch; ++b)
+        for (int c = 1; c <= iterations; ++c) {
+            const int64_t t = tenures[(size_t)b * iterations + (c - 1)];
+            if (t > 2147483647LL - c || t < -2147483647LL)
+                return fail(QAPB_ERR_UNSUPPORTED, "iteration + tenure must fit int32 (tenure " + std::to_string(t) + ")");
+        }
     const size_t pb = (size_t)batch * n * 8, sb = (size_t)batch * 8, tb = (size_t)batch * iterations * 8;
     const size_t cb = (size_t)batch * n * n * 8;
     DevBuf dp, dten, dbest, dbc, dcur, dcc, dcells, dstop, dsteps, dti, dtj, dtd, dtt;

@@ -509,3 +509,47 @@ def test_autotune_installs_the_fastest_plan(q):
     di = device_instance(inst.flow, inst.distance)
     assert di.info["threads"] == timings[0].threads
     assert q.autotune(shapes.by_name("tai45b")) == []
+
+
+@pytest.mark.parametrize("n", [5, 12, 30, 100, 130])
+def test_explicit_tenures_at_the_edges(q, orc, n):
+    """Caller-provided tenures outside the sampled interval (`tabu_run` takes any int64 array,
+    _kernels.pyx:121,176): zero and negative tenures (the cell is never tabu), a mix, and tenures so
+    long that every move becomes tabu and the search stops early (_kernels.pyx:168-170)."""
+    from paper_2307_11248_b200 import shapes
+
+    inst = shapes.rand(n, 300 + n)
+    rng = orc.Rng(5 + n)
+    perm = rng.permutation(n)
+    iters = 40 if n <= 30 else 12
+    gen = np.random.default_rng(n)
+    patterns = {
+        "zero": np.zeros(iters, np.int64),
+        "negative": np.full(iters, -3, np.int64),
+        "mixed": gen.integers(-2, 6, iters).astype(np.int64),
+        "long": np.full(iters, 1_000_000, np.int64),
+        "alternating": np.where(np.arange(iters) % 2 == 0, 1_000_000, 0).astype(np.int64),
+    }
+    # n = 30 also with entries that force the int64 generic kernel
+    variants = [(inst.flow, inst.distance)] + ([(inst.flow * 40000, inst.distance * 9000)] if n == 30 else [])
+    for flow, dist in variants:
+        for label, ten in patterns.items():
+            got = q.kernels.tabu_run(flow, dist, perm, iters, ten)
+            want = orc.tabu_run(flow, dist, perm, iters, ten)
+            for idx, (g, w) in enumerate(zip(got[:7], want[:7])):
+                assert np.array_equal(g, w), f"{label}: tabu_run output {idx}"
+            for idx, (g, w) in enumerate(zip(got[7], want[7])):
+                assert np.array_equal(g, w), f"{label}: trail array {idx}"
+
+
+def test_tenure_beyond_int32_is_refused(q):
+    """Expiry iterations are kept in int32 on the device: a tenure that would overflow is an error,
+    not a silent wrap."""
+    from paper_2307_11248_b200 import shapes
+
+    inst = shapes.rand(12, 1)
+    perm = np.arange(12, dtype=np.int64)
+    with pytest.raises(q.QapError):
+        q.kernels.tabu_run(inst.flow, inst.distance, perm, 4, np.array([1, 2**31, 1, 1], np.int64))
+    with pytest.raises(q.QapError):
+        q.kernels.tabu_run(inst.flow, inst.distance, perm, 4, np.array([1, 1, -2**31 - 9, 1], np.int64))
