@@ -248,6 +248,11 @@ class _CudaKernels:
     @staticmethod
     def two_opt_run(flow, dist, perm, iterations: int):
         """(best, best_cost, current, current_cost, move_i, move_j, move_delta) -- _kernels.pyx:118."""
+        if int(iterations) == 0:  # no sweep: the start is the answer (the loop of _kernels.pyx:94 does not run)
+            p0 = np.array(perm, dtype=_i64)
+            c0 = _CudaKernels.full_cost(flow, dist, p0)
+            empty = np.zeros(0, _i64)
+            return p0, c0, p0.copy(), c0, empty, empty.copy(), empty.copy()
         best, bc, cur, cc, mi, mj, md = device_instance(flow, dist).two_opt(perm, int(iterations))
         return best[0], int(bc[0]), cur[0], int(cc[0]), mi[0], mj[0], md[0]
 
@@ -256,6 +261,12 @@ class _CudaKernels:
         """(best, best_cost, current, current_cost, cells, stopped_early, steps_done, trail)
         with trail = (i, j, delta, tabu_flag, aspirated_flag, tenure), each cut to
         steps_done -- _kernels.pyx:189-197."""
+        if int(iterations) == 0:
+            p0 = np.array(perm, dtype=_i64)
+            c0 = _CudaKernels.full_cost(flow, dist, p0)
+            n = p0.shape[0]
+            return (p0, c0, p0.copy(), c0, np.zeros((n, n), _i64), False, 0,
+                    tuple(np.zeros(0, _i64) for _ in range(6)))
         best, bc, cur, cc, cz, stop, steps, tr, ten = device_instance(flow, dist).tabu(
             perm, int(iterations), tenures)
         k = int(steps[0])

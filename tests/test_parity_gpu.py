@@ -553,3 +553,21 @@ def test_tenure_beyond_int32_is_refused(q):
         q.kernels.tabu_run(inst.flow, inst.distance, perm, 4, np.array([1, 2**31, 1, 1], np.int64))
     with pytest.raises(q.QapError):
         q.kernels.tabu_run(inst.flow, inst.distance, perm, 4, np.array([1, 1, -2**31 - 9, 1], np.int64))
+
+
+def test_zero_iterations_return_the_start(q, orc):
+    """kernels.two_opt_run / tabu_run with an empty budget (the loops of _kernels.pyx:94,153 do not
+    run): best = current = start, empty move arrays, zero cells -- as the reference returns."""
+    from paper_2307_11248_b200 import shapes
+
+    inst = shapes.rand(12, 9)
+    perm = orc.Rng(4).permutation(12)
+    cost = orc.full_cost(inst.flow, inst.distance, perm)
+    got = q.kernels.two_opt_run(inst.flow, inst.distance, perm, 0)
+    assert np.array_equal(got[0], perm) and np.array_equal(got[2], perm) and got[1] == cost == got[3]
+    assert all(a.shape == (0,) and a.dtype == np.int64 for a in got[4:])
+    got = q.kernels.tabu_run(inst.flow, inst.distance, perm, 0, np.zeros(0, np.int64))
+    assert np.array_equal(got[0], perm) and got[1] == cost and np.array_equal(got[2], perm) and got[3] == cost
+    assert not got[4].any() and got[4].shape == (12, 12) and got[5] is False and got[6] == 0
+    assert len(got[7]) == 6 and all(a.shape == (0,) for a in got[7])
+    assert got[0] is not perm
