@@ -187,7 +187,9 @@ _ID_CACHE: dict = {}
 
 
 def _frozen(a) -> bool:
-    return isinstance(a, np.ndarray) and a.dtype == _i64 and a.flags.c_contiguous and not a.flags.writeable
+    # owndata: a read-only VIEW of a writeable base can still change underneath us -> hash those
+    return (isinstance(a, np.ndarray) and a.dtype == _i64 and a.flags.c_contiguous and not a.flags.writeable
+            and a.flags.owndata)
 
 
 _SERIAL = [0]

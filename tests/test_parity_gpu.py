@@ -571,3 +571,29 @@ def test_zero_iterations_return_the_start(q, orc):
     assert not got[4].any() and got[4].shape == (12, 12) and got[5] is False and got[6] == 0
     assert len(got[7]) == 6 and all(a.shape == (0,) for a in got[7])
     assert got[0] is not perm
+
+
+def test_instance_cache_never_serves_stale_matrices(q, orc):
+    """The kernels interface takes (flow, dist) on every call (backend.py:16-29) and the shim caches
+    the uploaded instance: by identity only for frozen arrays that own their data, by content
+    otherwise -- an in-place edit of a caller's array (or of the base of a read-only view) must be seen."""
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.backend import device_instance
+
+    inst = shapes.rand(12, 77)
+    assert device_instance(inst.flow, inst.distance) is device_instance(inst.flow, inst.distance)
+    perm = np.arange(12, dtype=np.int64)
+
+    f = inst.flow.copy()
+    d = inst.distance.copy()
+    assert q.kernels.full_cost(f, d, perm) == orc.full_cost(f, d, perm)
+    f[0, 1] += 5
+    assert q.kernels.full_cost(f, d, perm) == orc.full_cost(f, d, perm)
+    assert np.array_equal(q.kernels.all_deltas(f, d, perm), orc.all_deltas(f, d, perm))
+
+    view = f.view()
+    view.setflags(write=False)
+    before = q.kernels.full_cost(view, d, perm)
+    f[0, 1] += 7  # the base changes under the read-only view
+    after = q.kernels.full_cost(view, d, perm)
+    assert after == orc.full_cost(f, d, perm) and after != before
