@@ -87,6 +87,8 @@ class DeviceInstance:
         return out
 
     def two_opt(self, perms, iterations: int, moves: bool = True):
+        if iterations < 1:
+            raise DomainError(f"iterations must be >= 1, got {iterations}")
         p = self._perms(perms)
         b = p.shape[0]
         best, cur = np.empty((b, self.n), _i64), np.empty((b, self.n), _i64)
@@ -98,6 +100,8 @@ class DeviceInstance:
         return best, bc, cur, cc, mv[0], mv[1], mv[2]
 
     def tabu(self, perms, iterations: int, tenures, cells: bool = True, trail: bool = True):
+        if iterations < 1:
+            raise DomainError(f"iterations must be >= 1, got {iterations}")
         p = self._perms(perms)
         b = p.shape[0]
         t = np.ascontiguousarray(tenures, dtype=_i64)

@@ -257,7 +257,9 @@ def test_error_mapping(q):
 
     inst = shapes.rand(5, 1)
     with pytest.raises(q.DomainError):
-        q.kernels.two_opt_run(inst.flow, inst.distance, np.arange(5), 0)
+        q.kernels.two_opt_run(inst.flow, inst.distance, np.arange(5), -1)
+    with pytest.raises(q.DomainError):
+        q.run_two_opt(inst, 1, 0)  # the solver entry point refuses an empty budget (two_opt.py:62-63)
     with pytest.raises(q.DomainError):
         q.full_cost(inst, np.arange(4))
 
