@@ -133,4 +133,11 @@ def test_full_size_properties(q, shape, algo, starts, iters):
         deltas = md[0]
     c0 = q.evaluate_cost(inst, start)
     assert c0 + int(deltas.sum()) == int(cc[0]) == q.evaluate_cost(inst, cur[0])
+    if algo == "tabu" and inst.n <= 150:
+        # the solve command's --trail flow (cli.py:99-103, criterion 6 of test_acceptance.py:157-175): re-run
+        # the winning start with its trail and let the host auditor replay every move of it
+        rec, trail = q.run_tabu(inst, q.SplitMix64(q.derive_seed(42, k)), iters)
+        assert rec.cost == res.best.cost and np.array_equal(rec.permutation, res.best.permutation)
+        audited = q.replay_and_audit(inst, trail)
+        assert audited.cost == rec.cost and np.array_equal(audited.permutation, rec.permutation)
     assert int(bc[0]) == q.evaluate_cost(inst, best[0]) == c0 + int(np.minimum.accumulate(np.concatenate([[0], np.cumsum(deltas)])).min())
