@@ -333,7 +333,8 @@ def run_ours(args) -> None:
                 res = di.multistart(ALGO, 0, 0, STARTS_PER_GPU, it, ten.low, ten.high)
                 runs.append((it, res[1], di.last_kernel_ms() * 1e-3))
             target = runs[-1][1]
-            gap = {"target_cost": target, "target": "best of the 8n-iteration run, master_seed 0 (= CPU reference result)",
+            gap = {"starts": STARTS_PER_GPU, "scope": "one GPU (rank 0), device time of the whole multistart pipeline",
+                   "target_cost": target, "target": "best of the 8n-iteration run, master_seed 0 (= CPU reference result)",
                    "runs": [{"iterations": it, "best_cost": c, "seconds": sec, "gap_pct": 100.0 * (c - target) / target}
                             for it, c, sec in runs]}
             for g in (1.0, 0.5):
