@@ -133,6 +133,18 @@ int qapb_multistart_seeds(qapb_handle *h, int algo, const uint64_t *seeds, int c
                           int64_t ten_low, int64_t ten_high, int64_t *per_start_costs,
                           int64_t *best_perms, void *stream);
 
+/* qapb_multistart_seeds with each start's trajectory recorded: move_i/move_j/move_delta are
+ * [count, iterations] (rows past steps_done[b] are left untouched; a tabu start can stop early,
+ * _kernels.pyx:168-170).  The best cost after any shorter budget v is then
+ *   c0 + min(0, min prefix sums of move_delta[b, :v])   with c0 = per_start_costs[b] - min(0, min prefix sums),
+ * because the tenure stream of a run does not depend on its budget (tabu.py:184-186 draws it after the
+ * start permutation, in order) -- so the `neighborhoods` sweep of cli.py:162-166 over increasing
+ * iteration counts is ONE run at the largest count. */
+int qapb_multistart_trace(qapb_handle *h, int algo, const uint64_t *seeds, int count, int iterations,
+                          int64_t ten_low, int64_t ten_high, int64_t *per_start_costs,
+                          int64_t *best_perms, int64_t *steps_done, int64_t *move_i, int64_t *move_j,
+                          int64_t *move_delta, void *stream);
+
 /* Host-buffer variants (synchronous; copies inside). */
 int qapb_full_cost_host(qapb_handle *h, const int64_t *perms, int batch, int64_t *costs);
 int qapb_all_deltas_host(qapb_handle *h, const int64_t *perms, int batch, int64_t *deltas);
@@ -151,6 +163,11 @@ int qapb_multistart_host(qapb_handle *h, int algo, uint64_t master_seed, uint64_
 int qapb_multistart_seeds_host(qapb_handle *h, int algo, const uint64_t *seeds, int count,
                                int iterations, int64_t ten_low, int64_t ten_high,
                                int64_t *per_start_costs, int64_t *best_perms);
+
+int qapb_multistart_trace_host(qapb_handle *h, int algo, const uint64_t *seeds, int count,
+                               int iterations, int64_t ten_low, int64_t ten_high,
+                               int64_t *per_start_costs, int64_t *best_perms, int64_t *steps_done,
+                               int64_t *move_i, int64_t *move_j, int64_t *move_delta);
 
 /* Launch-configuration tuning (the GPU counterpart of the (N, t, b) space of tuner.py:28-78: here a
  * configuration is how one search is laid out on an SM).  `qapb_plan_candidates` lists the plans of

@@ -94,12 +94,14 @@ SIGNATURES = {
     "qapb_tabu": (c_int, [c_void_p, _P, c_int, c_int, _P] + [_P] * 11 + [c_void_p]),
     "qapb_multistart": (c_int, [c_void_p, c_int, c_uint64, c_uint64, c_int, c_int, c_int64, c_int64, _P, _P, _P, c_void_p]),
     "qapb_multistart_seeds": (c_int, [c_void_p, c_int, _P, c_int, c_int, c_int64, c_int64, _P, _P, c_void_p]),
+    "qapb_multistart_trace": (c_int, [c_void_p, c_int, _P, c_int, c_int, c_int64, c_int64] + [_P] * 6 + [c_void_p]),
     "qapb_full_cost_host": (c_int, [c_void_p, _P, c_int, _P]),
     "qapb_all_deltas_host": (c_int, [c_void_p, _P, c_int, _P]),
     "qapb_two_opt_host": (c_int, [c_void_p, _P, c_int, c_int] + [_P] * 7),
     "qapb_tabu_host": (c_int, [c_void_p, _P, c_int, c_int, _P] + [_P] * 11),
     "qapb_multistart_host": (c_int, [c_void_p, c_int, c_uint64, c_uint64, c_int, c_int, c_int64, c_int64, _P, _P, _P]),
     "qapb_multistart_seeds_host": (c_int, [c_void_p, c_int, _P, c_int, c_int, c_int64, c_int64, _P, _P]),
+    "qapb_multistart_trace_host": (c_int, [c_void_p, c_int, _P, c_int, c_int, c_int64, c_int64] + [_P] * 6),
     "qapb_plan_candidates": (c_int, [c_void_p, _P, c_int, POINTER(c_int)]),
     "qapb_set_plan": (c_int, [c_void_p, c_int, c_int, c_int, c_int]),
     "qapb_last_kernel_ms": (c_int, [c_void_p, POINTER(c_float)]),

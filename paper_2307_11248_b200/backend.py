@@ -145,6 +145,24 @@ class DeviceInstance:
             self._h, algo, _addr(sd), count, iterations, ten_low, ten_high, _addr(costs), _addr(perms)))
         return costs, perms
 
+    def multistart_trace(self, algorithm: str, seeds, iterations: int, ten_low: int = 1, ten_high: int = 1):
+        """`multistart_seeds` with every start's trajectory: (per_start_costs[count], best_perms[count, n],
+        steps_done[count], move_i, move_j, move_delta -- each [count, iterations], zero past steps_done)."""
+        sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+        if sd.ndim != 1 or sd.size < 1:
+            raise DomainError("seeds must be a non-empty 1-d array")
+        if iterations < 1:
+            raise DomainError(f"iterations must be >= 1, got {iterations}")
+        count = int(sd.size)
+        costs, steps = np.empty(count, _i64), np.empty(count, _i64)
+        perms = np.empty((count, self.n), _i64)
+        mv = [np.empty((count, iterations), _i64) for _ in range(3)]
+        algo = _lib.ALGO_TABU if algorithm == "tabu" else _lib.ALGO_2OPT
+        _lib.check(_lib.lib().qapb_multistart_trace_host(
+            self._h, algo, _addr(sd), count, iterations, ten_low, ten_high, _addr(costs), _addr(perms), _addr(steps),
+            _addr(mv[0]), _addr(mv[1]), _addr(mv[2])))
+        return costs, perms, steps, mv[0], mv[1], mv[2]
+
     def multistart_device(self, algorithm: str, master_seed: int, first_index: int, count: int,
                           iterations: int, ten_low: int, ten_high: int,
                           costs_ptr: int, key_ptr: int, perm_ptr: int, stream: int = 0) -> None:

@@ -861,6 +861,36 @@ extern "C" int qapb_multistart_seeds(qapb_handle *h, int algo, const uint64_t *s
     return launch_search(h, P, count, head, (cudaStream_t)stream);
 }
 
+extern "C" int qapb_multistart_trace(qapb_handle *h, int algo, const uint64_t *seeds, int count, int iterations,
+                                     int64_t ten_low, int64_t ten_high, int64_t *per_start_costs, int64_t *best_perms,
+                                     int64_t *steps_done, int64_t *move_i, int64_t *move_j, int64_t *move_delta,
+                                     void *stream)
+{
+    int rc = check_common(h, count);
+    if (rc) return rc;
+    rc = check_multistart_args(algo, iterations, ten_low, ten_high);
+    if (rc) return rc;
+    if (!seeds || !per_start_costs || !best_perms || !steps_done || !move_i || !move_j || !move_delta)
+        return fail(QAPB_ERR_INVALID, "NULL buffer");
+    const size_t perm_bytes = (size_t)count * h->n * sizeof(int64_t);
+    const size_t head = perm_bytes + (size_t)count * sizeof(int64_t);
+    rc = ensure_ws(h, plan_ws(h, count, head).total);
+    if (rc) return rc;
+    SearchParams P;
+    base_params(h, P);
+    P.mode = algo == QAPB_ALGO_TABU ? MODE_TABU : MODE_TWO_OPT;
+    P.rng = 1;
+    P.iterations = iterations;
+    P.seeds = (const unsigned long long *)seeds;
+    P.ten_lo = ten_low;
+    P.ten_hi = ten_high;
+    P.best = best_perms; P.best_cost = per_start_costs;
+    P.cur = (int64_t *)h->ws; P.cur_cost = (int64_t *)((char *)h->ws + perm_bytes);
+    P.steps = steps_done;
+    P.tr_i = move_i; P.tr_j = move_j; P.tr_d = move_delta;  // selects the recording instantiation
+    return launch_search(h, P, count, head, (cudaStream_t)stream);
+}
+
 extern "C" int qapb_plan_candidates(qapb_handle *h, int32_t *plans, int cap, int *count)
 {
     if (!h || !count || (cap > 0 && !plans)) return fail(QAPB_ERR_INVALID, "NULL argument");
@@ -1056,6 +1086,35 @@ extern "C" int qapb_multistart_seeds_host(qapb_handle *h, int algo, const uint64
     if (rc) return rc;
     D2H(per_start_costs, d + cb, cb);
     D2H(best_perms, d + 2 * cb, pb);
+    return QAPB_OK;
+}
+
+extern "C" int qapb_multistart_trace_host(qapb_handle *h, int algo, const uint64_t *seeds, int count, int iterations,
+                                          int64_t ten_low, int64_t ten_high, int64_t *per_start_costs,
+                                          int64_t *best_perms, int64_t *steps_done, int64_t *move_i, int64_t *move_j,
+                                          int64_t *move_delta)
+{
+    int rc = check_common(h, count);
+    if (rc) return rc;
+    if (iterations < 1) return fail(QAPB_ERR_INVALID, "iterations must be >= 1, got " + std::to_string(iterations));
+    if (!seeds || !per_start_costs || !best_perms || !steps_done || !move_i || !move_j || !move_delta)
+        return fail(QAPB_ERR_INVALID, "NULL buffer");
+    const size_t cb = (size_t)count * 8, pb = (size_t)count * h->n * 8, tb = (size_t)count * iterations * 8;
+    DevBuf buf;  // [seeds | costs | steps | perms | move_i | move_j | move_delta]
+    CU(buf.alloc(3 * cb + pb + 3 * tb));
+    char *d = buf.as<char>();
+    H2D(d, seeds, cb);
+    CU(cudaMemsetAsync(d + 3 * cb + pb, 0, 3 * tb, nullptr));  // rows past steps_done read as zero
+    rc = qapb_multistart_trace(h, algo, (const uint64_t *)d, count, iterations, ten_low, ten_high, (int64_t *)(d + cb),
+                               (int64_t *)(d + 3 * cb), (int64_t *)(d + 2 * cb), (int64_t *)(d + 3 * cb + pb),
+                               (int64_t *)(d + 3 * cb + pb + tb), (int64_t *)(d + 3 * cb + pb + 2 * tb), nullptr);
+    if (rc) return rc;
+    D2H(per_start_costs, d + cb, cb);
+    D2H(steps_done, d + 2 * cb, cb);
+    D2H(best_perms, d + 3 * cb, pb);
+    D2H(move_i, d + 3 * cb + pb, tb);
+    D2H(move_j, d + 3 * cb + pb + tb, tb);
+    D2H(move_delta, d + 3 * cb + pb + 2 * tb, tb);
     return QAPB_OK;
 }
 

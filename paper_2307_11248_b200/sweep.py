@@ -92,6 +92,44 @@ def run_multistart_many(inst: Instance, configs: Sequence[SearchConfig], *, _see
     return out  # type: ignore[return-value]
 
 
+def _cuda_trace_runner(inst: Instance, algorithm: str, seeds: np.ndarray, iterations: int, low: int, high: int):
+    import torch
+
+    from .backend import device_instance
+
+    if not torch.cuda.is_available():
+        raise QapError("no CUDA device: the multi-start path has no CPU fallback")
+    di = device_instance(inst.flow, inst.distance, torch.cuda.current_device())
+    costs, _perms, steps, _mi, _mj, deltas = di.multistart_trace(algorithm, seeds, iterations, low, high)
+    return costs, steps, deltas
+
+
+def best_costs_at_budgets(inst: Instance, cfg: SearchConfig, budgets: Sequence[int], *, _trace_runner=None) -> np.ndarray:
+    """Best cost of every start of `cfg` after each iteration budget in `budgets`, from ONE run at the
+    largest budget: array [len(budgets), n_starts], row k equal to
+    `run_multistart(inst, replace(cfg, iterations=budgets[k])).per_start_costs`.
+
+    A run's tenure stream is drawn in order after its start permutation (tabu.py:184-186), so the
+    run with budget v is the first v iterations of any longer run (and a start that stops early,
+    _kernels.pyx:168-170, stops at the same step under every budget that reaches it).  The recorded
+    move deltas give the cost after each step; the running minimum is the best-so-far."""
+    if not budgets or any(v < 1 for v in budgets):
+        raise DomainError("budgets must be a non-empty list of positive iteration counts")
+    runner = _trace_runner or _cuda_trace_runner
+    ten = cfg.resolved_tenure(inst.n)
+    top = max(budgets)
+    seeds = derive_seeds(cfg.master_seed, 0, cfg.n_starts)
+    costs, steps, deltas = runner(inst, cfg.algorithm, seeds, top, ten.low, ten.high)
+    costs = np.asarray(costs, dtype=np.int64)
+    steps = np.asarray(steps, dtype=np.int64)
+    deltas = np.asarray(deltas, dtype=np.int64)[:, :top]
+    live = np.arange(top)[None, :] < steps[:, None]
+    walk = np.cumsum(np.where(live, deltas, 0), axis=1)  # cost after each step, relative to the start cost
+    low_water = np.minimum.accumulate(np.minimum(walk, 0), axis=1)  # best-so-far (strict <: ties keep the earlier best)
+    start_cost = costs - low_water[:, -1]
+    return np.stack([start_cost + low_water[:, min(v, top) - 1] for v in budgets])
+
+
 def run_repetitions(inst: Instance, cfg: SearchConfig, repetitions: int) -> list[MultiStartResult]:
     """The bench loop of cli.py:113-115: master seeds `cfg.master_seed + rep`, one launch."""
     if repetitions < 1:
@@ -134,9 +172,15 @@ def expand(plan: SweepPlan, repetitions: int) -> Iterator[tuple[int, int, int]]:
 
 def run_sweep(inst: Instance, plan: SweepPlan, repetitions: int) -> list[tuple[int, int, int]]:
     """Rows (axis_value, repetition, best_cost) of the reference's sweep command (cli.py:162-175):
-    neighborhoods -> iterations = value; instances -> n_starts = value; seeds -> minimum over
-    `value` master seeds `seed + 7919 * idx`.  All runs go through `run_multistart_many`."""
+    neighborhoods -> iterations = value (all budgets of a repetition from one traced run,
+    `best_costs_at_budgets`); instances -> n_starts = value; seeds -> minimum over `value` master
+    seeds `seed + 7919 * idx`.  The latter two go through `run_multistart_many`."""
     rows = list(expand(plan, repetitions))
+    if plan.axis == "neighborhoods":
+        # every budget of one repetition is a prefix of its longest run: one traced run per repetition
+        table = {seed: best_costs_at_budgets(inst, replace(plan.base, master_seed=seed), list(plan.values))
+                 for seed in sorted({seed for _v, _r, seed in rows})}
+        return [(value, rep, int(table[seed][plan.values.index(value)].min())) for value, rep, seed in rows]
     configs: list[SearchConfig] = []
     spans: list[tuple[int, int]] = []
     for value, _rep, seed in rows:

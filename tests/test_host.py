@@ -319,3 +319,41 @@ def test_report_accuracy_and_bench_report():
     assert q.bench_report(inst, cfg, 1, None, _seed_runner=fake).row()[2] == "no-best-known"
     with pytest.raises(q.DomainError):
         q.bench_report(inst, cfg, 0, reg, _seed_runner=fake)
+
+
+def test_best_costs_at_budgets_from_one_trace(built):
+    """sweep.best_costs_at_budgets: the prefix property behind the one-run `neighborhoods` sweep
+    (cli.py:162-166) -- checked with a trace runner made of the oracle's single-start runs against the
+    oracle's own multistart at every budget, including a start that stops early."""
+    from dataclasses import replace
+
+    from paper_2307_11248_b200 import shapes
+    import oracle as orc
+    from paper_2307_11248_b200.sweep import best_costs_at_budgets
+
+    def oracle_trace(inst_, algorithm, seeds, iterations, low, high):
+        costs, steps, deltas = [], [], np.zeros((len(seeds), iterations), np.int64)
+        for b, sd in enumerate(seeds):
+            rng = orc.Rng(int(sd))
+            perm = rng.permutation(inst_.n)
+            if algorithm == "tabu":
+                out = orc.tabu_run(inst_.flow, inst_.distance, perm, iterations, rng.tenures(low, high, iterations))
+                k, d = int(out[6]), out[7][2]
+            else:
+                out = orc.two_opt_run(inst_.flow, inst_.distance, perm, iterations)
+                k, d = iterations, out[6]
+            costs.append(int(out[1])); steps.append(k); deltas[b, :k] = d[:k]
+        return np.array(costs, np.int64), np.array(steps, np.int64), deltas
+
+    for inst, algo, ten in ((shapes.rand(12, 5), "tabu", None), (shapes.rand(9, 2), "2opt", None),
+                            (shapes.rand(4, 8), "tabu", q.TenureInterval(40, 60))):  # n = 4, long tenures: early stops
+        cfg = q.SearchConfig(algorithm=algo, n_starts=6, iterations=1, master_seed=31, tenure=ten)
+        budgets = [1, 3, 10, 37]
+        got = best_costs_at_budgets(inst, cfg, budgets, _trace_runner=oracle_trace)
+        assert got.shape == (4, 6)
+        t = cfg.resolved_tenure(inst.n)
+        for row, v in zip(got, budgets):
+            want = orc.multistart(inst.flow, inst.distance, algo, 31, 6, v, tenure=(t.low, t.high))
+            assert np.array_equal(row, want[0]), (inst.n, algo, v)
+    with pytest.raises(q.DomainError):
+        best_costs_at_budgets(inst, cfg, [], _trace_runner=oracle_trace)

@@ -599,3 +599,43 @@ def test_instance_cache_never_serves_stale_matrices(q, orc):
     f[0, 1] += 7  # the base changes under the read-only view
     after = q.kernels.full_cost(view, d, perm)
     assert after == orc.full_cost(f, d, perm) and after != before
+
+
+@pytest.mark.parametrize("shape,algo,starts,budgets", [("rand23", "tabu", 9, [1, 5, 23, 60]), ("rand30", "2opt", 7, [2, 40]),
+                                                       ("tai100a", "tabu", 40, [50, 100, 400]),
+                                                       ("tai150b", "tabu", 6, [10, 60])])
+def test_budget_sweep_from_one_traced_run(q, orc, shape, algo, starts, budgets):
+    """qapb_multistart_trace + sweep.best_costs_at_budgets: one run at the largest budget reproduces
+    `run_multistart(...).per_start_costs` of every shorter budget (the neighborhoods axis of
+    cli.py:162-166); the recorded trajectories equal the oracle's, and run_sweep uses it."""
+    from dataclasses import replace
+
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.backend import device_instance
+    from paper_2307_11248_b200.sweep import derive_seeds
+
+    inst = shapes.by_name(shape)
+    cfg = q.SearchConfig(algorithm=algo, n_starts=starts, iterations=budgets[-1], master_seed=77)
+    table = q.best_costs_at_budgets(inst, cfg, budgets)
+    for row, v in zip(table, budgets):
+        assert np.array_equal(row, q.run_multistart(inst, replace(cfg, iterations=v)).per_start_costs), v
+    # trajectories of the traced run against the oracle (first starts; the oracle is O(n^3) per iteration)
+    ten = q.tenure_bounds(inst.n)
+    top = budgets[-1] if inst.n <= 30 else budgets[0]
+    seeds = derive_seeds(77, 0, starts)
+    costs, perms, steps, mi, mj, md = device_instance(inst.flow, inst.distance).multistart_trace(algo, seeds, top, ten.low, ten.high)
+    for b in range(min(starts, 3)):
+        rng = orc.Rng(int(seeds[b]))
+        perm = rng.permutation(inst.n)
+        if algo == "tabu":
+            want = orc.tabu_run(inst.flow, inst.distance, perm, top, rng.tenures(ten.low, ten.high, top))
+            k, wi, wj, wd = int(want[6]), want[7][0], want[7][1], want[7][2]
+        else:
+            want = orc.two_opt_run(inst.flow, inst.distance, perm, top)
+            k, wi, wj, wd = top, want[4], want[5], want[6]
+        assert int(steps[b]) == k and int(costs[b]) == int(want[1]) and np.array_equal(perms[b], want[0])
+        assert np.array_equal(mi[b, :k], wi[:k]) and np.array_equal(mj[b, :k], wj[:k]) and np.array_equal(md[b, :k], wd[:k])
+    if inst.n <= 30:
+        rows = q.run_sweep(inst, q.make_sweep("neighborhoods", budgets, cfg), 2)
+        for value, rep, cost in rows:
+            assert cost == q.run_multistart(inst, replace(cfg, iterations=value, master_seed=77 + rep)).best.cost
