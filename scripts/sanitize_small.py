@@ -13,6 +13,8 @@ def run(name, starts=3, iters=12):
     rec, trail = q.run_tabu(inst, 3, iters)
     q.all_deltas(inst, rec.permutation)
     many = q.run_repetitions(inst, q.SearchConfig(algorithm="tabu", n_starts=2, iterations=iters, master_seed=1), 2)
+    for algo in ("tabu", "2opt"):  # device RNG + recorded moves (qapb_multistart_trace)
+        q.best_costs_at_budgets(inst, q.SearchConfig(algorithm=algo, n_starts=2, iterations=iters, master_seed=1), [3, iters])
     info = q.backend.device_instance(inst.flow, inst.distance).info
     print(name, res.best.cost, res2.best.cost, rec.cost, many[1].best.cost, "storage", info["storage"], "threads", info["threads"], "acc", info["acc_bits"])
 
