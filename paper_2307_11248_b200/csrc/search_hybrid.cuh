@@ -580,6 +580,14 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             fill_tenure_chunk(st, P.ten_lo, P.ten_hi, P.force_seq_rng, sTen, sMisc, tid, T);
             if (tid == 0) sMisc[4] = (long long)st;
         }
+        if (REC && tabu && !P.rng && ((c - 1) & (TENURE_CHUNK - 1)) == 0) {
+            // caller-provided tenures: stage the next chunk, so that the owner of the winning pair reads
+            // shared memory instead of waiting for L2 on the serial path (visible after barrier 1;
+            // c + tenure is taken modulo 2^32 either way)
+            const int64_t *src = P.tenures + (size_t)b * iters + (c - 1);
+            const int m = min((int)TENURE_CHUNK, iters - (c - 1));
+            for (int k = tid; k < m; k += T) sTen[k] = (int32_t)src[k];
+        }
 
         // ---------------- pass: update + select over this thread's units
         int32_t my_d = MAXV;
@@ -786,8 +794,8 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 ks = (Dsr - Drs) * Fprps;
             }
             // the tenure of this move (tabu.py:184-186): drawn on the device or provided by the caller
-            const long long ten = !tabu ? 0 : (P.rng ? (long long)sTen[(c - 1) & (TENURE_CHUNK - 1)]
-                                                     : (long long)P.tenures[(size_t)b * iters + (c - 1)]);
+            const long long ten = !tabu ? 0 : ((P.rng || REC) ? (long long)sTen[(c - 1) & (TENURE_CHUNK - 1)]
+                                                              : (long long)P.tenures[(size_t)b * iters + (c - 1)]);
             const int32_t new_exp = (int32_t)(c + ten);
             int32_t mrs = 0, msr = 0;
             unsigned was = 0;
