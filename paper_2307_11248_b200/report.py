@@ -31,12 +31,12 @@ def format_accuracy(value: Fraction) -> str:
 @dataclass
 class RunReport:
     instance_name: str
-    algorithm: str
-    best_cost: int
-    best_known: int | None
-    per_run_costs: list[int] = field(default_factory=list)
-    wall_times: list[float] = field(default_factory=list)
-    config_digest: str = ""
+    algorithm: str                       # "2opt" | "tabu"
+    best_cost: int                       # minimum over the repetitions
+    best_known: int | None               # registry entry, None if the instance has none
+    per_run_costs: list[int] = field(default_factory=list)   # one per repetition (master_seed + rep)
+    wall_times: list[float] = field(default_factory=list)    # one entry: the repetitions ran as one launch
+    config_digest: str = ""              # digest of the base configuration (repetition 0)
 
     @property
     def accuracy(self) -> Fraction | None:
