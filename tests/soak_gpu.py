@@ -27,6 +27,8 @@ while time.time() - t0 < budget:
     if rs.random() < 0.3:
         f[rs.random((n, n)) < 0.6] = 0
     iters = int(rs.integers(1, 3 * n + 8)) if n <= 64 else int(rs.integers(1, 40))
+    if n <= 33 and rs.random() < 0.08:
+        iters = int(rs.integers(250, 700))  # across the 256-iteration tenure chunk boundaries
     starts = int(rs.integers(1, 7))
     algo = "tabu" if rs.random() < 0.7 else "2opt"
     master = int(rs.integers(0, 2**62))
