@@ -81,8 +81,23 @@ def save(name, d):
     print("wrote", path, os.path.getsize(path), "bytes")
 
 
+def full_length():
+    """Full-length single-start runs of the big BASELINE.json configurations (the lengths bench.py
+    times): about three minutes of the reference's compiled kernel, one-off."""
+    save("full_cfg2_tai100a_tabu", single("tai100a", "tabu", qapsolve.derive_seed(0, 0), 800))
+    save("full_cfg4_tai150b_tabu", single("tai150b", "tabu", qapsolve.derive_seed(3, 1), 1200))
+    save("full_cfg4_sko100_tabu", single("sko100", "tabu", qapsolve.derive_seed(3, 2), 800))
+    save("full_cfg3_tai256c_2opt", single("tai256c", "2opt", 11, 1024))
+    save("full_cfg3_tai256c_tabu", single("tai256c", "tabu", 11, 2048))
+    # criterion-6 style audit at n >= 150 (test_acceptance.py:157-175): 6 starts x 8n iterations
+    save("full_cfg4_tai150b_multi6", multi("tai150b", "tabu", 6, 1200, 7))
+
+
 if __name__ == "__main__":
     print("reference backend:", qapsolve.backend.kernels.BACKEND_NAME)
+    if "--full" in sys.argv:
+        full_length()
+        sys.exit(0)
     # BASELINE.json configs[0]: 2opt single start, nug12 shape, 4n iterations
     save("cfg0_nug12_2opt", single("nug12", "2opt", 3, 48))
     save("cfg0_nug12_tabu", single("nug12", "tabu", 3, 96))
