@@ -184,11 +184,20 @@ int qapb_set_plan(qapb_handle *h, int reg_units, int unit_threads, int smem_unit
  * roofline figure. */
 int qapb_last_kernel_ms(qapb_handle *h, float *ms);
 
+/* Sum of steps_done over the starts of the most recent qapb_multistart on this handle (synchronises
+ * with that launch).  A tabu start can stop early (_kernels.pyx:168-170), so the number of move
+ * evaluations of a run is this sum times n(n-1)/2, not starts x iterations. */
+int qapb_last_total_steps(qapb_handle *h, int64_t *steps);
+
 /* Integer-pipe peak probe: runs a dependent-chain-free IMAD/IADD3 loop on every
  * SM and reports lane-operations per second (the roofline denominator SURVEY.md
  * section 8d asks to be measured on the box).  `kind`: 0 = IMAD only,
  * 1 = IADD3 only, 2 = mixed 1:1. */
 int qapb_probe_int_peak(int device, int kind, double *ops_per_sec);
+
+/* Shared-memory bandwidth probe: conflict-free 128-bit loads on every SM, bytes per second (the
+ * shared-memory roofline denominator of SURVEY.md section 8d). */
+int qapb_probe_smem_peak(int device, double *bytes_per_sec);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,8 @@ from .errors import DomainError, QapError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_PKG, "csrc")
-LIB_PATH = os.path.join(_PKG, "libqapb.so")
+# QAPB_LIB: development override (a single-instantiation build from scripts/devbuild.sh)
+LIB_PATH = os.environ.get("QAPB_LIB") or os.path.join(_PKG, "libqapb.so")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
@@ -106,6 +107,8 @@ SIGNATURES = {
     "qapb_set_plan": (c_int, [c_void_p, c_int, c_int, c_int, c_int]),
     "qapb_last_kernel_ms": (c_int, [c_void_p, POINTER(c_float)]),
     "qapb_probe_int_peak": (c_int, [c_int, c_int, POINTER(c_double)]),
+    "qapb_probe_smem_peak": (c_int, [c_int, POINTER(c_double)]),
+    "qapb_last_total_steps": (c_int, [c_void_p, POINTER(c_int64)]),
 }
 
 

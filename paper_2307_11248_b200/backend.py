@@ -191,6 +191,12 @@ class DeviceInstance:
         _lib.check(_lib.lib().qapb_set_plan(self._h, *[int(x) for x in plan]))
         self._refresh_info()
 
+    def last_total_steps(self) -> int:
+        """Sum of steps_done over the starts of the last `multistart*` call on this handle."""
+        v = ctypes.c_int64(0)
+        _lib.check(_lib.lib().qapb_last_total_steps(self._h, ctypes.byref(v)))
+        return int(v.value)
+
     def last_kernel_ms(self) -> float:
         ms = ctypes.c_float(0)
         _lib.check(_lib.lib().qapb_last_kernel_ms(self._h, ctypes.byref(ms)))
@@ -219,12 +225,14 @@ _SERIAL = [0]
 
 def device_instance(flow, dist, device: int = 0) -> DeviceInstance:
     """Cached `DeviceInstance`: by identity for frozen arrays (no hashing), else keyed by matrix contents.
-    Both kinds live in one LRU that closes evicted handles."""
+    Both kinds live in one LRU; eviction only drops the cache's reference."""
     by_id = _frozen(flow) and _frozen(dist)
     with _CACHE_LOCK:
         if by_id:
             hit = _ID_CACHE.get((id(flow), id(dist), device))
             if hit is not None and hit[0]() is flow and hit[1]() is dist and hit[2]._h:
+                if hit[3] in _CACHE:
+                    _CACHE.move_to_end(hit[3])
                 return hit[2]
             _SERIAL[0] += 1
             key = ("id", _SERIAL[0])
@@ -239,12 +247,15 @@ def device_instance(flow, dist, device: int = 0) -> DeviceInstance:
         inst = DeviceInstance(f, d, device)
         _CACHE[key] = inst
         while len(_CACHE) > _CACHE_MAX:
+            # drop the cache's reference only: a caller (or another thread inside a C call) may still hold
+            # the evicted instance; its handle is destroyed when the last reference goes (__del__)
             _, old = _CACHE.popitem(last=False)
-            old.close()
+            for k in [k for k, v in _ID_CACHE.items() if v[2] is old]:
+                del _ID_CACHE[k]
         if by_id:
             for k in [k for k, v in _ID_CACHE.items() if v[0]() is None or v[1]() is None or not v[2]._h]:
                 del _ID_CACHE[k]
-            _ID_CACHE[(id(flow), id(dist), device)] = (weakref.ref(flow), weakref.ref(dist), inst)
+            _ID_CACHE[(id(flow), id(dist), device)] = (weakref.ref(flow), weakref.ref(dist), inst, key)
         return inst
 
 

@@ -22,6 +22,7 @@
 using namespace qapb;
 
 int g_attr_smem(int device);  // opt-in shared memory per block of a device seen by qapb_create
+static cudaError_t ensure_smem_optin(const void *kern, int device, unsigned bytes);
 static thread_local std::string g_err;
 static int fail(int code, const std::string &msg)
 {
@@ -44,6 +45,7 @@ struct qapb_handle {
     int toff = 0, us = 0, exp_in_smem = 1;         // hybrid plan
     int staged = 0, fits_i16 = 0;                  // int16 copies of D/F staged in shared memory
     int dsm = 0;                                   // hybrid: diagonal blocks in shared memory (no dedicated warps)
+    int dd = 0;                                    // hybrid: diagonal blocks paired in the registers of the threads after the last unit
     unsigned smem_bytes = 0;
     int ctas_per_sm = 0, sm_count = 0;
     long long delta_bound = 0;
@@ -56,9 +58,29 @@ struct qapb_handle {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int have_timing = 0;
     int force_seq_rng = 0;
+    size_t steps_total_off = (size_t)-1;  // workspace offset of the last multistart's summed steps_done
 };
 
 typedef void (*kern_t)(const SearchParams);
+#ifdef QAPB_DEV_ONLY
+// development build (seconds instead of minutes): only one instantiation, -DQAPB_DEV_ONLY=<preset>
+#if QAPB_DEV_ONLY == 1   // tai100a / sko100 multi-start tabu (staged one-register-unit plan)
+#define QAPB_DEV_ARGS 1, true, 1, false, true, 80, false, false, false
+#elif QAPB_DEV_ONLY == 2 // tai256c multi-start tabu (shared-memory units, DSM)
+#define QAPB_DEV_ARGS 1, true, 2, true, false, 128, true, false, false
+#elif QAPB_DEV_ONLY == 4 // preset 1 with paired diagonal blocks (DD), 64 registers
+#define QAPB_DEV_ARGS 1, true, 1, false, true, 64, false, false, false, true
+#elif QAPB_DEV_ONLY == 6 // DD at 80 registers
+#define QAPB_DEV_ARGS 1, true, 1, false, true, 80, false, false, false, true
+#elif QAPB_DEV_ONLY == 5 // recording instantiation of preset 4
+#define QAPB_DEV_ARGS 1, true, 1, false, true, 64, false, false, true, true
+#elif QAPB_DEV_ONLY == 3 // recording instantiation of preset 1 (single-run entries: parity tests)
+#define QAPB_DEV_ARGS 1, true, 1, false, true, 80
+#endif
+static kern_t pick_kernel(int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
+static kern_t pick_hybrid_kernel(int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
+static kern_t multistart_kernel(int, int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
+#else
 static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
 {
 #define K(A, S, MT, MB) (kern_t) qap_search_kernel<A, S, MT, MB>
@@ -81,17 +103,22 @@ static kern_t pick_hybrid_kernel(int symm, int packed, int plan)
     // plan 3/4: two register units per thread on half the threads, 112 registers (109 <= n <= 120:
     //           two CTAs per SM where plan 0/1 would fit only one), without / with int16 staging
     // plan 5: plan 2 with the diagonal blocks in shared memory (no dedicated diagonal warps)
+    // plan 6/7: plan 0/1 with the diagonal blocks paired in the threads after the last unit (DD), 64 registers
 #define KH(S, PK) {(kern_t) qap_search_hybrid_kernel<S, PK, 1, false, false, 80>, \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, true, 80>,  \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128>,  \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, false, 112>, \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, true, 112>, \
-                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128, true>}
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128, true>,  \
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, false, 64, false, false, true, true>, \
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, true, 64, false, false, true, true>}
 #define KH2(PK) {(kern_t) qap_search_hybrid_kernel<2, PK, 1, false, false, 80>, \
                  (kern_t) qap_search_hybrid_kernel<2, PK, 1, false, true, 80>,  \
                  nullptr, nullptr, nullptr,                                     \
-                 (kern_t) qap_search_hybrid_kernel<2, PK, 2, true, false, 128, true>}
-    static kern_t tab[3][2][6] = {{KH(0, false), KH(0, true)}, {KH(1, false), KH(1, true)}, {KH2(false), KH2(true)}};
+                 (kern_t) qap_search_hybrid_kernel<2, PK, 2, true, false, 128, true>,  \
+                 (kern_t) qap_search_hybrid_kernel<2, PK, 1, false, false, 64, false, false, true, true>, \
+                 (kern_t) qap_search_hybrid_kernel<2, PK, 1, false, true, 64, false, false, true, true>}
+    static kern_t tab[3][2][8] = {{KH(0, false), KH(0, true)}, {KH(1, false), KH(1, true)}, {KH2(false), KH2(true)}};
 #undef KH
 #undef KH2
     kern_t k = tab[symm][packed != 0][plan];
@@ -104,12 +131,14 @@ static kern_t multistart_kernel(int symm, int packed, int plan, int two_opt)
 {
     if (!packed || symm > 1) return nullptr;
 #define KM(S, NT) (plan == 1 ? (kern_t) qap_search_hybrid_kernel<S, true, 1, false, true, 80, false, NT, false> \
+                   : plan == 7 ? (kern_t) qap_search_hybrid_kernel<S, true, 1, false, true, 64, false, NT, false, true> \
                              : (kern_t) qap_search_hybrid_kernel<S, true, 2, true, false, 128, true, NT, false>)
-    if (plan != 1 && plan != 5) return nullptr;
+    if (plan != 1 && plan != 5 && plan != 7) return nullptr;
     if (two_opt) return symm ? KM(1, true) : KM(0, true);
     return symm ? KM(1, false) : KM(0, false);
 #undef KM
 }
+#endif
 
 static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_opt = 0)
 {
@@ -117,6 +146,7 @@ static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_op
     const int packed = h->delta_bound < ((1LL << 27) - 1);
     int plan = h->us > 0 ? 2 : (h->upt == 2 ? (h->staged ? 4 : 3) : (h->staged ? 1 : 0));
     if (h->dsm) plan = 5;
+    if (h->dd) plan = h->staged ? 7 : 6;
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
     if (multistart && h->storage == 3)
         if (kern_t k2 = multistart_kernel(symm, packed, plan, two_opt)) return k2;
@@ -130,7 +160,10 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
                             unsigned smem_target = 0)
 {
     const int nb = h->nb, dw = (nb + 31) / 32;
-    const int threads = dsm ? toff : toff + 32 * dw;
+    const int dd = dsm == 2;  // diagonal blocks paired in registers: no dedicated warps, toff counts every thread
+    if (dd) dsm = 0;
+    if (dd && !(ur == 1 && us == 0 && toff >= h->noff + (nb + 1) / 2)) return false;
+    const int threads = (dsm || dd) ? toff : toff + 32 * dw;
     if (dsm && !(ur == 2 && us > 0)) return false;  // the instantiated shape
     if (dsm && threads < nb) return false;
     if ((long long)(ur + us) * toff < h->noff) return false;
@@ -150,10 +183,11 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     if (us == 0 && h->fits_i16 && !getenv("QAPB_NO_STAGE")) {
         // stage while two CTAs per SM still fit
         HybLayout Ls = make_hyb_layout(h->npad, nb, toff, us, exp_in_smem, 1, h->symmetric, dsm);
-        if (Ls.total <= std::min(smem_cap, (dsm ? 74u : 110u) * 1024u)) { staged = 1; L = Ls; }
+        if (Ls.total <= std::min(smem_cap, ((dsm || dd) ? 74u : 110u) * 1024u)) { staged = 1; L = Ls; }
     }
     h->staged = staged;
     h->dsm = dsm;
+    h->dd = dd;
     h->upt = ur; h->toff = toff; h->us = us; h->exp_in_smem = exp_in_smem;
     h->threads = threads;
     h->lb_class = 0;
@@ -175,7 +209,7 @@ static int hybrid_occupancy(const qapb_handle *h)
             if (e.k == k && e.threads == h->threads && e.smem == h->smem_bytes && e.device == h->device) return e.occ;
     }
     int occ = 0;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes) != cudaSuccess ||
+    if (ensure_smem_optin(k, h->device, h->smem_bytes) != cudaSuccess ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, h->threads, h->smem_bytes) != cudaSuccess) {
         cudaGetLastError();
         return 0;
@@ -218,6 +252,11 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
         return try_hybrid_plan(h, smem_cap, 2, toff, us);
     }
     const int t1 = (noff + 31) / 32 * 32, t2 = ((noff + 1) / 2 + 31) / 32 * 32;
+    const int td = (noff + (nb + 1) / 2 + 31) / 32 * 32;
+    // paired diagonal blocks (three searches per SM at n = 100) are a candidate plan, not the default: the
+    // warp that carries them runs an off-diagonal pass AND two diagonal passes, and the other warps wait
+    // for it at barrier 1 (580 against 800 G evals/s at n = 100)
+    if (getenv("QAPB_DD") && try_hybrid_plan(h, smem_cap, 1, td, 0, 2)) return true;
     if (!try_hybrid_plan(h, smem_cap, 1, t1, 0)) return false;
     if (hybrid_occupancy(h) >= 2 || t2 < 32) return true;
     const qapb_handle one = *h;
@@ -242,6 +281,7 @@ static std::vector<std::array<int, 4>> hybrid_candidates(const qapb_handle *h)
         const int toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
         add(2, toff, std::max(0, (noff - 2 * toff + toff - 1) / toff), 0);
     } else {
+        add(1, (noff + (nb + 1) / 2 + 31) / 32 * 32, 0, 2);
         add(1, (noff + 31) / 32 * 32, 0, 0);
         add(2, ((noff + 1) / 2 + 31) / 32 * 32, 0, 0);
     }
@@ -322,12 +362,35 @@ DevAttr g_attr[64];
 }  // namespace
 int g_attr_smem(int device) { return g_attr[device & 63].smem_optin; }
 
+// Opt-in dynamic shared memory of a kernel instantiation: several handles (and host threads) share one
+// instantiation, so the attribute only ever grows -- set to the maximum requested so far, under a mutex.
+static cudaError_t ensure_smem_optin(const void *kern, int device, unsigned bytes)
+{
+    struct Key { const void *k; int device; unsigned bytes; };
+    static std::mutex mu;
+    static std::vector<Key> seen;
+    std::lock_guard<std::mutex> lk(mu);
+    for (Key &e : seen)
+        if (e.k == kern && e.device == device) {
+            if (e.bytes >= bytes) return cudaSuccess;
+            cudaError_t rc = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+            if (rc == cudaSuccess) e.bytes = bytes;
+            return rc;
+        }
+    cudaError_t rc = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (rc == cudaSuccess) seen.push_back({kern, device, bytes});
+    return rc;
+}
+
 static int ensure_ws(qapb_handle *h, size_t bytes)
 {
     if (bytes <= h->ws_bytes) return QAPB_OK;
+    // launches of this handle that are still in flight write the old workspace: wait before recycling it
+    if (h->have_timing) CU(cudaEventSynchronize(h->ev1));
     pool_free(h->device, h->ws, h->ws_bytes);
     h->ws = nullptr;
     h->ws_bytes = 0;
+    h->steps_total_off = (size_t)-1;
     size_t want = bytes + bytes / 4 + 4096, got = 0;
     h->ws = pool_alloc(h->device, want, &got);
     if (!h->ws) return fail(QAPB_ERR_NOMEM, "workspace allocation of " + std::to_string(want) + " bytes failed");
@@ -384,6 +447,63 @@ static double placement_bound(int n, const std::vector<long long> &F0, const std
             best = std::max(best, s);
         }
     return best + extra;
+}
+
+// Unit table of a handle: entry uid = I | J << 8 for the off-diagonal units (uid < noff), then the nb diagonal
+// blocks.  The generic kernel addresses units by formula (locate()), so its table is lexicographic.  The
+// hybrid kernel is table-driven, and there the order decides which WARPS touch block row/column R or S of a
+// move: the 4n entries on those rows/columns are fixed in divergent regions that a warp executes when any of
+// its units touches the block, and in lexicographic order nearly every warp does (a warp spans one or two
+// block rows I and all the columns J > I).  Greedy clustering -- grow a vertex set of the complete graph on
+// the blocks, taking each time the block with the most unassigned edges into the set -- gives every warp a
+// near-clique: n = 100 (25 blocks, 10 warps) 4.4 warps per block instead of ~9.
+static void fill_unit_table(const qapb_handle *h, uint16_t *units)
+{
+    const int nb = h->nb, noff = h->noff;
+    int u = 0;
+    const bool clustered = h->storage == 3 && !getenv("QAPB_NO_CLUSTER");
+    if (!clustered) {
+        for (int I = 0; I < nb; ++I)
+            for (int J = I + 1; J < nb; ++J) units[u++] = (uint16_t)(I | (J << 8));
+    } else {
+        // slots of warp w: uid = k * toff + 32 w + lane for every unit slot k of a thread (registers, then
+        // shared memory); its capacity = the slots below noff
+        const int toff = std::max(32, h->toff), K = std::max(1, h->upt + h->us), W = toff / 32;
+        std::vector<char> rem((size_t)nb * nb, 0);
+        std::vector<int> deg(nb, nb - 1);
+        for (int I = 0; I < nb; ++I)
+            for (int J = 0; J < nb; ++J) rem[(size_t)I * nb + J] = I != J;
+        for (int q = 0; q < noff; ++q) units[q] = 0xffffu;
+        for (int w = 0; w < W; ++w) {
+            std::vector<int> slots;
+            for (int k = 0; k < K; ++k)
+                for (int l = 0; l < 32; ++l)
+                    if (k * toff + 32 * w + l < noff) slots.push_back(k * toff + 32 * w + l);
+            std::vector<int> S;
+            size_t used = 0;
+            while (used < slots.size()) {
+                int best = -1, binto = -1, bdeg = -1;
+                for (int v = 0; v < nb; ++v) {
+                    if (deg[v] == 0 || std::find(S.begin(), S.end(), v) != S.end()) continue;
+                    int into = 0;
+                    for (int x : S) into += rem[(size_t)v * nb + x];
+                    if (into > binto || (into == binto && deg[v] > bdeg)) { best = v; binto = into; bdeg = deg[v]; }
+                }
+                if (best < 0) break;
+                for (int x : S) {
+                    if (used >= slots.size()) break;
+                    if (!rem[(size_t)best * nb + x]) continue;
+                    rem[(size_t)best * nb + x] = rem[(size_t)x * nb + best] = 0;
+                    --deg[best]; --deg[x];
+                    const int I = std::min(best, x), J = std::max(best, x);
+                    units[slots[used++]] = (uint16_t)(I | (J << 8));
+                }
+                S.push_back(best);
+            }
+        }
+        u = noff;
+    }
+    for (int I = 0; I < nb; ++I) units[u++] = (uint16_t)(I | (I << 8));
 }
 
 extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int device, qapb_handle **out)
@@ -516,10 +636,7 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
                     pDT[(size_t)j * npad + i] = d;
                 }
             }
-            int u = 0;
-            for (int I = 0; I < nb; ++I)
-                for (int J = I + 1; J < nb; ++J) units[u++] = (uint16_t)(I | (J << 8));
-            for (int I = 0; I < nb; ++I) units[u++] = (uint16_t)(I | (I << 8));
+            fill_unit_table(h, units);
             e = cudaMemcpy(h->arena, g_stage, total, cudaMemcpyHostToDevice);
         }
     }
@@ -533,7 +650,7 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
     kern_t kern = handle_kernel(h);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
+    if (e == cudaSuccess) e = ensure_smem_optin((const void *)kern, device, h->smem_bytes);
     if (e != cudaSuccess) {
         std::string msg = std::string("instance upload failed: ") + cudaGetErrorString(e);
         qapb_destroy(h);
@@ -563,7 +680,7 @@ extern "C" int qapb_get_info(const qapb_handle *h, qapb_info *info)
     if (h->ctas_per_sm == 0) {
         qapb_handle *hm = const_cast<qapb_handle *>(h);
         cudaSetDevice(h->device);
-        cudaFuncSetAttribute((const void *)handle_kernel(h), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
+        ensure_smem_optin((const void *)handle_kernel(h), h->device, h->smem_bytes);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hm->ctas_per_sm, (const void *)handle_kernel(h), h->threads, h->smem_bytes);
     }
     info->n = h->n; info->device = h->device; info->acc_bits = h->acc_bits; info->symmetric = h->symmetric;
@@ -680,8 +797,8 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
         P.lay = make_layout(h->npad, h->nunits, h->threads, h->upt, h->acc_bits / 8, h->storage);
         P.inv_t = (unsigned)(((1ULL << 32) + (unsigned)h->threads - 1) / (unsigned)h->threads);
     }
-    // several handles share one kernel instantiation: (re)assert this launch's opt-in size
-    CU(cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes));
+    // several handles share one kernel instantiation: its opt-in size is the maximum requested so far
+    CU(ensure_smem_optin((const void *)kern, h->device, h->smem_bytes));
     CU(cudaEventRecord(h->ev0, st));
     // start permutations (+ stream state), then M and h as one batched tiled integer product
     BuildParams BP;
@@ -712,6 +829,8 @@ extern "C" int qapb_full_cost(qapb_handle *h, const int64_t *perms, int batch, i
     qap_full_cost_kernel<<<batch, 256, h->npad * sizeof(int32_t), (cudaStream_t)stream>>>(
         h->n, h->npad, h->dF, h->dD, h->dfd, h->ddd, perms, costs);
     CU(cudaGetLastError());
+    CU(cudaEventRecord(h->ev1, (cudaStream_t)stream));  // qapb_destroy waits for it before recycling the arena
+    if (!h->have_timing) { CU(cudaEventRecord(h->ev0, (cudaStream_t)stream)); h->have_timing = 1; }
     return QAPB_OK;
 }
 
@@ -796,9 +915,9 @@ extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, u
         return fail(QAPB_ERR_UNSUPPORTED, "iterations + tenure must fit int32");
     if (!per_start_costs || !best_key || !best_perm) return fail(QAPB_ERR_INVALID, "NULL buffer");
     const int n = h->n;
-    // workspace head: best perms [count,n], cur perms [count,n], cur costs [count]
+    // workspace head: best perms [count,n], cur perms [count,n], cur costs [count], steps [count], total steps [1]
     const size_t perm_bytes = (size_t)count * n * sizeof(int64_t);
-    const size_t head = 2 * perm_bytes + (size_t)count * sizeof(int64_t);
+    const size_t head = 2 * perm_bytes + 2 * (size_t)count * sizeof(int64_t) + 16;
     SearchParams P;
     base_params(h, P);
     P.mode = algo == QAPB_ALGO_TABU ? MODE_TABU : MODE_TWO_OPT;
@@ -814,10 +933,14 @@ extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, u
     int64_t *w_best = (int64_t *)h->ws;
     int64_t *w_cur = (int64_t *)((char *)h->ws + perm_bytes);
     int64_t *w_curcost = (int64_t *)((char *)h->ws + 2 * perm_bytes);
+    int64_t *w_steps = w_curcost + count;
     P.best = w_best; P.best_cost = per_start_costs; P.cur = w_cur; P.cur_cost = w_curcost;
+    P.steps = w_steps;
     rc = launch_search(h, P, count, head, (cudaStream_t)stream);
     if (rc) return rc;
-    qap_pick_best_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(count, n, first_index, per_start_costs, w_best, best_key, best_perm);
+    h->steps_total_off = (size_t)((char *)(w_steps + count) - (char *)h->ws);
+    qap_pick_best_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(count, n, first_index, per_start_costs, w_best, best_key, best_perm,
+                                                               w_steps, w_steps + count);
     CU(cudaGetLastError());
     CU(cudaEventRecord(h->ev1, (cudaStream_t)stream));
     return QAPB_OK;
@@ -898,7 +1021,7 @@ extern "C" int qapb_plan_candidates(qapb_handle *h, int32_t *plans, int cap, int
     if (h->storage != 3) return QAPB_OK;  // generic kernel: one configuration
     qapb_handle probe = *h;               // try each candidate on a copy (no device state is touched)
     for (const auto &c : hybrid_candidates(h)) {
-        const unsigned target = (c[3] && c[1] <= 256) ? 113u * 1024u : 0u;
+        const unsigned target = (c[3] == 1 && c[1] <= 256) ? 113u * 1024u : 0u;
         if (!try_hybrid_plan(&probe, device_smem_cap(h->device), c[0], c[1], c[2], c[3], target)) continue;
         if (*count < cap)
             for (int q = 0; q < 4; ++q) plans[*count * 4 + q] = c[q];
@@ -914,13 +1037,26 @@ extern "C" int qapb_set_plan(qapb_handle *h, int reg_units, int unit_threads, in
     CU(cudaSetDevice(h->device));
     if (h->have_timing) CU(cudaEventSynchronize(h->ev1));  // no launch of the old plan in flight
     qapb_handle probe = *h;
-    const unsigned target = (diag_in_smem && unit_threads <= 256) ? 113u * 1024u : 0u;
+    const unsigned target = (diag_in_smem == 1 && unit_threads <= 256) ? 113u * 1024u : 0u;
     if ((reg_units != 1 && reg_units != 2) || unit_threads < 0 || unit_threads % 32 != 0 || smem_units < 0 ||
-        !try_hybrid_plan(&probe, device_smem_cap(h->device), reg_units, unit_threads, smem_units, diag_in_smem ? 1 : 0, target))
+        !try_hybrid_plan(&probe, device_smem_cap(h->device), reg_units, unit_threads, smem_units, diag_in_smem, target))
         return fail(QAPB_ERR_INVALID, "plan {" + std::to_string(reg_units) + ", " + std::to_string(unit_threads) + ", " +
                                           std::to_string(smem_units) + ", " + std::to_string(diag_in_smem) + "} does not fit this instance");
     probe.ctas_per_sm = 0;  // re-queried by qapb_get_info
     *h = probe;
+    std::vector<uint16_t> units(h->nunits);  // the unit order follows the plan
+    fill_unit_table(h, units.data());
+    CU(cudaMemcpy(h->dunit, units.data(), units.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    return QAPB_OK;
+}
+
+extern "C" int qapb_last_total_steps(qapb_handle *h, int64_t *steps)
+{
+    if (!h || !steps) return fail(QAPB_ERR_INVALID, "NULL argument");
+    if (h->steps_total_off == (size_t)-1 || !h->ws) return fail(QAPB_ERR_INVALID, "no multistart recorded");
+    CU(cudaSetDevice(h->device));
+    CU(cudaEventSynchronize(h->ev1));
+    CU(cudaMemcpy(steps, (char *)h->ws + h->steps_total_off, sizeof(int64_t), cudaMemcpyDeviceToHost));
     return QAPB_OK;
 }
 
@@ -1115,6 +1251,32 @@ extern "C" int qapb_multistart_trace_host(qapb_handle *h, int algo, const uint64
     D2H(move_i, d + 3 * cb + pb, tb);
     D2H(move_j, d + 3 * cb + pb + tb, tb);
     D2H(move_delta, d + 3 * cb + pb + 2 * tb, tb);
+    return QAPB_OK;
+}
+
+extern "C" int qapb_probe_smem_peak(int device, double *bytes_per_sec)
+{
+    if (!bytes_per_sec) return fail(QAPB_ERR_INVALID, "bad argument");
+    CU(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    DevBuf sink;
+    CU(sink.alloc(4));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    const int iters = 4000, threads = 1024, blocks = prop.multiProcessorCount * 2;
+    qap_smem_probe_kernel<<<blocks, threads>>>(100, sink.as<int>());
+    CU(cudaDeviceSynchronize());
+    CU(cudaEventRecord(e0));
+    qap_smem_probe_kernel<<<blocks, threads>>>(iters, sink.as<int>());
+    CU(cudaEventRecord(e1));
+    CU(cudaEventSynchronize(e1));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *bytes_per_sec = (double)iters * 8.0 * 16.0 * threads * blocks / (ms * 1e-3);
     return QAPB_OK;
 }
 

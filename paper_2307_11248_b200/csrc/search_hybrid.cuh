@@ -385,10 +385,15 @@ __device__ __forceinline__ void expire_bits(unsigned &tb, int32_t &mexp, int c, 
 // and stores the combined vector (P.symmetric: 2 = distance symmetric, 3 = flow symmetric).
 // REC: the run may record a trail / the tabu memory `cells` (the single-run entries); the multi-start
 // entries never do, and their instantiations leave that code out of the winner's serial chain.
+// DD: no dedicated diagonal warps -- the nb diagonal blocks ride, two per thread (one in U, one in L:
+// the register footprint of one off-diagonal unit), in the threads that follow the last off-diagonal
+// unit.  n = 100: 300 + 13 threads = 10 warps instead of 11, which at 64 registers is what lets THREE
+// searches share an SM.
 template <int SYMM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG, bool DSM = false, bool NOTABU = false,
-          bool REC = true>
+          bool REC = true, bool DD = false>
 __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams P)
 {
+    static_assert(!DD || (UR == 1 && !SMEMU && !DSM), "paired diagonal blocks: one register unit per thread");
     constexpr bool SYM = SYMM != 0;       // single-product pass
     constexpr bool FULLSYM = SYMM == 1;   // symmetric closed forms in the publish phase, no transposes
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -491,7 +496,10 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     const bool offt = tid < Toff;
     // diagonal blocks: one per thread of the last warps in registers, or (DSM) in shared memory, owned by
     // the last nb threads of the CTA in addition to their off-diagonal units
-    const bool diag = !DSM && tid >= Toff && (tid - Toff) < nb;
+    const bool diag = !DSM && !DD && tid >= Toff && (tid - Toff) < nb;
+    // DD: thread noff + q carries diagonal blocks 2q (in U) and 2q + 1 (in L; absent when 2q + 1 == nb)
+    // (I[0], J[0] = the two blocks, J[0] = -1 for an absent one; own[0] tells a carrier from an idle thread)
+    const bool ddiag = DD && tid >= noff;
     const bool dsm_owner = DSM && tid >= T - nb;
     const int dsmI = T - 1 - tid;  // diagonal block of a DSM owner
     int32_t *sDG = reinterpret_cast<int32_t *>(smem_raw + lay.offDG);              // [nb][16]
@@ -510,7 +518,28 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         I[k] = 0; J[k] = 0; uidv[k] = 0; tb[k] = 0xffffu; mexp[k] = MAXV;
         if (own[k]) { I[k] = P.unit_ij[uid] & 0xff; J[k] = P.unit_ij[uid] >> 8; uidv[k] = uid; }
         if (k == 0 && diag) { I[0] = tid - Toff; J[0] = I[0]; uidv[0] = noff + I[0]; own[0] = true; }
-        if (own[k]) {
+        if (DD && k == 0 && ddiag && 2 * (tid - noff) < nb) {
+            int32_t tmp[4][4];
+            unsigned deadA, deadB = 0xffffu;
+            const int ddA = 2 * (tid - noff), ddB = ddA + 1 < nb ? ddA + 1 : -1;
+            I[0] = ddA; J[0] = ddB; uidv[0] = noff + ddA; own[0] = true;
+            load_unit(Minit, npad, n, ddA, ddA, U[0], tmp, deadA, PACKED ? (1 << 25) : (1 << 29));
+            deadA |= 0xF731u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) L[0][u][v] = 0;
+            if (ddB >= 0) {
+                load_unit(Minit, npad, n, ddB, ddB, L[0], tmp, deadB, PACKED ? (1 << 25) : (1 << 29));
+                deadB |= 0xF731u;
+            }
+            tb[0] = deadA | (deadB << 16);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                xp[(noff + ddA) * 16 + q] = ((deadA >> q) & 1u) ? MAXV : 0;
+                if (ddB >= 0) xp[(noff + ddB) * 16 + q] = ((deadB >> q) & 1u) ? MAXV : 0;
+            }
+        } else if (own[k]) {
             unsigned dead;
             load_unit(Minit, npad, n, I[k], J[k], U[k], L[k], dead, PACKED ? (1 << 25) : (1 << 29));
             if (diag) dead |= 0xF731u;  // slots with u >= v are not pairs of a diagonal block
@@ -598,7 +627,23 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             if (!own[k]) continue;
             int32_t dk;
             int sk;
-            if (I[k] != J[k]) {
+            if (DD && ddiag) {
+                // two diagonal blocks: U = block I (tabu bits 0..15), L = block J (bits 16..31)
+                if (R >= 0) diag_update<SYM>(U[k], I[k], R, S, ru, su, V);
+                diag_select(U[k], tb[k] & 0xffffu, I[k], thr, V.H, dk, sk);
+                if (dk != MAXV) {
+                    my_d = dk; my_key = pair_key(4 * I[k] + (sk >> 2), 4 * I[k] + (sk & 3), 0); my_slot = sk;
+                }
+                if (J[k] >= 0) {
+                    if (R >= 0) diag_update<SYM>(L[k], J[k], R, S, ru, su, V);
+                    diag_select(L[k], tb[k] >> 16, J[k], thr, V.H, dk, sk);
+                    if (dk < my_d) {  // block J comes later in (i, j) order: strict
+                        my_d = dk; my_key = pair_key(4 * J[k] + (sk >> 2), 4 * J[k] + (sk & 3), 0); my_slot = 16 + sk;
+                    }
+                }
+                continue;
+            }
+            if (DD || I[k] != J[k]) {
                 if (R >= 0) unit_update<SYM>(U[k], L[k], I[k], J[k], R, S, ru, su, V);
                 unit_select<PACKED, NOTABU>(U[k], L[k], tb[k], I[k], J[k], thr, V, one, sixteen, dk, sk);
             } else {
@@ -690,7 +735,23 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         for (int k = 0; k < UR; ++k) {
             if (!own[k]) continue;
             const int Ik = I[k], Jk = J[k];
-            if (Ik != Jk) {
+            if (DD && ddiag) {
+                const int ddA = Ik, ddB = Jk;
+                if (ddA == R) {
+                    QAPB_SWITCH4(ru, { st_vec4(V.ColR, ddA, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
+                }
+                if (ddA == S) {
+                    QAPB_SWITCH4(su, { st_vec4(V.ColS, ddA, q == 0 ? 0 : U[k][0][q], q == 1 ? 0 : U[k][1][q], q == 2 ? 0 : U[k][2][q], q == 3 ? 0 : U[k][3][q]); })
+                }
+                if (ddB == R) {
+                    QAPB_SWITCH4(ru, { st_vec4(V.ColR, ddB, q == 0 ? 0 : L[k][0][q], q == 1 ? 0 : L[k][1][q], q == 2 ? 0 : L[k][2][q], q == 3 ? 0 : L[k][3][q]); })
+                }
+                if (ddB == S) {
+                    QAPB_SWITCH4(su, { st_vec4(V.ColS, ddB, q == 0 ? 0 : L[k][0][q], q == 1 ? 0 : L[k][1][q], q == 2 ? 0 : L[k][2][q], q == 3 ? 0 : L[k][3][q]); })
+                }
+                continue;
+            }
+            if (DD || Ik != Jk) {
                 // ONE uniform 16-way switch on (r & 3, s & 3) (a jump table: one indirect branch on the serial
                 // path instead of two two-level trees), per-thread predicated 128-bit stores inside
 #define QAPB_DUMP(a, b)                                                                                    \
@@ -818,6 +879,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                     if (tabu) {
                         tb[k] |= 1u << my_slot;
                         mexp[k] = min(mexp[k], new_exp);
+                        // (DD: slots 16..31 are the second diagonal block of this thread, the next row of xp)
                         xp[uidv[k] * 16 + my_slot] = new_exp;
                     }
                 }
@@ -859,7 +921,19 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         // shared-memory diagonal blocks publish their parts of columns r and s
 #pragma unroll
         for (int k = 0; k < UR; ++k)
-            if (own[k] && c + 1 >= mexp[k]) expire_bits(tb[k], mexp[k], c + 1, xp + uidv[k] * 16);
+            if (own[k] && c + 1 >= mexp[k]) {
+                if (DD && ddiag) {
+                    unsigned lo = tb[k] & 0xffffu, hi = tb[k] >> 16;
+                    int32_t ma, mb;
+                    expire_bits(lo, ma, c + 1, xp + uidv[k] * 16);
+                    if (J[k] >= 0) expire_bits(hi, mb, c + 1, xp + (uidv[k] + 1) * 16);
+                    else mb = MAXV;
+                    tb[k] = lo | (hi << 16);
+                    mexp[k] = min(ma, mb);
+                } else {
+                    expire_bits(tb[k], mexp[k], c + 1, xp + uidv[k] * 16);
+                }
+            }
         if (SMEMU && offt) {
 #pragma unroll 1
             for (int k2 = 0; k2 < US; ++k2) {

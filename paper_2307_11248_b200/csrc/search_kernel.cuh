@@ -658,9 +658,17 @@ __global__ void qap_full_cost_kernel(int n, int npad, const int32_t *__restrict_
 __global__ void qap_pick_best_kernel(int count, int n, unsigned long long first_index,
                                      const int64_t *__restrict__ costs,
                                      const int64_t *__restrict__ best_perms /* [count,n] */,
-                                     int64_t *__restrict__ best_key, int64_t *__restrict__ best_perm)
+                                     int64_t *__restrict__ best_key, int64_t *__restrict__ best_perm,
+                                     const int64_t *__restrict__ steps = nullptr, int64_t *__restrict__ total_steps = nullptr)
 {
     __shared__ long long sc[32];
+    __shared__ long long ssum[33];
+    if (total_steps) {  // sum of steps_done over the starts: evals = sum * n(n-1)/2 even when starts stop early
+        long long part = 0;
+        for (int k = threadIdx.x; k < count; k += blockDim.x) part += steps[k];
+        part = block_sum_i64(part, ssum, threadIdx.x, blockDim.x);
+        if (threadIdx.x == 0) *total_steps = part;
+    }
     __shared__ int si[32];
     __shared__ int winner;
     const int tid = threadIdx.x, T = blockDim.x;
@@ -695,6 +703,30 @@ __global__ void qap_pick_best_kernel(int count, int n, unsigned long long first_
     }
     __syncthreads();
     for (int i = tid; i < n; i += T) best_perm[i] = best_perms[(size_t)winner * n + i];
+}
+
+// ---- shared-memory bandwidth probe: conflict-free 128-bit loads, eight independent chains per thread ----
+__global__ void __launch_bounds__(1024) qap_smem_probe_kernel(int iters, int *sink)
+{
+    __shared__ int4 buf[1024 * 2];
+    for (int k = threadIdx.x; k < 2048; k += blockDim.x) buf[k] = make_int4(k, k + 1, k + 2, k + 3);
+    __syncthreads();
+    int4 acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = make_int4(0, 0, 0, 0);
+    int idx = threadIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int4 v = buf[(idx + 32 * q) & 2047];
+            acc[q].x += v.x; acc[q].y ^= v.y; acc[q].z += v.z; acc[q].w ^= v.w;
+        }
+        idx = (idx + 256) & 2047;
+    }
+    int t = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t ^= acc[q].x ^ acc[q].y ^ acc[q].z ^ acc[q].w;
+    if (t == 0x12345678) *sink = 1;
 }
 
 // ---- integer-pipe peak probe -----------------------------------------------

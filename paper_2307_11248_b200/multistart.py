@@ -33,6 +33,7 @@ from .two_opt import run_two_opt
 
 ALGORITHMS = ("2opt", "tabu")
 _I64_MAX = np.iinfo(np.int64).max
+_I64_MIN = np.iinfo(np.int64).min  # in-band "this rank failed" marker of the min-reduction
 
 
 @dataclass(frozen=True)
@@ -164,27 +165,56 @@ def run_multistart(inst: Instance, cfg: SearchConfig, *, group=None, _shard_runn
 
     t0 = time.perf_counter()
     world, rank = 1, 0
-    if dist.is_available() and dist.is_initialized():
+    grouped = dist.is_available() and dist.is_initialized()
+    if grouped:
         world, rank = dist.get_world_size(group), dist.get_rank(group)
+    # a one-rank group normally skips the collectives; QAPB_FORCE_COLLECTIVE=1 takes them anyway (how the
+    # NCCL branch is exercised on a single-GPU box)
+    collective = world > 1 or (grouped and os.environ.get("QAPB_FORCE_COLLECTIVE") == "1")
     lo, hi = shard_bounds(cfg.n_starts, world, rank)
     runner = _shard_runner or _cuda_shard_runner
-    costs, key, perm = runner(inst, cfg, lo, hi - lo)
+    failure = None
+    if not collective:
+        costs, key, perm = runner(inst, cfg, lo, hi - lo)
+    else:
+        # The reference discards partial results when a worker fails (multistart.py:151-154: QapError).  Here a
+        # rank-local failure must not leave the other ranks waiting in the all-reduce: the failing rank still
+        # takes part, contributing the smallest int64 -- the min-reduction hands it to everyone and every rank
+        # raises QapError.  (A CUDA fault that poisons the context also breaks NCCL on that rank; then the
+        # others fail at the process group's timeout.)
+        try:
+            costs, key, perm = runner(inst, cfg, lo, hi - lo)
+            if costs.is_cuda:
+                torch.cuda.current_stream(costs.device).synchronize()  # surface asynchronous launch errors here
+        except Exception as exc:  # noqa: BLE001 -- any failure of this rank's shard
+            failure = exc
+            dev = (torch.device("cuda", torch.cuda.current_device())
+                   if _shard_runner is None and torch.cuda.is_available() else torch.device("cpu"))
+            costs = torch.full((hi - lo,), _I64_MAX, dtype=torch.int64, device=dev)
+            key = torch.full((2,), _I64_MIN, dtype=torch.int64, device=dev)
+            perm = torch.zeros(inst.n, dtype=torch.int64, device=dev)
 
-    if world > 1:
+    if collective:
         bits = _index_bits(cfg.n_starts)
         if _packable(inst, cfg.n_starts):
-            empty = key[0] == _I64_MAX
-            packed = torch.where(empty, key[0], (key[0] << bits) | key[1]).reshape(1)
+            special = (key[0] == _I64_MAX) | (key[0] == _I64_MIN)  # empty shard / failed rank
+            packed = torch.where(special, key[0], (key[0] << bits) | key[1]).reshape(1)
             dist.all_reduce(packed, op=dist.ReduceOp.MIN, group=group)  # the one data-path collective
-            best_cost = int(packed.item()) >> bits
-            best_index = int(packed.item()) & ((1 << bits) - 1)
+            reduced = int(packed.item())
+            best_cost, best_index = reduced >> bits, reduced & ((1 << bits) - 1)
+            failed = reduced == _I64_MIN
         else:  # costs may be negative / huge: two-step lexicographic min
             c = key[0:1].clone()
             dist.all_reduce(c, op=dist.ReduceOp.MIN, group=group)
+            failed = int(c.item()) == _I64_MIN  # (a true cost of -2^63 is impossible: |cost| <= n^2 2^60)
             mine = key[1:2] if int(key[0].item()) == int(c.item()) else torch.full_like(key[1:2], _I64_MAX)
             mine = mine.clone()
             dist.all_reduce(mine, op=dist.ReduceOp.MIN, group=group)
             best_cost, best_index = int(c.item()), int(mine.item())
+        if failed:
+            if failure is not None:
+                raise QapError(f"multi-start shard [{lo}, {hi}) failed on rank {rank}: {failure}") from failure
+            raise QapError("multi-start failed on another rank; partial results discarded")
         owner = next(r for r in range(world) if shard_bounds(cfg.n_starts, world, r)[0] <= best_index
                      < shard_bounds(cfg.n_starts, world, r)[1])
         src = owner if group is None else dist.get_global_rank(group, owner)

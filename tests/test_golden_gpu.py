@@ -31,7 +31,10 @@ def _instance(g):
 
 
 @pytest.mark.parametrize("name", ["cfg0_nug12_2opt", "cfg0_nug12_tabu", "cfg1_tai30a_tabu", "cfg1_rand30_tabu",
-                                  "cfg2_tai100a_single", "cfg3_tai256c_2opt", "cfg3_tai256c_tabu"])
+                                  "cfg2_tai100a_single", "cfg3_tai256c_2opt", "cfg3_tai256c_tabu",
+                                  # full length: the iteration counts bench.py times, from the reference's kernel
+                                  "full_cfg2_tai100a_tabu", "full_cfg4_tai150b_tabu", "full_cfg4_sko100_tabu",
+                                  "full_cfg3_tai256c_2opt", "full_cfg3_tai256c_tabu"])
 def test_single_start_trajectories(q, name):
     """Drivers run_two_opt / run_tabu (host RNG -> kernel) against the reference's per-iteration
     trajectory: moves, deltas, tabu flags, tenures, final tabu matrix, best permutation."""
@@ -60,7 +63,7 @@ def test_single_start_trajectories(q, name):
 
 
 @pytest.mark.parametrize("name", ["kat30_multi_tabu", "kat30_multi_2opt", "cfg2_tai100a_multi", "cfg4_sko100_multi",
-                                  "cfg4_tai150b_multi", "cfg4_tai150b_2opt_multi"])
+                                  "cfg4_tai150b_multi", "cfg4_tai150b_2opt_multi", "full_cfg4_tai150b_multi6"])
 def test_multistart_results(q, name):
     g = golden(name)
     inst = _instance(g)

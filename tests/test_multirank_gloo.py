@@ -100,3 +100,65 @@ def test_single_process_path_with_runner(built):
     costs, bc, bi, _ = oracle.multistart(inst.flow, inst.distance, "tabu", 5, 24, 30)
     assert np.array_equal(res.per_start_costs, costs) and (res.best.cost, res.best_start_index) == (bc, bi)
     assert q.evaluate_cost(inst, res.best.permutation) == res.best.cost
+
+
+def _failing_worker(rank, world, port, out_dir):
+    """Rank 1's shard raises; every rank must come back with QapError instead of hanging in the all-reduce
+    (the analogue of the reference's pool-failure rule, multistart.py:151-154)."""
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2307_11248_b200 as q
+
+    def runner(inst, cfg, first_index, count):
+        if rank == 1:
+            raise RuntimeError("injected shard failure")
+        return _oracle_runner(inst, cfg, first_index, count)
+
+    try:
+        for k, (inst, cfg) in enumerate(_cases()[:3]):  # packed and two-step reductions
+            try:
+                q.run_multistart(inst, cfg, _shard_runner=runner)
+                outcome = "returned"
+            except q.QapError as exc:
+                outcome = "QapError: " + str(exc)
+            with open(os.path.join(out_dir, f"fail_r{rank}_c{k}.txt"), "w") as fh:
+                fh.write(outcome)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rank_failure_raises_on_every_rank(tmp_path, built):
+    world = 3
+    mp.spawn(_failing_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for k in range(3):
+        for rank in range(world):
+            text = open(os.path.join(tmp_path, f"fail_r{rank}_c{k}.txt")).read()
+            assert text.startswith("QapError"), (k, rank, text)
+            assert ("injected shard failure" in text) == (rank == 1)
+
+
+def _forced_collective_worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), QAPB_FORCE_COLLECTIVE="1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2307_11248_b200 as q
+
+    try:
+        inst, cfg = _cases()[0]
+        res = q.run_multistart(inst, cfg, _shard_runner=_oracle_runner)
+        np.savez(os.path.join(out_dir, "forced.npz"), costs=res.per_start_costs, cost=res.best.cost, index=res.best_start_index)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_one_rank_group_takes_the_collective_path_when_forced(tmp_path, built):
+    """QAPB_FORCE_COLLECTIVE=1: a one-rank group runs the all-reduce / broadcast / all-gather branch
+    (the -m gpu suite uses this to execute the NCCL branch on a single-GPU box)."""
+    import oracle
+
+    mp.spawn(_forced_collective_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
+    inst, cfg = _cases()[0]
+    costs, bc, bi, _ = oracle.multistart(inst.flow, inst.distance, "tabu", 5, 24, 30)
+    got = np.load(os.path.join(tmp_path, "forced.npz"))
+    assert np.array_equal(got["costs"], costs) and (int(got["cost"]), int(got["index"])) == (bc, bi)

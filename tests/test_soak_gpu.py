@@ -1,0 +1,95 @@
+"""Differential soak inside the driver-run suite: GPU vs the C oracle on random instances at the sizes
+whose launch plans keep part of a search in shared memory / L2 (n = 129 .. 256) and at the small sizes,
+with SHORT tenures ([1, 3]) and enough iterations that tabu bits expire and re-arm many times on every
+plan's expiry path (register units, shared-memory units, shared-memory diagonal blocks, L2 expiries).
+Every launch plan of each instance must reproduce the oracle bit for bit.  (tests/soak_gpu.py is the
+open-ended version of the same loop.)"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _instance(rs, n, kind, hi):
+    f = rs.integers(0, hi + 1, (n, n)).astype(np.int64)
+    d = rs.integers(0, hi + 1, (n, n)).astype(np.int64)
+    if kind in (1, 3):
+        d = d + d.T
+    if kind in (2, 3):
+        f = f + f.T
+    if kind != 0:
+        np.fill_diagonal(f, 0)
+        np.fill_diagonal(d, 0)
+    return f, d
+
+
+def _check_single(di, oracle, f, d, perm, iters, ten, tag):
+    g = di.tabu(perm, iters, ten)
+    w = oracle.tabu_run(f, d, perm, iters, ten)
+    assert np.array_equal(g[0][0], w[0]) and g[1][0] == w[1], tag
+    assert np.array_equal(g[2][0], w[2]) and g[3][0] == w[3], tag
+    assert np.array_equal(g[4][0], w[4]), tag                      # final tabu memory `cells`
+    assert bool(g[5][0]) == w[5] and g[6][0] == w[6], tag          # stopped_early, steps_done
+    for a in range(4):                                             # trail: i, j, delta, tabu flag
+        assert np.array_equal(g[7][a][0, : w[6]], w[7][a]), (tag, a)
+    return w
+
+
+@pytest.mark.parametrize("n,kind,hi", [(129, 3, 60), (160, 3, 99), (160, 1, 30), (200, 3, 99), (200, 0, 20),
+                                       (256, 3, 99), (256, 2, 12), (144, 3, 3000), (100, 3, 99), (100, 0, 99),
+                                       (64, 3, 99), (33, 1, 1000), (30, 3, 99), (12, 0, 50)])
+def test_short_tenures_every_plan(built, n, kind, hi):
+    import oracle
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    rs = np.random.default_rng(1000 * n + 10 * kind + 1)
+    f, d = _instance(rs, n, kind, hi)
+    iters = 64 if n > 128 else 150
+    rng = oracle.Rng(oracle.derive_seed(n, kind))
+    ten = rng.tenures(1, 3, iters)
+    di = DeviceInstance(f, d)
+    try:
+        # start next to a local optimum (the current permutation of a long 2opt run; any permutation is a valid
+        # input, the oracle checks the tabu run from it): the search then moves uphill, its reverse moves are
+        # tabu, expire after 1-3 iterations and are taken again -- every expiry path is hit many times
+        perm = di.two_opt(rng.permutation(n), 3 * n, moves=False)[2][0]
+        plans = di.plan_candidates() or [None]
+        want = None
+        for plan in plans:
+            if plan is not None:
+                di.set_plan(plan)
+            want = _check_single(di, oracle, f, d, perm, iters, ten, (n, kind, plan))
+        pairs = list(zip(want[7][0].tolist(), want[7][1].tolist()))
+        assert len(set(pairs)) < len(pairs), "no pair was ever taken twice: the case does not exercise expiry"
+        # batched device-RNG path with a short tenure interval: compare against single-start runs drawn on the host
+        for plan in plans[:2]:
+            if plan is not None:
+                di.set_plan(plan)
+            costs = di.multistart("tabu", 77, 0, 3, iters, 1, 3)[0]
+            for idx in range(3):
+                r2 = oracle.Rng(oracle.derive_seed(77, idx))
+                p2 = r2.permutation(n)
+                t2 = r2.tenures(1, 3, iters)
+                assert int(costs[idx]) == int(oracle.tabu_run(f, d, p2, iters, t2)[1]), (n, kind, plan, idx)
+    finally:
+        di.close()
+
+
+@pytest.mark.parametrize("n,hi", [(160, 99), (256, 40)])
+def test_two_opt_every_plan(built, n, hi):
+    import oracle
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    rs = np.random.default_rng(n)
+    f, d = _instance(rs, n, 3, hi)
+    perm = oracle.Rng(5).permutation(n)
+    w = oracle.two_opt_run(f, d, perm, 48)
+    di = DeviceInstance(f, d)
+    try:
+        for plan in di.plan_candidates() or [None]:
+            if plan is not None:
+                di.set_plan(plan)
+            g = di.two_opt(perm, 48)
+            assert all(np.array_equal(a[0], b) for a, b in zip(g, w)), (n, plan)
+    finally:
+        di.close()
