@@ -70,6 +70,8 @@ typedef void (*kern_t)(const SearchParams);
 #define QAPB_DEV_ARGS 1, true, 2, true, false, 128, true, false, false
 #elif QAPB_DEV_ONLY == 4 // preset 1 with paired diagonal blocks (DD), 64 registers
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 64, false, false, false, true
+#elif QAPB_DEV_ONLY == 7 // preset 1 at 56 registers (three 352-thread CTAs per SM)
+#define QAPB_DEV_ARGS 1, true, 1, false, true, 56, false, false, false
 #elif QAPB_DEV_ONLY == 6 // DD at 80 registers
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 80, false, false, false, true
 #elif QAPB_DEV_ONLY == 5 // recording instantiation of preset 4
@@ -1282,7 +1284,7 @@ extern "C" int qapb_probe_smem_peak(int device, double *bytes_per_sec)
 
 extern "C" int qapb_probe_int_peak(int device, int kind, double *ops_per_sec)
 {
-    if (!ops_per_sec || kind < 0 || kind > 2) return fail(QAPB_ERR_INVALID, "bad argument");
+    if (!ops_per_sec || kind < 0 || kind > 4) return fail(QAPB_ERR_INVALID, "bad argument");
     CU(cudaSetDevice(device));
     cudaDeviceProp prop;
     CU(cudaGetDeviceProperties(&prop, device));
@@ -1295,7 +1297,9 @@ extern "C" int qapb_probe_int_peak(int device, int kind, double *ops_per_sec)
     auto launch = [&](int it) {
         if (kind == 0) qap_int_probe_kernel<0><<<blocks, threads>>>(it, sink.as<int>(), 3);
         else if (kind == 1) qap_int_probe_kernel<1><<<blocks, threads>>>(it, sink.as<int>(), 3);
-        else qap_int_probe_kernel<2><<<blocks, threads>>>(it, sink.as<int>(), 3);
+        else if (kind == 2) qap_int_probe_kernel<2><<<blocks, threads>>>(it, sink.as<int>(), 3);
+        else if (kind == 3) qap_int_probe_kernel<3><<<blocks, threads>>>(it, sink.as<int>(), 3);
+        else qap_int_probe_kernel<4><<<blocks, threads>>>(it, sink.as<int>(), 3);
     };
     launch(200);
     CU(cudaDeviceSynchronize());
@@ -1307,7 +1311,7 @@ extern "C" int qapb_probe_int_peak(int device, int kind, double *ops_per_sec)
     CU(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    const double per_thread = (double)iters * 8.0 * (kind == 2 ? 8.0 : 4.0);
+    const double per_thread = (double)iters * 8.0 * (kind >= 2 ? 8.0 : 4.0);  // kinds 3, 4: four min + four xor
     *ops_per_sec = per_thread * threads * blocks / (ms * 1e-3);
     return QAPB_OK;
 }

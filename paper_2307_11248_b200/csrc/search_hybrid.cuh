@@ -281,7 +281,9 @@ __device__ __forceinline__ void unit_select(const int32_t (&U)[4][4], const int3
     }
 }
 
-// ---- diagonal block: update + fix-ups (column assignments first, then row increments) ----------
+// ---- diagonal block: update + fix-ups.  Per moved location: the column assignment, then the row increment
+// (x[.] is zero at r and s, so the two locations do not disturb each other's corner values) -- two divergent
+// regions per iteration instead of four: the pass of the diagonal warp is as long as an off-diagonal one.
 template <bool SYM>
 __device__ __forceinline__ void diag_update(int32_t (&U)[4][4], int Ik, int R, int S, int ru, int su, const Vecs &V)
 {
@@ -303,54 +305,61 @@ __device__ __forceinline__ void diag_update(int32_t (&U)[4][4], int Ik, int R, i
                 if (u != v) U[u][v] += aI[u] * bI[v] + cI[u] * eI[v];
     }
     if (Ik == R) {
-        int32_t cs[4], t[4];
-        ld_vec4(V.ColS, Ik, cs); ld_vec4(V.TR, Ik, t);
+        int32_t cs[4], t[4], x[4];
+        ld_vec4(V.ColS, Ik, cs); ld_vec4(V.TR, Ik, t); ld_vec4(V.XR, Ik, x);
         QAPB_SWITCH4(ru, {
 _Pragma("unroll")
             for (int u = 0; u < 4; ++u) if (u != q) U[u][q] = cs[u] + t[u];
-        })
-    }
-    if (Ik == S) {
-        int32_t cr[4], t[4];
-        ld_vec4(V.ColR, Ik, cr); ld_vec4(V.TS, Ik, t);
-        QAPB_SWITCH4(su, {
-_Pragma("unroll")
-            for (int u = 0; u < 4; ++u) if (u != q) U[u][q] = cr[u] + t[u];
-        })
-    }
-    if (Ik == R) {
-        int32_t x[4];
-        ld_vec4(V.XR, Ik, x);
-        QAPB_SWITCH4(ru, {
 _Pragma("unroll")
             for (int v = 0; v < 4; ++v) if (v != q) U[q][v] += x[v];
         })
     }
     if (Ik == S) {
-        int32_t x[4];
-        ld_vec4(V.XS, Ik, x);
+        int32_t cr[4], t[4], x[4];
+        ld_vec4(V.ColR, Ik, cr); ld_vec4(V.TS, Ik, t); ld_vec4(V.XS, Ik, x);
         QAPB_SWITCH4(su, {
+_Pragma("unroll")
+            for (int u = 0; u < 4; ++u) if (u != q) U[u][q] = cr[u] + t[u];
 _Pragma("unroll")
             for (int v = 0; v < 4; ++v) if (v != q) U[q][v] += x[v];
         })
     }
 }
 
-__device__ __forceinline__ void diag_select(const int32_t (&U)[4][4], unsigned tbk, int Ik, int32_t thr,
-                                            const int32_t *sH, int32_t &dbest, int &sbest)
+// The six pairs of a diagonal block.  PACKED: the keys of the off-diagonal units (16 delta + slot) in three
+// independent chains of admissible_min; else plain deltas in one compare-and-select chain.
+template <bool PACKED>
+__device__ __forceinline__ void diag_select(const int32_t (&U)[4][4], unsigned tbk, int Ik, int32_t thr, const Vecs &V,
+                                            int32_t &dbest, int &sbest)
 {
-    int32_t hI[4];
-    ld_vec4(sH, Ik, hI);
-    dbest = 0x7fffffff;
-    sbest = 0;
+    const int32_t MAXV = 0x7fffffff;
+    if (PACKED) {
+        int32_t hi[4], hj[4];
+        ld_vec4(V.HI, Ik, hi);
+        ld_vec4(V.HJ, Ik, hj);
+        const int32_t thr16 = max(thr, -(1 << 27)) * 16;
+        int32_t km[3] = {MAXV, MAXV, MAXV};
+#define QAPB_DPAIR(u, v, ch) admissible_min<(u) * 4 + (v)>(km[ch], (U[u][v] + U[v][u]) * 16 + (hi[u] + hj[v]), tbk, thr16);
+        QAPB_DPAIR(0, 1, 0) QAPB_DPAIR(0, 2, 1) QAPB_DPAIR(0, 3, 2)
+        QAPB_DPAIR(1, 2, 0) QAPB_DPAIR(1, 3, 1) QAPB_DPAIR(2, 3, 2)
+#undef QAPB_DPAIR
+        const int32_t m = min(min(km[0], km[1]), km[2]);
+        dbest = (m == MAXV) ? MAXV : (m >> 4);
+        sbest = m & 15;
+    } else {
+        int32_t hI[4];
+        ld_vec4(V.H, Ik, hI);
+        dbest = MAXV;
+        sbest = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int v = u + 1; v < 4; ++v) {
-            const int32_t d = U[u][v] + U[v][u] - hI[u] - hI[v];
-            const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
-            if (adm && d < dbest) { dbest = d; sbest = u * 4 + v; }
-        }
+            for (int v = u + 1; v < 4; ++v) {
+                const int32_t d = U[u][v] + U[v][u] - hI[u] - hI[v];
+                const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
+                if (adm && d < dbest) { dbest = d; sbest = u * 4 + v; }
+            }
+    }
 }
 
 // ---- tabu bits of a unit: clear the ones whose expiry has been reached ------------------------
@@ -630,13 +639,13 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             if (DD && ddiag) {
                 // two diagonal blocks: U = block I (tabu bits 0..15), L = block J (bits 16..31)
                 if (R >= 0) diag_update<SYM>(U[k], I[k], R, S, ru, su, V);
-                diag_select(U[k], tb[k] & 0xffffu, I[k], thr, V.H, dk, sk);
+                diag_select<PACKED>(U[k], tb[k] & 0xffffu, I[k], thr, V, dk, sk);
                 if (dk != MAXV) {
                     my_d = dk; my_key = pair_key(4 * I[k] + (sk >> 2), 4 * I[k] + (sk & 3), 0); my_slot = sk;
                 }
                 if (J[k] >= 0) {
                     if (R >= 0) diag_update<SYM>(L[k], J[k], R, S, ru, su, V);
-                    diag_select(L[k], tb[k] >> 16, J[k], thr, V.H, dk, sk);
+                    diag_select<PACKED>(L[k], tb[k] >> 16, J[k], thr, V, dk, sk);
                     if (dk < my_d) {  // block J comes later in (i, j) order: strict
                         my_d = dk; my_key = pair_key(4 * J[k] + (sk >> 2), 4 * J[k] + (sk & 3), 0); my_slot = 16 + sk;
                     }
@@ -648,7 +657,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 unit_select<PACKED, NOTABU>(U[k], L[k], tb[k], I[k], J[k], thr, V, one, sixteen, dk, sk);
             } else {
                 if (R >= 0) diag_update<SYM>(U[k], I[k], R, S, ru, su, V);
-                diag_select(U[k], tb[k], I[k], thr, V.H, dk, sk);
+                diag_select<PACKED>(U[k], tb[k], I[k], thr, V, dk, sk);
             }
             if (dk != MAXV) {
                 const unsigned key = pair_key(4 * I[k] + (sk >> 2), 4 * J[k] + (sk & 3), 0);
@@ -695,7 +704,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             }
             int32_t dk;
             int sk;
-            diag_select(Ud, sDGtb[dsmI], dsmI, thr, V.H, dk, sk);
+            diag_select<PACKED>(Ud, sDGtb[dsmI], dsmI, thr, V, dk, sk);
             if (dk != MAXV) {
                 const unsigned key = pair_key(4 * dsmI + (sk >> 2), 4 * dsmI + (sk & 3), 0);
                 if (dk < my_d || (dk == my_d && key < my_key)) { my_d = dk; my_key = key; my_which = WHICH_DIAG; my_slot = sk; }

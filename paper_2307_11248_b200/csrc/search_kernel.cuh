@@ -740,6 +740,15 @@ __global__ void qap_int_probe_kernel(int iters, int *sink, int seed)
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             if (KIND == 0 || KIND == 2) { x0 = x0 * m + a; x1 = x1 * m + a; x2 = x2 * m + a; x3 = x3 * m + a; }
+            if (KIND == 3) {  // DPX add-then-min (VIADDMNMX), four independent chains
+                y0 = __viaddmin_s32(x0, a, y0); y1 = __viaddmin_s32(x1, a, y1);
+                y2 = __viaddmin_s32(x2, a, y2); y3 = __viaddmin_s32(x3, a, y3);
+                x0 ^= y1; x1 ^= y2; x2 ^= y3; x3 ^= y0;
+            }
+            if (KIND == 4) {  // plain min (VIMNMX)
+                y0 = min(x0, y0); y1 = min(x1, y1); y2 = min(x2, y2); y3 = min(x3, y3);
+                x0 ^= y1; x1 ^= y2; x2 ^= y3; x3 ^= y0;
+            }
             if (KIND == 1 || KIND == 2) {
                 y0 = (y0 + a) + y1;
                 y1 = (y1 + a) + y2;
