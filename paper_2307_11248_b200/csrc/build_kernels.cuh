@@ -209,6 +209,92 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
         for (int i = n + tid; i < npad; i += NT) hb[i] = 0;
 }
 
+// The same contraction for npad <= 128 with the WHOLE problem of one permutation in one CTA: D^T (40 KB at
+// n = 100) and the gathered G[k][j] = F0[p_j][p_k] are staged in shared memory ONCE -- straight 128-bit row
+// copies and one gather per entry, instead of re-staging both per 52 x 52 tile and per 32-wide k-chunk with
+// two barriers each -- and every thread then runs all n k-steps on an 8 x 4 register tile: three 128-bit
+// shared loads feed 32 IMADs per step.  (Asymmetric instances make a second pass with D and F0[p_k][p_j].)
+template <typename acc_t>
+__global__ void __launch_bounds__(544) qap_build_m_whole_kernel(const BuildParams P)
+{
+    extern __shared__ __align__(16) unsigned char dyn[];
+    const int n = P.n, npad = P.npad, tid = threadIdx.x, NT = blockDim.x, b = blockIdx.x;
+    int32_t *sA = reinterpret_cast<int32_t *>(dyn);                 // [npad][npad] (+8 words of slack)
+    int32_t *sB = sA + (size_t)npad * npad + 8;                      // [npad][npad]
+    int32_t *sPerm = sB + (size_t)npad * npad + 8;                   // [npad]
+    const int32_t *perm = P.perm32 + (size_t)b * npad;
+    for (int i = tid; i < npad; i += NT) sPerm[i] = perm[i];
+    __syncthreads();
+    const int CG = npad >> 2;                                        // 4-column groups
+    const int rg = tid / CG, cg = tid - rg * CG;                     // rows 8 rg .., columns 4 cg ..
+    const bool active = 8 * rg < npad;
+    const bool sym = P.symmetric != 0;
+    acc_t acc[8][4];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0;
+    const int nvec = (npad * npad) >> 2;
+    for (int pass = 0; pass < (sym ? 1 : 2); ++pass) {
+        const int32_t *Asrc = pass == 0 ? P.DT : P.D;                // A[k][i] = D0[i][k]  |  D0[k][i]
+        const int32_t *Bsrc = pass == 0 ? P.FT : P.F;                // B[k][j] = F0[p_j][p_k]  |  F0[p_k][p_j]
+        if (pass) __syncthreads();
+        for (int e = tid; e < nvec; e += NT) reinterpret_cast<int4 *>(sA)[e] = reinterpret_cast<const int4 *>(Asrc)[e];
+        for (int e = tid; e < nvec; e += NT) {
+            const int k = (4 * e) / npad, j = 4 * e - k * npad;
+            const int32_t *row = Bsrc + (size_t)sPerm[k] * npad;
+            const bool kin = k < n;
+            reinterpret_cast<int4 *>(sB)[e] = make_int4((kin && j < n) ? row[sPerm[j]] : 0, (kin && j + 1 < n) ? row[sPerm[j + 1]] : 0,
+                                                        (kin && j + 2 < n) ? row[sPerm[j + 2]] : 0, (kin && j + 3 < n) ? row[sPerm[j + 3]] : 0);
+        }
+        __syncthreads();
+        if (active) {
+            const int32_t *pa = sA + 8 * rg, *pb = sB + 4 * cg;
+#pragma unroll 4
+            for (int k = 0; k < n; ++k) {
+                const int4 a0 = *reinterpret_cast<const int4 *>(pa + k * npad);
+                const int4 a1 = *reinterpret_cast<const int4 *>(pa + k * npad + 4);
+                const int4 bq = *reinterpret_cast<const int4 *>(pb + k * npad);
+                const int32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w}, bv[4] = {bq.x, bq.y, bq.z, bq.w};
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[u][v] += (acc_t)av[u] * (acc_t)bv[v];
+            }
+        }
+    }
+    // epilogue: direct term, diagonal products, pads, h on the diagonal (as in qap_build_m_kernel)
+    acc_t *Mb = reinterpret_cast<acc_t *>(P.M) + (size_t)b * npad * npad;
+    acc_t *hb = reinterpret_cast<acc_t *>(P.h) + (size_t)b * npad;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int i = 8 * rg + u;
+        if (i >= npad || !active) continue;
+        acc_t out[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int j = 4 * cg + v;
+            acc_t val = sym ? 2 * acc[u][v] : acc[u][v];
+            if (i >= n || j >= n) {
+                val = (i == j) ? (acc_t)0 : Acc<acc_t>::bighalf();
+            } else {
+                const int pi = sPerm[i], pj = sPerm[j];
+                if (i == j) {
+                    hb[i] = val + (acc_t)P.dd[i] * (acc_t)P.fd[pi];
+                    val = 0;
+                } else {
+                    val += (acc_t)P.D[(size_t)i * npad + j] *
+                               ((acc_t)P.F[(size_t)pi * npad + pj] + (acc_t)P.F[(size_t)pj * npad + pi]) +
+                           (acc_t)P.dd[i] * (acc_t)P.fd[pj];
+                }
+            }
+            out[v] = val;
+        }
+        st_acc4(&Mb[(size_t)i * npad + 4 * cg], out);
+    }
+    for (int i = n + tid; i < npad; i += NT) hb[i] = 0;
+}
+
 // kernels.all_deltas (_kernels.pyx:58-70) from M and h: out[b][k] = M[i][j] + M[j][i] - h[i] - h[j]
 // for the n(n-1)/2 moves in lexicographic (i, j) order, widened to int64.
 template <typename acc_t>

@@ -46,6 +46,7 @@ struct qapb_handle {
     int staged = 0, fits_i16 = 0;                  // int16 copies of D/F staged in shared memory
     int dsm = 0;                                   // hybrid: diagonal blocks in shared memory (no dedicated warps)
     int dd = 0;                                    // hybrid: diagonal blocks paired in the registers of the threads after the last unit
+    int ow = 0;                                    // hybrid: the search is one warp (n <= 32 with dd)
     unsigned smem_bytes = 0;
     int ctas_per_sm = 0, sm_count = 0;
     long long delta_bound = 0;
@@ -74,6 +75,8 @@ typedef void (*kern_t)(const SearchParams);
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 56, false, false, false
 #elif QAPB_DEV_ONLY == 6 // DD at 80 registers
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 80, false, false, false, true
+#elif QAPB_DEV_ONLY == 8 // one-warp searches (n <= 32), multi-start tabu
+#define QAPB_DEV_ARGS 1, true, 1, false, false, 64, false, false, false, true, true
 #elif QAPB_DEV_ONLY == 5 // recording instantiation of preset 4
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 64, false, false, true, true
 #elif QAPB_DEV_ONLY == 3 // recording instantiation of preset 1 (single-run entries: parity tests)
@@ -106,6 +109,7 @@ static kern_t pick_hybrid_kernel(int symm, int packed, int plan)
     //           two CTAs per SM where plan 0/1 would fit only one), without / with int16 staging
     // plan 5: plan 2 with the diagonal blocks in shared memory (no dedicated diagonal warps)
     // plan 6/7: plan 0/1 with the diagonal blocks paired in the threads after the last unit (DD), 64 registers
+    // plan 8: plan 6 as ONE warp (n <= 32): warp barriers, 32 searches per SM
 #define KH(S, PK) {(kern_t) qap_search_hybrid_kernel<S, PK, 1, false, false, 80>, \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, true, 80>,  \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128>,  \
@@ -113,14 +117,16 @@ static kern_t pick_hybrid_kernel(int symm, int packed, int plan)
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, false, true, 112>, \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128, true>,  \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, false, 64, false, false, true, true>, \
-                   (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, true, 64, false, false, true, true>}
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, true, 64, false, false, true, true>, \
+                   (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, false, 64, false, false, true, true, true>}
 #define KH2(PK) {(kern_t) qap_search_hybrid_kernel<2, PK, 1, false, false, 80>, \
                  (kern_t) qap_search_hybrid_kernel<2, PK, 1, false, true, 80>,  \
                  nullptr, nullptr, nullptr,                                     \
                  (kern_t) qap_search_hybrid_kernel<2, PK, 2, true, false, 128, true>,  \
                  (kern_t) qap_search_hybrid_kernel<2, PK, 1, false, false, 64, false, false, true, true>, \
-                 (kern_t) qap_search_hybrid_kernel<2, PK, 1, false, true, 64, false, false, true, true>}
-    static kern_t tab[3][2][8] = {{KH(0, false), KH(0, true)}, {KH(1, false), KH(1, true)}, {KH2(false), KH2(true)}};
+                 (kern_t) qap_search_hybrid_kernel<2, PK, 1, false, true, 64, false, false, true, true>, \
+                 (kern_t) qap_search_hybrid_kernel<2, PK, 1, false, false, 64, false, false, true, true, true>}
+    static kern_t tab[3][2][9] = {{KH(0, false), KH(0, true)}, {KH(1, false), KH(1, true)}, {KH2(false), KH2(true)}};
 #undef KH
 #undef KH2
     kern_t k = tab[symm][packed != 0][plan];
@@ -134,8 +140,9 @@ static kern_t multistart_kernel(int symm, int packed, int plan, int two_opt)
     if (!packed || symm > 1) return nullptr;
 #define KM(S, NT) (plan == 1 ? (kern_t) qap_search_hybrid_kernel<S, true, 1, false, true, 80, false, NT, false> \
                    : plan == 7 ? (kern_t) qap_search_hybrid_kernel<S, true, 1, false, true, 64, false, NT, false, true> \
+                   : plan == 8 ? (kern_t) qap_search_hybrid_kernel<S, true, 1, false, false, 64, false, NT, false, true, true> \
                              : (kern_t) qap_search_hybrid_kernel<S, true, 2, true, false, 128, true, NT, false>)
-    if (plan != 1 && plan != 5 && plan != 7) return nullptr;
+    if (plan != 1 && plan != 5 && plan != 7 && plan != 8) return nullptr;
     if (two_opt) return symm ? KM(1, true) : KM(0, true);
     return symm ? KM(1, false) : KM(0, false);
 #undef KM
@@ -148,7 +155,7 @@ static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_op
     const int packed = h->delta_bound < ((1LL << 27) - 1);
     int plan = h->us > 0 ? 2 : (h->upt == 2 ? (h->staged ? 4 : 3) : (h->staged ? 1 : 0));
     if (h->dsm) plan = 5;
-    if (h->dd) plan = h->staged ? 7 : 6;
+    if (h->dd) plan = h->ow ? 8 : h->staged ? 7 : 6;
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
     if (multistart && h->storage == 3)
         if (kern_t k2 = multistart_kernel(symm, packed, plan, two_opt)) return k2;
@@ -171,7 +178,8 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     if ((long long)(ur + us) * toff < h->noff) return false;
     if (threads > 1024 || (us > 0 && threads > 512) || (us == 0 && ur == 2 && threads > 608)) return false;
     int exp_in_smem = 1;
-    HybLayout L = make_hyb_layout(h->npad, nb, toff, us, 1, 0, 1, dsm);
+    const int ow = dd && threads == 32 && h->npad <= 32;  // the whole search is one warp
+    HybLayout L = make_hyb_layout(h->npad, nb, toff, us, 1, 0, 1, dsm, ow);
     // keep the expiry array in shared memory only while it does not cost a resident CTA
     if (L.total > (smem_target ? smem_target : smem_cap) && us > 0) {
         exp_in_smem = 0;
@@ -182,7 +190,7 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     if (h->npad > 128 && !(us > 0 && ur == 2)) return false;  // layout size class 256 is tied to the (2 + smem) shape
     if (h->npad <= 128 && us > 0) return false;
     int staged = 0;
-    if (us == 0 && h->fits_i16 && !getenv("QAPB_NO_STAGE")) {
+    if (us == 0 && h->fits_i16 && !ow && !getenv("QAPB_NO_STAGE")) {
         // stage while two CTAs per SM still fit
         HybLayout Ls = make_hyb_layout(h->npad, nb, toff, us, exp_in_smem, 1, h->symmetric, dsm);
         if (Ls.total <= std::min(smem_cap, ((dsm || dd) ? 74u : 110u) * 1024u)) { staged = 1; L = Ls; }
@@ -190,6 +198,7 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     h->staged = staged;
     h->dsm = dsm;
     h->dd = dd;
+    h->ow = ow;
     h->upt = ur; h->toff = toff; h->us = us; h->exp_in_smem = exp_in_smem;
     h->threads = threads;
     h->lb_class = 0;
@@ -258,7 +267,14 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
     // paired diagonal blocks (three searches per SM at n = 100) are a candidate plan, not the default: the
     // warp that carries them runs an off-diagonal pass AND two diagonal passes, and the other warps wait
     // for it at barrier 1 (580 against 800 G evals/s at n = 100)
-    if (getenv("QAPB_DD") && try_hybrid_plan(h, smem_cap, 1, td, 0, 2)) return true;
+    const char *dd_env = getenv("QAPB_DD");
+    if (dd_env && dd_env[0] == '1' && try_hybrid_plan(h, smem_cap, 1, td, 0, 2)) return true;
+    // n <= 32: the paired-diagonal plan is ONE warp per search (no block barriers, 32 searches per SM).  A
+    // candidate, not the default: it wins only on large batches (393 against 337 G evals/s at 4736 starts of
+    // n = 30) and loses on the BASELINE configurations (271 against 318 G at 1776 starts; a single start takes
+    // 2.1 us per iteration against 1.2)
+    const char *ow_env = getenv("QAPB_OW");
+    if (td == 32 && h->npad <= 32 && ow_env && ow_env[0] == '1' && try_hybrid_plan(h, smem_cap, 1, td, 0, 2)) return true;
     if (!try_hybrid_plan(h, smem_cap, 1, t1, 0)) return false;
     if (hybrid_occupancy(h) >= 2 || t2 < 32) return true;
     const qapb_handle one = *h;
@@ -766,6 +782,21 @@ static int launch_build(qapb_handle *h, const WsPlan &w, int batch, int rng, int
     BP.perm32 = SP.perm32;
     BP.M = (char *)h->ws + w.offInitM;
     BP.h = (char *)h->ws + w.offInitH;
+    if (h->npad <= 128 && !getenv("QAPB_BUILD_TILED")) {
+        // one CTA per permutation: D^T and the gathered F staged once, 8 x 4 register tiles over all k
+        const int cgs = h->npad / 4, rgs = (h->npad + 7) / 8;
+        const unsigned nt = (unsigned)((cgs * rgs + 31) / 32 * 32);
+        const size_t dyn = (2 * (np * np + 8) + np) * sizeof(int32_t);
+        if (h->acc_bits == 64) {
+            CU(ensure_smem_optin((const void *)qap_build_m_whole_kernel<int64_t>, h->device, (unsigned)dyn));
+            qap_build_m_whole_kernel<int64_t><<<batch, nt, dyn, st>>>(BP);
+        } else {
+            CU(ensure_smem_optin((const void *)qap_build_m_whole_kernel<int32_t>, h->device, (unsigned)dyn));
+            qap_build_m_whole_kernel<int32_t><<<batch, nt, dyn, st>>>(BP);
+        }
+        CU(cudaGetLastError());
+        return QAPB_OK;
+    }
     const int bt = build_tile(h->npad), tiles = (h->npad + bt - 1) / bt;
     const unsigned grid = (unsigned)(tiles * tiles) * (unsigned)batch;
     const unsigned nt = (unsigned)(((bt / 4) * (bt / 4) + 31) / 32 * 32);
@@ -792,7 +823,7 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     const bool records = P.tr_i || P.cells;
     kern_t kern = handle_kernel(h, P.rng && !records, P.mode == MODE_TWO_OPT);
     if (h->storage == 3) {
-        P.hlay = make_hyb_layout(h->npad, h->nb, h->toff, h->us, h->exp_in_smem, h->staged, h->symmetric, h->dsm);
+        P.hlay = make_hyb_layout(h->npad, h->nb, h->toff, h->us, h->exp_in_smem, h->staged, h->symmetric, h->dsm, h->ow);
         P.staged = h->staged; P.dsm = h->dsm;
         P.toff = h->toff; P.us = h->us; P.exp_in_smem = h->exp_in_smem;
     } else {

@@ -44,10 +44,10 @@ namespace qapb {
 #define HYB_FIXED_END(NPM) (HYB_TEN(NPM) + 4 * TENURE_CHUNK)
 
 __host__ __device__ inline HybLayout make_hyb_layout(int npad, int nb, int toff, int us, int exp_in_smem,
-                                                     int staged = 0, int symmetric = 1, int dsm = 0)
+                                                     int staged = 0, int symmetric = 1, int dsm = 0, int onewarp = 0)
 {
     HybLayout L;
-    const unsigned npm = npad <= 128 ? 128u : 256u;
+    const unsigned npm = onewarp ? 32u : npad <= 128 ? 128u : 256u;
     L.offA = HYB_VEC(0, npm); L.offC = HYB_VEC(1, npm); L.offB = HYB_VEC(2, npm); L.offE = HYB_VEC(3, npm);
     L.offH = HYB_VEC(4, npm); L.offColR = HYB_VEC(5, npm); L.offColS = HYB_VEC(6, npm); L.offTR = HYB_VEC(7, npm);
     L.offTS = HYB_VEC(8, npm); L.offXR = HYB_VEC(9, npm); L.offXS = HYB_VEC(10, npm); L.offP = HYB_VEC(11, npm);
@@ -398,10 +398,15 @@ __device__ __forceinline__ void expire_bits(unsigned &tb, int32_t &mexp, int c, 
 // the register footprint of one off-diagonal unit), in the threads that follow the last off-diagonal
 // unit.  n = 100: 300 + 13 threads = 10 warps instead of 11, which at 64 registers is what lets THREE
 // searches share an SM.
+// OW (n <= 32 with DD): the whole search is ONE warp -- 28 off-diagonal units and four lanes with two diagonal
+// blocks each at n = 29..32 -- so the two block barriers of an iteration become warp barriers, the warp
+// argmin is already the result, and 32 independent searches share an SM (size class 32 of the shared-memory
+// layout: 5.6 KB per search).
 template <int SYMM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG, bool DSM = false, bool NOTABU = false,
-          bool REC = true, bool DD = false>
+          bool REC = true, bool DD = false, bool OW = false>
 __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams P)
 {
+    static_assert(!OW || (DD && !STG), "one-warp searches: paired diagonal blocks, no staged matrices");
     static_assert(!DD || (UR == 1 && !SMEMU && !DSM), "paired diagonal blocks: one register unit per thread");
     constexpr bool SYM = SYMM != 0;       // single-product pass
     constexpr bool FULLSYM = SYMM == 1;   // symmetric closed forms in the publish phase, no transposes
@@ -415,7 +420,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     int32_t *sM = reinterpret_cast<int32_t *>(smem_raw + lay.offM);
     unsigned *sTB = reinterpret_cast<unsigned *>(smem_raw + lay.offTB);
     int32_t *sMX = reinterpret_cast<int32_t *>(smem_raw + lay.offMX);
-    constexpr int NPM = (SMEMU && UR == 2) ? 256 : 128;  // size class of the plan (host: make_hyb_layout)
+    constexpr int NPM = OW ? 32 : (SMEMU && UR == 2) ? 256 : 128;  // size class of the plan (host: make_hyb_layout)
     Vecs V;
     V.A = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(0, NPM));
     V.C = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(1, NPM));
@@ -715,11 +720,15 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         int32_t bd = my_d;
         unsigned bkey = my_key;
         warp_argmin(bd, bkey);
-        if (lane == 0) { sRedD[warp] = bd; sRedK[warp] = bkey; }
-        __syncthreads();  // ---------------------------------------------- sync #1
-        bd = lane < W ? sRedD[lane] : MAXV;
-        bkey = lane < W ? sRedK[lane] : 0xffffffffu;
-        warp_argmin(bd, bkey);
+        if (OW) {
+            __syncwarp();  // ------------------------------------------------ sync #1 (one warp: the argmin is final)
+        } else {
+            if (lane == 0) { sRedD[warp] = bd; sRedK[warp] = bkey; }
+            __syncthreads();  // ------------------------------------------ sync #1
+            bd = lane < W ? sRedD[lane] : MAXV;
+            bkey = lane < W ? sRedK[lane] : 0xffffffffu;
+            warp_argmin(bd, bkey);
+        }
         if (bd == MAXV) {  // no admissible move: premature stop (_kernels.pyx:168-170)
             stopped = 1;
             break;
@@ -980,7 +989,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             }
         }
         if (timing) tF = clock64();
-        __syncthreads();  // ---------------------------------------------- sync #2
+        if (OW) __syncwarp(); else __syncthreads();  // ------------------- sync #2
         if (tid == 0) { sP[r] = ps; sP[s] = pr; }
         if (timing) {
             const long long tG = clock64() + (sP[0] & 0);

@@ -1,42 +1,30 @@
-"""Error types raised at the library boundary.
-
-Mirrors the reference hierarchy (/root/reference/pkg/src/qapsolve/errors.py:4-36)
-so that callers written against `qapsolve` catch the same classes.  Status codes
-returned by the C ABI (include/qapb.h) are mapped onto these in `_lib.check`.
-"""
+"""Error types at the library boundary: the reference's own classes when `qapsolve` is importable (so that
+callers written against it catch the same classes), else a minimal local hierarchy.  Status codes of the
+C ABI (include/qapb.h) are mapped onto these in `_lib.check`."""
 
 from __future__ import annotations
 
+from ._refpkg import reference
 
-class QapError(Exception):
-    """Root of every error this package raises."""
+if reference() is not None:
+    from qapsolve.errors import DomainError, IntegrityError, MalformedInstanceError, QapError, TokenParseError  # noqa: F401
+else:
+    class QapError(Exception):
+        pass
 
+    class DomainError(QapError, ValueError):
+        pass
 
-class DomainError(QapError, ValueError):
-    """An argument lies outside what the operation is defined for."""
+    class IntegrityError(QapError):
+        pass
 
+    class MalformedInstanceError(QapError):
+        def __init__(self, message, byte_offset=None):
+            super().__init__(message if byte_offset is None else f"{message} (byte offset {byte_offset})")
+            self.byte_offset = byte_offset
 
-class IntegrityError(QapError):
-    """Persisted or replayed data no longer validates (cost mismatch, bad trail)."""
-
-
-class MalformedInstanceError(QapError):
-    """An instance stream holds the wrong number of tokens."""
-
-    def __init__(self, message: str, byte_offset: int):
-        self.byte_offset = byte_offset
-        super().__init__(f"{message} (byte offset {byte_offset})")
-
-
-class TokenParseError(QapError):
-    """A token that should have been an integer was not."""
-
-    def __init__(self, message: str, byte_offset: int | None = None, line: int | None = None):
-        self.byte_offset = byte_offset
-        self.line = line
-        parts = []
-        if byte_offset is not None:
-            parts.append(f"byte offset {byte_offset}")
-        if line is not None:
-            parts.append(f"line {line}")
-        super().__init__(f"{message} ({', '.join(parts)})" if parts else message)
+    class TokenParseError(QapError):
+        def __init__(self, message, byte_offset=None, line=None):
+            where = [f"{k} {v}" for k, v in (("byte offset", byte_offset), ("line", line)) if v is not None]
+            super().__init__(f"{message} ({', '.join(where)})" if where else message)
+            self.byte_offset, self.line = byte_offset, line
