@@ -214,8 +214,13 @@ __global__ void __launch_bounds__(256) qap_build_m_kernel(const BuildParams P)
 // copies and one gather per entry, instead of re-staging both per 52 x 52 tile and per 32-wide k-chunk with
 // two barriers each -- and every thread then runs all n k-steps on an 8 x 4 register tile: three 128-bit
 // shared loads feed 32 IMADs per step.  (Asymmetric instances make a second pass with D and F0[p_k][p_j].)
-template <typename acc_t>
-__global__ void __launch_bounds__(544) qap_build_m_whole_kernel(const BuildParams P)
+// EMIT (kernels.all_deltas): instead of writing M and h for a search kernel, the CTA parks them in its own
+// shared memory (row stride npad + 1: the column reads M[j][i] are conflict-free) and writes the n(n-1)/2
+// deltas M[i][j] + M[j][i] - h[i] - h[j] in lexicographic order straight away -- no M round trip through
+// global memory and no second kernel.
+// (MAXT / MINB: up to 352 threads -- n <= 104 -- two CTAs share an SM, so the register budget is 88.)
+template <typename acc_t, bool EMIT, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) qap_build_m_whole_kernel(const BuildParams P, int64_t *__restrict__ deltas)
 {
     extern __shared__ __align__(16) unsigned char dyn[];
     const int n = P.n, npad = P.npad, tid = threadIdx.x, NT = blockDim.x, b = blockIdx.x;
@@ -250,49 +255,96 @@ __global__ void __launch_bounds__(544) qap_build_m_whole_kernel(const BuildParam
         __syncthreads();
         if (active) {
             const int32_t *pa = sA + 8 * rg, *pb = sB + 4 * cg;
-#pragma unroll 4
+            // software pipeline: the operands of step k + 1 are in flight while the 32 IMADs of step k issue
+            int4 a0 = *reinterpret_cast<const int4 *>(pa), a1 = *reinterpret_cast<const int4 *>(pa + 4);
+            int4 bq = *reinterpret_cast<const int4 *>(pb);
+#pragma unroll 2
             for (int k = 0; k < n; ++k) {
-                const int4 a0 = *reinterpret_cast<const int4 *>(pa + k * npad);
-                const int4 a1 = *reinterpret_cast<const int4 *>(pa + k * npad + 4);
-                const int4 bq = *reinterpret_cast<const int4 *>(pb + k * npad);
+                const int kn = (k + 1 < n) ? k + 1 : k;
+                const int4 a0n = *reinterpret_cast<const int4 *>(pa + kn * npad);
+                const int4 a1n = *reinterpret_cast<const int4 *>(pa + kn * npad + 4);
+                const int4 bqn = *reinterpret_cast<const int4 *>(pb + kn * npad);
                 const int32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w}, bv[4] = {bq.x, bq.y, bq.z, bq.w};
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
 #pragma unroll
                     for (int v = 0; v < 4; ++v) acc[u][v] += (acc_t)av[u] * (acc_t)bv[v];
+                a0 = a0n; a1 = a1n; bq = bqn;
             }
         }
     }
-    // epilogue: direct term, diagonal products, pads, h on the diagonal (as in qap_build_m_kernel)
-    acc_t *Mb = reinterpret_cast<acc_t *>(P.M) + (size_t)b * npad * npad;
-    acc_t *hb = reinterpret_cast<acc_t *>(P.h) + (size_t)b * npad;
+    // epilogue: direct term, diagonal products, pads, h on the diagonal.  The matrix entries it needs are in
+    // shared memory already: after the last pass sA[i][j] = D0[i][j] and sB[i][j] = F0[p_i][p_j] (by symmetry in
+    // the one-pass case), so the direct term D0[i][j] (F0[p_i][p_j] + F0[p_j][p_i]) costs 128-bit shared loads
+    // instead of three dependent global loads per entry (they were over half of the kernel's time).
+    const int ldm = EMIT ? npad + 1 : npad;
+    acc_t *Mb = EMIT ? reinterpret_cast<acc_t *>(dyn) : reinterpret_cast<acc_t *>(P.M) + (size_t)b * npad * npad;
+    acc_t *hb = EMIT ? Mb + (size_t)npad * ldm : reinterpret_cast<acc_t *>(P.h) + (size_t)b * npad;
+    acc_t hdiag[8];
+    if (active) {
+        int32_t fdj[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        const int i = 8 * rg + u;
-        if (i >= npad || !active) continue;
-        acc_t out[4];
+        for (int v = 0; v < 4; ++v) fdj[v] = (4 * cg + v < n) ? P.fd[sPerm[4 * cg + v]] : 0;
+        int32_t ft[4][8];  // F0[p_j][p_i] for the thread's 4 columns j and 8 rows i
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-            const int j = 4 * cg + v;
-            acc_t val = sym ? 2 * acc[u][v] : acc[u][v];
-            if (i >= n || j >= n) {
-                val = (i == j) ? (acc_t)0 : Acc<acc_t>::bighalf();
-            } else {
-                const int pi = sPerm[i], pj = sPerm[j];
-                if (i == j) {
-                    hb[i] = val + (acc_t)P.dd[i] * (acc_t)P.fd[pi];
+            const int4 t0 = *reinterpret_cast<const int4 *>(sB + (size_t)(4 * cg + v) * npad + 8 * rg);
+            const int4 t1 = *reinterpret_cast<const int4 *>(sB + (size_t)(4 * cg + v) * npad + 8 * rg + 4);
+            ft[v][0] = t0.x; ft[v][1] = t0.y; ft[v][2] = t0.z; ft[v][3] = t0.w;
+            ft[v][4] = t1.x; ft[v][5] = t1.y; ft[v][6] = t1.z; ft[v][7] = t1.w;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = 8 * rg + u;
+            hdiag[u] = 0;
+            if (i >= npad) continue;
+            const int4 d4 = *reinterpret_cast<const int4 *>(sA + (size_t)i * npad + 4 * cg);
+            const int4 f4 = *reinterpret_cast<const int4 *>(sB + (size_t)i * npad + 4 * cg);
+            const int32_t dv[4] = {d4.x, d4.y, d4.z, d4.w}, fv[4] = {f4.x, f4.y, f4.z, f4.w};
+            const int32_t ddi = i < n ? P.dd[i] : 0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int j = 4 * cg + v;
+                acc_t val = sym ? 2 * acc[u][v] : acc[u][v];
+                if (i >= n || j >= n) {
+                    val = (i == j) ? (acc_t)0 : Acc<acc_t>::bighalf();
+                } else if (i == j) {
+                    hdiag[u] = val + (acc_t)ddi * (acc_t)fdj[v];
                     val = 0;
                 } else {
-                    val += (acc_t)P.D[(size_t)i * npad + j] *
-                               ((acc_t)P.F[(size_t)pi * npad + pj] + (acc_t)P.F[(size_t)pj * npad + pi]) +
-                           (acc_t)P.dd[i] * (acc_t)P.fd[pj];
+                    val += (acc_t)dv[v] * ((acc_t)fv[v] + (acc_t)ft[v][u]) + (acc_t)ddi * (acc_t)fdj[v];
                 }
+                acc[u][v] = val;
             }
-            out[v] = val;
         }
-        st_acc4(&Mb[(size_t)i * npad + 4 * cg], out);
+    }
+    if (EMIT) __syncthreads();  // every thread is done with sA / sB / sPerm: M may be parked over them
+    if (active) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = 8 * rg + u;
+            if (i >= npad) continue;
+            if (i < n && (i >> 2) == cg) hb[i] = hdiag[u];  // the thread that holds the diagonal entry of row i
+            if (EMIT) {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) Mb[(size_t)i * ldm + 4 * cg + v] = acc[u][v];
+            } else {
+                st_acc4(&Mb[(size_t)i * npad + 4 * cg], acc[u]);
+            }
+        }
     }
     for (int i = n + tid; i < npad; i += NT) hb[i] = 0;
+    if (EMIT) {
+        __syncthreads();
+        const int npairs = n * (n - 1) / 2;
+        int64_t *ob = deltas + (size_t)b * npairs;
+        int i = 0, j = tid + 1;  // pair number k in row-major order of the upper triangle: row i holds j = i+1 .. n-1
+        for (int k = tid; k < npairs; k += NT) {
+            while (j >= n) { j = j - n + (i + 2); ++i; }  // carry into the following rows
+            ob[k] = (int64_t)(Mb[(size_t)i * ldm + j] + Mb[(size_t)j * ldm + i] - hb[i] - hb[j]);
+            j += NT;
+        }
+    }
 }
 
 // kernels.all_deltas (_kernels.pyx:58-70) from M and h: out[b][k] = M[i][j] + M[j][i] - h[i] - h[j]

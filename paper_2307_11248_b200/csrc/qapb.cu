@@ -768,8 +768,10 @@ static WsPlan plan_ws(const qapb_handle *h, int batch, size_t head)
 // qap_start_kernel + qap_build_m_kernel for `batch` permutations (caller-provided or device-drawn)
 static int launch_build(qapb_handle *h, const WsPlan &w, int batch, int rng, int force_seq, unsigned long long master_seed,
                         unsigned long long first_index, const unsigned long long *seeds, const int64_t *perms,
-                        cudaStream_t st, BuildParams &BP, StartParams &SP)
+                        cudaStream_t st, BuildParams &BP, StartParams &SP, int64_t *emit_deltas = nullptr,
+                        int *emitted = nullptr)
 {
+    if (emitted) *emitted = 0;
     const size_t np = (size_t)h->npad;
     SP.n = h->n; SP.npad = h->npad; SP.rng = rng; SP.force_seq_rng = force_seq;
     SP.master_seed = master_seed; SP.first_index = first_index; SP.seeds = seeds; SP.perms = perms;
@@ -786,15 +788,26 @@ static int launch_build(qapb_handle *h, const WsPlan &w, int batch, int rng, int
         // one CTA per permutation: D^T and the gathered F staged once, 8 x 4 register tiles over all k
         const int cgs = h->npad / 4, rgs = (h->npad + 7) / 8;
         const unsigned nt = (unsigned)((cgs * rgs + 31) / 32 * 32);
-        const size_t dyn = (2 * (np * np + 8) + np) * sizeof(int32_t);
-        if (h->acc_bits == 64) {
-            CU(ensure_smem_optin((const void *)qap_build_m_whole_kernel<int64_t>, h->device, (unsigned)dyn));
-            qap_build_m_whole_kernel<int64_t><<<batch, nt, dyn, st>>>(BP);
-        } else {
-            CU(ensure_smem_optin((const void *)qap_build_m_whole_kernel<int32_t>, h->device, (unsigned)dyn));
-            qap_build_m_whole_kernel<int32_t><<<batch, nt, dyn, st>>>(BP);
-        }
+        const size_t acc = h->acc_bits / 8;
+        const size_t dyn_build = (2 * (np * np + 8) + np) * sizeof(int32_t);
+        const size_t dyn = emit_deltas ? std::max(dyn_build, (np * (np + 1) + np) * acc + 16) : dyn_build;
+#define QAPB_WHOLE2(A, E, T, B)                                                                                  \
+    do {                                                                                                         \
+        const void *kf = (const void *)qap_build_m_whole_kernel<A, E, T, B>;                                     \
+        CU(ensure_smem_optin(kf, h->device, (unsigned)dyn));                                                     \
+        CU(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared)); \
+        qap_build_m_whole_kernel<A, E, T, B><<<batch, nt, dyn, st>>>(BP, emit_deltas);                           \
+    } while (0)
+#define QAPB_WHOLE(A, E)                                                                                         \
+    do {                                                                                                         \
+        if (nt <= 352 && sizeof(A) == 4) QAPB_WHOLE2(A, E, 352, 2); else QAPB_WHOLE2(A, E, 544, 1);              \
+    } while (0)
+        if (h->acc_bits == 64) { if (emit_deltas) QAPB_WHOLE(int64_t, true); else QAPB_WHOLE(int64_t, false); }
+        else { if (emit_deltas) QAPB_WHOLE(int32_t, true); else QAPB_WHOLE(int32_t, false); }
+#undef QAPB_WHOLE
+#undef QAPB_WHOLE2
         CU(cudaGetLastError());
+        if (emitted) *emitted = emit_deltas != nullptr;  // the deltas have been written: no emission kernel needed
         return QAPB_OK;
     }
     const int bt = build_tile(h->npad), tiles = (h->npad + bt - 1) / bt;
@@ -880,12 +893,15 @@ extern "C" int qapb_all_deltas(qapb_handle *h, const int64_t *perms, int batch, 
     CU(cudaEventRecord(h->ev0, st));
     BuildParams BP;
     StartParams SP;
-    rc = launch_build(h, w, batch, 0, 0, 0, 0, nullptr, perms, st, BP, SP);
+    int emitted = 0;
+    rc = launch_build(h, w, batch, 0, 0, 0, 0, nullptr, perms, st, BP, SP, deltas, &emitted);
     if (rc) return rc;
-    const dim3 grid(batch, std::min(h->n - 1, 64));
-    if (h->acc_bits == 64) qap_emit_deltas_kernel<int64_t><<<grid, 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
-    else qap_emit_deltas_kernel<int32_t><<<grid, 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
-    CU(cudaGetLastError());
+    if (!emitted) {  // tiled build (n > 128): M and h are in the workspace, emit from there
+        const dim3 grid(batch, std::min(h->n - 1, 64));
+        if (h->acc_bits == 64) qap_emit_deltas_kernel<int64_t><<<grid, 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
+        else qap_emit_deltas_kernel<int32_t><<<grid, 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
+        CU(cudaGetLastError());
+    }
     CU(cudaEventRecord(h->ev1, st));
     h->have_timing = 1;
     return QAPB_OK;
