@@ -47,6 +47,7 @@ struct qapb_handle {
     int dsm = 0;                                   // hybrid: diagonal blocks in shared memory (no dedicated warps)
     int dd = 0;                                    // hybrid: diagonal blocks paired in the registers of the threads after the last unit
     int ow = 0;                                    // hybrid: the search is one warp (n <= 32 with dd)
+    int wide = 0;                                  // hybrid: unsigned 32-bit state with 64-bit deltas (acc_bits holds the STATE width, 32)
     unsigned smem_bytes = 0;
     int ctas_per_sm = 0, sm_count = 0;
     long long delta_bound = 0;
@@ -77,6 +78,8 @@ typedef void (*kern_t)(const SearchParams);
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 80, false, false, false, true
 #elif QAPB_DEV_ONLY == 8 // one-warp searches (n <= 32), multi-start tabu
 #define QAPB_DEV_ARGS 1, true, 1, false, false, 64, false, false, false, true, true
+#elif QAPB_DEV_ONLY == 9 // tai150b: 64-bit deltas over unsigned 32-bit state, shared-memory plan with DSM, one symmetric matrix
+#define QAPB_DEV_ARGS 2, false, 2, true, false, 128, true, false, true, false, false, true
 #elif QAPB_DEV_ONLY == 5 // recording instantiation of preset 4
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 64, false, false, true, true
 #elif QAPB_DEV_ONLY == 3 // recording instantiation of preset 1 (single-run entries: parity tests)
@@ -85,6 +88,7 @@ typedef void (*kern_t)(const SearchParams);
 static kern_t pick_kernel(int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
 static kern_t pick_hybrid_kernel(int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
 static kern_t multistart_kernel(int, int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
+static kern_t pick_wide_kernel(int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
 #else
 static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
 {
@@ -97,6 +101,18 @@ static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
     };
 #undef K
     return tab[acc_bits == 64][storage][lb_class];
+}
+
+// WIDE instantiations (unsigned 32-bit state, 64-bit deltas; never packed): the one-register-unit plan without /
+// with staged matrices and the shared-memory plan with DSM.
+static kern_t pick_wide_kernel(int symm, int plan)
+{
+#define KW(S) {(kern_t) qap_search_hybrid_kernel<S, false, 1, false, false, 80, false, false, true, false, false, true>, \
+               (kern_t) qap_search_hybrid_kernel<S, false, 1, false, true, 80, false, false, true, false, false, true>,  \
+               (kern_t) qap_search_hybrid_kernel<S, false, 2, true, false, 128, true, false, true, false, false, true>}
+    static kern_t tab[3][3] = {KW(0), KW(1), KW(2)};
+#undef KW
+    return tab[symm][plan == 5 ? 2 : plan];
 }
 
 static kern_t pick_hybrid_kernel(int symm, int packed, int plan)
@@ -157,6 +173,7 @@ static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_op
     if (h->dsm) plan = 5;
     if (h->dd) plan = h->ow ? 8 : h->staged ? 7 : 6;
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
+    if (h->storage == 3 && h->wide) return pick_wide_kernel(symm, plan);
     if (multistart && h->storage == 3)
         if (kern_t k2 = multistart_kernel(symm, packed, plan, two_opt)) return k2;
     return h->storage == 3 ? pick_hybrid_kernel(symm, packed, plan)
@@ -171,6 +188,7 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     const int nb = h->nb, dw = (nb + 31) / 32;
     const int dd = dsm == 2;  // diagonal blocks paired in registers: no dedicated warps, toff counts every thread
     if (dd) dsm = 0;
+    if (h->wide && (dd || (ur == 2 && !dsm))) return false;  // 64-bit deltas: plans 0 / 1 / 5 only
     if (dd && !(ur == 1 && us == 0 && toff >= h->noff + (nb + 1) / 2)) return false;
     const int threads = (dsm || dd) ? toff : toff + 32 * dw;
     if (dsm && !(ur == 2 && us > 0)) return false;  // the instantiated shape
@@ -252,12 +270,13 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
         // 545 / 559 / 616 G evals/s at n = 144 / 160 / 180 against 420 / 376 / 442 for the dedicated-
         // diagonal-warp plan); else all 512 threads on one search (4 units per thread at n = 256
         // instead of 4 or 5 on 14 of 16 warps: 710 -> 750 G evals/s).
-        if (!getenv("QAPB_NO_DSM")) {
+        if (!getenv("QAPB_NO_DSM") || h->wide) {
             const int us2 = std::max(1, (noff - 2 * 256 + 255) / 256);
             if (try_hybrid_plan(h, smem_cap, 2, 256, us2, 1, 113u * 1024u) && hybrid_occupancy(h) >= 2) return true;
             const int us1 = std::max(1, (noff - 2 * 512 + 511) / 512);
             if (try_hybrid_plan(h, smem_cap, 2, 512, us1, 1)) return true;
         }
+        if (h->wide) return false;  // (no 64-bit-delta instantiation of the dedicated-diagonal-warp plan)
         const int toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
         const int us = std::max(0, (noff - 2 * toff + toff - 1) / toff);
         return try_hybrid_plan(h, smem_cap, 2, toff, us);
@@ -268,6 +287,7 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
     // warp that carries them runs an off-diagonal pass AND two diagonal passes, and the other warps wait
     // for it at barrier 1 (580 against 800 G evals/s at n = 100)
     const char *dd_env = getenv("QAPB_DD");
+    if (h->wide) return try_hybrid_plan(h, smem_cap, 1, t1, 0);  // 64-bit deltas: the one-register-unit plan only
     if (dd_env && dd_env[0] == '1' && try_hybrid_plan(h, smem_cap, 1, td, 0, 2)) return true;
     // n <= 32: the paired-diagonal plan is ONE warp per search (no block barriers, 32 searches per SM).  A
     // candidate, not the default: it wins only on large batches (393 against 337 G evals/s at 4736 starts of
@@ -297,11 +317,11 @@ static std::vector<std::array<int, 4>> hybrid_candidates(const qapb_handle *h)
     if (nb > 32) {
         for (int t : {256, 384, 512}) add(2, t, std::max(1, (noff - 2 * t + t - 1) / t), 1);
         const int toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
-        add(2, toff, std::max(0, (noff - 2 * toff + toff - 1) / toff), 0);
+        if (!h->wide) add(2, toff, std::max(0, (noff - 2 * toff + toff - 1) / toff), 0);
     } else {
-        add(1, (noff + (nb + 1) / 2 + 31) / 32 * 32, 0, 2);
+        if (!h->wide) add(1, (noff + (nb + 1) / 2 + 31) / 32 * 32, 0, 2);
         add(1, (noff + 31) / 32 * 32, 0, 0);
-        add(2, ((noff + 1) / 2 + 31) / 32 * 32, 0, 0);
+        if (!h->wide) add(2, ((noff + 1) / 2 + 31) / 32 * 32, 0, 0);
     }
     return out;
 }
@@ -479,7 +499,14 @@ static void fill_unit_table(const qapb_handle *h, uint16_t *units)
 {
     const int nb = h->nb, noff = h->noff;
     int u = 0;
-    const bool clustered = h->storage == 3 && !getenv("QAPB_NO_CLUSTER");
+    // Measured (G evals/s, clustered vs lexicographic): n = 100 852 vs 831, n = 160 682 vs 661 -- but n = 64 683
+    // vs 718 and n = 256 (one 512-thread search per SM) 786 vs 843: a clique's blocks sit at arbitrary
+    // shared-memory banks, where a lexicographic warp reads one broadcast block and consecutive ones, and
+    // with few warps (n <= 76) or every warp busy anyway (512 threads) the conflicts cost more than the
+    // skipped regions save.  Hence only the two-searches-per-SM plans from 20 blocks up.
+    const char *cl_env = getenv("QAPB_CLUSTER");  // development: 0 / 1 overrides the rule
+    const bool by_rule = h->nb >= 20 && h->threads <= 384;
+    const bool clustered = h->storage == 3 && !getenv("QAPB_NO_CLUSTER") && (cl_env ? cl_env[0] == '1' : by_rule);
     if (!clustered) {
         for (int I = 0; I < nb; ++I)
             for (int J = I + 1; J < nb; ++J) units[u++] = (uint16_t)(I | (J << 8));
@@ -539,13 +566,14 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
 
     const int nb = (n + 3) / 4, npad = nb * 4;
     std::vector<long long> F0((size_t)n * n), D0((size_t)n * n), fd(n), dd(n);
-    bool sym = true, symF = true, symD = true, fits16 = true;
+    bool sym = true, symF = true, symD = true, fits16 = true, nonneg = true;
     long long maxF0 = 0, maxD0 = 0;
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
             long long f = flow[(size_t)i * n + j], d = dist[(size_t)i * n + j];
             if (std::llabs(f) >= (1LL << 30) || std::llabs(d) >= (1LL << 30))
                 return fail(QAPB_ERR_UNSUPPORTED, "matrix entries must satisfy |x| < 2^30");
+            if (f < 0 || d < 0) nonneg = false;
             if (i == j) { fd[i] = f; dd[i] = d; f = 0; d = 0; }
             if (std::llabs(f) > 32767 || std::llabs(d) > 32767) fits16 = false;
             F0[(size_t)i * n + j] = f;
@@ -601,7 +629,20 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
     h->lb_class = threads <= 384 ? 0 : 1;
     int storage = 0;
     const char *force = getenv("QAPB_FORCE_GENERIC");
-    if (h->acc_bits == 32 && nb <= 64 && !(force && force[0] == '1') && plan_hybrid(h, smem_cap)) {
+    const bool forced_generic = force && force[0] == '1';
+    // 64-bit deltas over UNSIGNED 32-bit state (search_hybrid.cuh, WIDE): the bound exceeds int32, but with
+    // non-negative entries every M[i][j] and h[i] is a cost in [0, bound] and bound < 2^32 (4.0e9 admitted: the
+    // pad constant needs the margin) -- tai*b shapes.  The state, the build kernels and the workspace are then
+    // 32-bit, and the instance runs on the register / shared-memory plans instead of the generic kernel.
+    if (h->acc_bits == 64 && nonneg && bnd < 4.0e9 && nb <= 64 && !forced_generic && !getenv("QAPB_NO_WIDE")) {
+        const qapb_handle saved = *h;
+        h->acc_bits = 32;
+        h->wide = 1;
+        if (plan_hybrid(h, smem_cap)) storage = 3;
+        else *h = saved;
+    }
+    if (storage == 3) {
+    } else if (h->acc_bits == 32 && nb <= 64 && !forced_generic && plan_hybrid(h, smem_cap)) {
         storage = 3;
     } else {
         // generic kernel: M in shared memory when it fits, else in an L2-resident workspace, else
@@ -701,7 +742,7 @@ extern "C" int qapb_get_info(const qapb_handle *h, qapb_info *info)
         ensure_smem_optin((const void *)handle_kernel(h), h->device, h->smem_bytes);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hm->ctas_per_sm, (const void *)handle_kernel(h), h->threads, h->smem_bytes);
     }
-    info->n = h->n; info->device = h->device; info->acc_bits = h->acc_bits; info->symmetric = h->symmetric;
+    info->n = h->n; info->device = h->device; info->acc_bits = h->wide ? 64 : h->acc_bits; info->symmetric = h->symmetric;
     info->threads = h->threads; info->units_per_thread = h->upt; info->storage = h->storage;
     info->smem_bytes = (int32_t)h->smem_bytes; info->ctas_per_sm = h->ctas_per_sm; info->sm_count = h->sm_count;
     info->delta_bound = h->delta_bound;
@@ -887,18 +928,22 @@ extern "C" int qapb_all_deltas(qapb_handle *h, const int64_t *perms, int batch, 
     if (!perms || !deltas) return fail(QAPB_ERR_INVALID, "NULL buffer");
     // the full evaluator as a tiled contraction (qap_build_m_kernel) + emission
     cudaStream_t st = (cudaStream_t)stream;
-    const WsPlan w = plan_ws(h, batch, 0);
+    // (a WIDE handle keeps 32-bit state, but the deltas themselves need 64 bits: build M in int64 here)
+    qapb_handle hv = *h;
+    if (h->wide) { hv.acc_bits = 64; hv.wide = 0; }
+    const WsPlan w = plan_ws(&hv, batch, 0);
     rc = ensure_ws(h, w.total);
     if (rc) return rc;
+    hv.ws = h->ws; hv.ws_bytes = h->ws_bytes;
     CU(cudaEventRecord(h->ev0, st));
     BuildParams BP;
     StartParams SP;
     int emitted = 0;
-    rc = launch_build(h, w, batch, 0, 0, 0, 0, nullptr, perms, st, BP, SP, deltas, &emitted);
+    rc = launch_build(&hv, w, batch, 0, 0, 0, 0, nullptr, perms, st, BP, SP, deltas, &emitted);
     if (rc) return rc;
     if (!emitted) {  // tiled build (n > 128): M and h are in the workspace, emit from there
         const dim3 grid(batch, std::min(h->n - 1, 64));
-        if (h->acc_bits == 64) qap_emit_deltas_kernel<int64_t><<<grid, 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
+        if (hv.acc_bits == 64) qap_emit_deltas_kernel<int64_t><<<grid, 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
         else qap_emit_deltas_kernel<int32_t><<<grid, 256, 0, st>>>(h->n, h->npad, BP.M, BP.h, deltas);
         CU(cudaGetLastError());
     }

@@ -207,6 +207,63 @@ __device__ __forceinline__ void admissible_min(int32_t &km, int32_t kd, unsigned
         : "r"(kd), "r"(tbk), "n"(1u << BIT), "r"(thr16));
 }
 
+// ---- WIDE: unsigned 32-bit state, 64-bit deltas --------------------------------------------------
+// Instances whose proven bound on |M| and |h| exceeds 2^31 but not 2^32, with non-negative entries (the
+// tai*b shapes: 2.25e9 at n = 150), keep M and h as UNSIGNED 32-bit values -- every one of them is a
+// non-negative cost, and all updates are exact modulo 2^32 -- in the same registers / shared memory as the
+// int32 plans, so two searches still share an SM.  Only the delta of a pair, M[i][j] + M[j][i] - h[i] - h[j],
+// which needs 34 bits, the aspiration threshold and the argmin are 64-bit.
+template <bool WIDE> struct DeltaT { typedef int32_t type; };
+template <> struct DeltaT<true> { typedef int64_t type; };
+template <typename DT> __device__ __forceinline__ DT delta_max();
+template <> __device__ __forceinline__ int32_t delta_max<int32_t>() { return 0x7fffffff; }
+template <> __device__ __forceinline__ int64_t delta_max<int64_t>() { return 0x7fffffffffffffffLL; }
+__device__ __forceinline__ int64_t wide_delta(int32_t u, int32_t l, int32_t hi, int32_t hj)
+{
+    return (int64_t)(uint32_t)u + (int64_t)(uint32_t)l - (int64_t)(uint32_t)hi - (int64_t)(uint32_t)hj;
+}
+
+__device__ __forceinline__ void unit_select_wide(const int32_t (&U)[4][4], const int32_t (&L)[4][4], unsigned tbk, int Ik,
+                                                 int Jk, int64_t thr, const Vecs &V, int64_t &dbest, int &sbest)
+{
+    int32_t hI[4], hJ[4];
+    ld_vec4(V.H, Ik, hI);
+    ld_vec4(V.H, Jk, hJ);
+    // two running first-minima (rows 0-1 and rows 2-3): a 64-bit value and a slot each -- more chains cost
+    // registers the 128-register plans do not have
+    int64_t rd[2] = {delta_max<int64_t>(), delta_max<int64_t>()};
+    int rs[2] = {0, 8};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t d = wide_delta(U[u][v], L[v][u], hI[u], hJ[v]);
+            const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
+            if (adm && d < rd[u >> 1]) { rd[u >> 1] = d; rs[u >> 1] = u * 4 + v; }
+        }
+    }
+    if (rd[1] < rd[0]) { rd[0] = rd[1]; rs[0] = rs[1]; }
+    dbest = rd[0];
+    sbest = rs[0];
+}
+
+__device__ __forceinline__ void diag_select_wide(const int32_t (&U)[4][4], unsigned tbk, int Ik, int64_t thr, const Vecs &V,
+                                                 int64_t &dbest, int &sbest)
+{
+    int32_t hI[4];
+    ld_vec4(V.H, Ik, hI);
+    dbest = delta_max<int64_t>();
+    sbest = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = u + 1; v < 4; ++v) {
+            const int64_t d = wide_delta(U[u][v], U[v][u], hI[u], hI[v]);
+            const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
+            if (adm && d < dbest) { dbest = d; sbest = u * 4 + v; }
+        }
+}
+
 template <bool PACKED, bool NOTABU>
 __device__ __forceinline__ void unit_select(const int32_t (&U)[4][4], const int32_t (&L)[4][4], unsigned tbk, int Ik,
                                             int Jk, int32_t thr, const Vecs &V, int one, int sixteen,
@@ -403,10 +460,13 @@ __device__ __forceinline__ void expire_bits(unsigned &tb, int32_t &mexp, int c, 
 // argmin is already the result, and 32 independent searches share an SM (size class 32 of the shared-memory
 // layout: 5.6 KB per search).
 template <int SYMM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG, bool DSM = false, bool NOTABU = false,
-          bool REC = true, bool DD = false, bool OW = false>
+          bool REC = true, bool DD = false, bool OW = false, bool WIDE = false>
 __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams P)
 {
     static_assert(!OW || (DD && !STG), "one-warp searches: paired diagonal blocks, no staged matrices");
+    static_assert(!WIDE || !PACKED, "64-bit deltas have no packed keys");
+    typedef typename DeltaT<WIDE>::type delta_t;   // type of a delta, of the aspiration threshold and of the argmin value
+    const delta_t MAXD = delta_max<delta_t>();
     static_assert(!DD || (UR == 1 && !SMEMU && !DSM), "paired diagonal blocks: one register unit per thread");
     constexpr bool SYM = SYMM != 0;       // single-product pass
     constexpr bool FULLSYM = SYMM == 1;   // symmetric closed forms in the publish phase, no transposes
@@ -452,6 +512,9 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     const int32_t *__restrict__ DT = P.DT;
     const int32_t MAXV = 0x7fffffff;
     const int one = P.one, sixteen = P.sixteen;
+    // pad entries: never the minimum, never aspirated (WIDE: 2^32 - 1 as an unsigned value, so that the delta
+    // of a pad pair, 2 (2^32 - 1) - h[i] - h[j], stays positive: the host admits bounds up to 4.0e9 only)
+    const int32_t PADV = WIDE ? (int32_t)0xFFFFFFFFu : PACKED ? (1 << 25) : (1 << 29);
     // STG: int16 copies of D, F (and their transposes when asymmetric) in shared memory, so the
     // publish phase between the barriers never waits on an L1/L2 miss
     const int16_t *sD16 = reinterpret_cast<const int16_t *>(smem_raw + lay.offD16);
@@ -537,14 +600,14 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             unsigned deadA, deadB = 0xffffu;
             const int ddA = 2 * (tid - noff), ddB = ddA + 1 < nb ? ddA + 1 : -1;
             I[0] = ddA; J[0] = ddB; uidv[0] = noff + ddA; own[0] = true;
-            load_unit(Minit, npad, n, ddA, ddA, U[0], tmp, deadA, PACKED ? (1 << 25) : (1 << 29));
+            load_unit(Minit, npad, n, ddA, ddA, U[0], tmp, deadA, PADV);
             deadA |= 0xF731u;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
                 for (int v = 0; v < 4; ++v) L[0][u][v] = 0;
             if (ddB >= 0) {
-                load_unit(Minit, npad, n, ddB, ddB, L[0], tmp, deadB, PACKED ? (1 << 25) : (1 << 29));
+                load_unit(Minit, npad, n, ddB, ddB, L[0], tmp, deadB, PADV);
                 deadB |= 0xF731u;
             }
             tb[0] = deadA | (deadB << 16);
@@ -555,7 +618,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             }
         } else if (own[k]) {
             unsigned dead;
-            load_unit(Minit, npad, n, I[k], J[k], U[k], L[k], dead, PACKED ? (1 << 25) : (1 << 29));
+            load_unit(Minit, npad, n, I[k], J[k], U[k], L[k], dead, PADV);
             if (diag) dead |= 0xF731u;  // slots with u >= v are not pairs of a diagonal block
             tb[k] = dead;
 #pragma unroll
@@ -565,7 +628,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     if (dsm_owner) {
         int32_t Ud[4][4], Ld[4][4];
         unsigned dead;
-        load_unit(Minit, npad, n, dsmI, dsmI, Ud, Ld, dead, PACKED ? (1 << 25) : (1 << 29));
+        load_unit(Minit, npad, n, dsmI, dsmI, Ud, Ld, dead, PADV);
         dead |= 0xF731u;  // slots with u >= v are not pairs of a diagonal block
 #pragma unroll
         for (int u = 0; u < 4; ++u) st_vec4(sDG + 16 * dsmI, u, Ud[u][0], Ud[u][1], Ud[u][2], Ud[u][3]);
@@ -581,7 +644,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 int32_t Us[4][4], Ls[4][4];
                 unsigned dead;
                 const int Ik = P.unit_ij[uid] & 0xff, Jk = P.unit_ij[uid] >> 8;
-                load_unit(Minit, npad, n, Ik, Jk, Us, Ls, dead, PACKED ? (1 << 25) : (1 << 29));
+                load_unit(Minit, npad, n, Ik, Jk, Us, Ls, dead, PADV);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     st_row(sM, k2 * 8 + u, Toff, tid, Us[u]);
@@ -598,7 +661,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
 
     // ------------------------------------------------------------ iterations
     long long best_cost = cost;
-    int32_t thr = 0;  // best_cost - cost, clamped; aspiration <=> delta < thr  (_kernels.pyx:162)
+    delta_t thr = 0;  // best_cost - cost, clamped; aspiration <=> delta < thr  (_kernels.pyx:162)
     const bool tabu = P.mode == MODE_TABU;
     const int iters = P.iterations;
     int steps_done = 0, stopped = 0;
@@ -633,24 +696,24 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         }
 
         // ---------------- pass: update + select over this thread's units
-        int32_t my_d = MAXV;
+        delta_t my_d = MAXD;
         unsigned my_key = 0xffffffffu;
         int my_which = 0, my_slot = 0;  // which: register unit k, or UR + k2 for a shared-memory unit
 #pragma unroll
         for (int k = 0; k < UR; ++k) {
             if (!own[k]) continue;
-            int32_t dk;
+            delta_t dk;
             int sk;
             if (DD && ddiag) {
                 // two diagonal blocks: U = block I (tabu bits 0..15), L = block J (bits 16..31)
                 if (R >= 0) diag_update<SYM>(U[k], I[k], R, S, ru, su, V);
-                diag_select<PACKED>(U[k], tb[k] & 0xffffu, I[k], thr, V, dk, sk);
-                if (dk != MAXV) {
+                if constexpr (WIDE) diag_select_wide(U[k], tb[k] & 0xffffu, I[k], thr, V, dk, sk); else diag_select<PACKED>(U[k], tb[k] & 0xffffu, I[k], thr, V, dk, sk);
+                if (dk != MAXD) {
                     my_d = dk; my_key = pair_key(4 * I[k] + (sk >> 2), 4 * I[k] + (sk & 3), 0); my_slot = sk;
                 }
                 if (J[k] >= 0) {
                     if (R >= 0) diag_update<SYM>(L[k], J[k], R, S, ru, su, V);
-                    diag_select<PACKED>(L[k], tb[k] >> 16, J[k], thr, V, dk, sk);
+                    if constexpr (WIDE) diag_select_wide(L[k], tb[k] >> 16, J[k], thr, V, dk, sk); else diag_select<PACKED>(L[k], tb[k] >> 16, J[k], thr, V, dk, sk);
                     if (dk < my_d) {  // block J comes later in (i, j) order: strict
                         my_d = dk; my_key = pair_key(4 * J[k] + (sk >> 2), 4 * J[k] + (sk & 3), 0); my_slot = 16 + sk;
                     }
@@ -659,12 +722,12 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             }
             if (DD || I[k] != J[k]) {
                 if (R >= 0) unit_update<SYM>(U[k], L[k], I[k], J[k], R, S, ru, su, V);
-                unit_select<PACKED, NOTABU>(U[k], L[k], tb[k], I[k], J[k], thr, V, one, sixteen, dk, sk);
+                if constexpr (WIDE) unit_select_wide(U[k], L[k], tb[k], I[k], J[k], thr, V, dk, sk); else unit_select<PACKED, NOTABU>(U[k], L[k], tb[k], I[k], J[k], thr, V, one, sixteen, dk, sk);
             } else {
                 if (R >= 0) diag_update<SYM>(U[k], I[k], R, S, ru, su, V);
-                diag_select<PACKED>(U[k], tb[k], I[k], thr, V, dk, sk);
+                if constexpr (WIDE) diag_select_wide(U[k], tb[k], I[k], thr, V, dk, sk); else diag_select<PACKED>(U[k], tb[k], I[k], thr, V, dk, sk);
             }
-            if (dk != MAXV) {
+            if (dk != MAXD) {
                 const unsigned key = pair_key(4 * I[k] + (sk >> 2), 4 * J[k] + (sk & 3), 0);
                 if (dk < my_d || (dk == my_d && key < my_key)) { my_d = dk; my_key = key; my_which = k; my_slot = sk; }
             }
@@ -689,10 +752,10 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                         st_row(sM, k2 * 8 + 4 + u, Toff, tid, Ls[u]);
                     }
                 }
-                int32_t dk;
+                delta_t dk;
                 int sk;
-                unit_select<PACKED, NOTABU>(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V, one, sixteen, dk, sk);
-                if (dk != MAXV) {
+                if constexpr (WIDE) unit_select_wide(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V, dk, sk); else unit_select<PACKED, NOTABU>(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V, one, sixteen, dk, sk);
+                if (dk != MAXD) {
                     const unsigned key = pair_key(4 * Ik + (sk >> 2), 4 * Jk + (sk & 3), 0);
                     if (dk < my_d || (dk == my_d && key < my_key)) { my_d = dk; my_key = key; my_which = UR + k2; my_slot = sk; }
                 }
@@ -707,29 +770,30 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
 #pragma unroll
                 for (int u = 0; u < 4; ++u) st_vec4(sDG + 16 * dsmI, u, Ud[u][0], Ud[u][1], Ud[u][2], Ud[u][3]);
             }
-            int32_t dk;
+            delta_t dk;
             int sk;
-            diag_select<PACKED>(Ud, sDGtb[dsmI], dsmI, thr, V, dk, sk);
-            if (dk != MAXV) {
+            if constexpr (WIDE) diag_select_wide(Ud, sDGtb[dsmI], dsmI, thr, V, dk, sk); else diag_select<PACKED>(Ud, sDGtb[dsmI], dsmI, thr, V, dk, sk);
+            if (dk != MAXD) {
                 const unsigned key = pair_key(4 * dsmI + (sk >> 2), 4 * dsmI + (sk & 3), 0);
                 if (dk < my_d || (dk == my_d && key < my_key)) { my_d = dk; my_key = key; my_which = WHICH_DIAG; my_slot = sk; }
             }
         }
 
         if (timing) tB = clock64();
-        int32_t bd = my_d;
+        delta_t bd = my_d;
         unsigned bkey = my_key;
         warp_argmin(bd, bkey);
         if (OW) {
             __syncwarp();  // ------------------------------------------------ sync #1 (one warp: the argmin is final)
         } else {
-            if (lane == 0) { sRedD[warp] = bd; sRedK[warp] = bkey; }
+            delta_t *sRedT = reinterpret_cast<delta_t *>(sRedD);  // 32 x 8 bytes are reserved
+            if (lane == 0) { sRedT[warp] = bd; sRedK[warp] = bkey; }
             __syncthreads();  // ------------------------------------------ sync #1
-            bd = lane < W ? sRedD[lane] : MAXV;
+            bd = lane < W ? sRedT[lane] : MAXD;
             bkey = lane < W ? sRedK[lane] : 0xffffffffu;
             warp_argmin(bd, bkey);
         }
-        if (bd == MAXV) {  // no admissible move: premature stop (_kernels.pyx:168-170)
+        if (bd == MAXD) {  // no admissible move: premature stop (_kernels.pyx:168-170)
             stopped = 1;
             break;
         }
@@ -737,7 +801,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
         cost += (long long)bd;
         const bool improved = cost < best_cost;
         if (improved) best_cost = cost;
-        thr = Acc<int32_t>::clamp_thr(best_cost - cost);
+        thr = Acc<delta_t>::clamp_thr(best_cost - cost);
         steps_done = c;
         R = r >> 2; S = s >> 2; ru = r & 3; su = s & 3;
         // only the publish threads and the owner of the winning pair need the two units

@@ -499,9 +499,12 @@ def test_every_launch_plan_gives_identical_results(q, orc, shape, iters):
             di.set_plan((1, 32, 0, 0) if inst.n > 64 else (2, 4096, 0, 0))
     finally:
         di.close()
-    # instances of the generic kernel have a single configuration
-    big = shapes.by_name("tai45b")
+    # instances of the generic kernel have a single configuration (n > 256 here; tai*b shapes run on the
+    # register / shared-memory plans with 64-bit deltas since round 2)
+    big = shapes.by_name("tai300a")
     assert DeviceInstance(big.flow, big.distance).plan_candidates() == []
+    wide = DeviceInstance(shapes.by_name("tai45b").flow, shapes.by_name("tai45b").distance)
+    assert wide.info["storage"] == 3 and wide.info["acc_bits"] == 64 and len(wide.plan_candidates()) >= 1
 
 
 def test_autotune_installs_the_fastest_plan(q):
@@ -513,7 +516,7 @@ def test_autotune_installs_the_fastest_plan(q):
     assert timings and all(a.evals_per_second >= b.evals_per_second for a, b in zip(timings, timings[1:]))
     di = device_instance(inst.flow, inst.distance)
     assert di.info["threads"] == timings[0].threads
-    assert q.autotune(shapes.by_name("tai45b")) == []
+    assert q.autotune(shapes.by_name("tai300a"), iterations=8, n_starts=8) == []  # generic kernel: one configuration
 
 
 @pytest.mark.parametrize("n", [5, 12, 30, 100, 130])
@@ -642,3 +645,49 @@ def test_budget_sweep_from_one_traced_run(q, orc, shape, algo, starts, budgets):
         rows = q.run_sweep(inst, q.make_sweep("neighborhoods", budgets, cfg), 2)
         for value, rep, cost in rows:
             assert cost == q.run_multistart(inst, replace(cfg, iterations=value, master_seed=77 + rep)).best.cost
+
+
+@pytest.mark.parametrize("n,kind,scale", [(27, 0, 23000), (27, 1, 6000), (27, 2, 12000), (100, 2, 3800), (100, 0, 6600),
+                                          (150, 2, 2600), (150, 1, 1500), (150, 0, 4800), (130, 3, 2900)])
+def test_unsigned_state_with_64_bit_deltas(q, orc, n, kind, scale):
+    """Non-negative instances whose bound exceeds int32 but not 2^32 (tai*b shapes) keep unsigned 32-bit state on the
+    register / shared-memory plans; only deltas, threshold and argmin are 64-bit.  Every plan, every symmetry class
+    (kind 0: none, 1: both, 2: distance only, 3: flow only), tabu with trail and cells, 2opt, all_deltas, multi-start."""
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    rs = np.random.default_rng(7 * n + kind)
+    f = (rs.integers(0, 60, (n, n)) * scale).astype(np.int64)
+    d = rs.integers(0, 60, (n, n)).astype(np.int64)
+    f[rs.random((n, n)) < 0.4] = 0
+    if kind in (1, 2):
+        d = d + d.T
+    if kind in (1, 3):
+        f = f + f.T
+    np.fill_diagonal(f, rs.integers(0, 9, n))
+    np.fill_diagonal(d, rs.integers(0, 5, n))
+    di = DeviceInstance(f, d)
+    try:
+        assert di.info["storage"] == 3 and di.info["acc_bits"] == 64, di.info
+        iters = 40 if n > 100 else 90
+        rng = orc.Rng(orc.derive_seed(n, kind))
+        perm = rng.permutation(n)
+        ten = rng.tenures(1, 4, iters)
+        want = orc.tabu_run(f, d, perm, iters, ten)
+        assert abs(int(np.abs(want[7][2]).max())) > 2 ** 27, "deltas too small to exercise the wide path"
+        for plan in di.plan_candidates() or [None]:
+            if plan is not None:
+                di.set_plan(plan)
+            best, bc, cur, cc, cz, stop, steps, tr, _ = di.tabu(perm, iters, ten)
+            assert np.array_equal(best[0], want[0]) and bc[0] == want[1] and np.array_equal(cur[0], want[2]) and cc[0] == want[3], plan
+            assert np.array_equal(cz[0], want[4]) and steps[0] == want[6] and bool(stop[0]) == want[5], plan
+            for a in range(4):
+                assert np.array_equal(tr[a][0, : want[6]], want[7][a]), (plan, a)
+            for g, w in zip([x[0] for x in di.two_opt(perm, iters)], orc.two_opt_run(f, d, perm, iters)):
+                assert np.array_equal(g, w), plan
+        assert np.array_equal(di.all_deltas(perm)[0], orc.all_deltas(f, d, perm))
+        lo, hi = orc.tenure_bounds(n)
+        got = di.multistart("tabu", 3, 0, 5, iters, lo, hi)
+        w2 = orc.multistart(f, d, "tabu", 3, 5, iters, threads=orc.max_threads())
+        assert np.array_equal(got[0], w2[0]) and got[1:3] == (w2[1], w2[2]) and np.array_equal(got[3], w2[3])
+    finally:
+        di.close()
