@@ -231,7 +231,7 @@ def run_reference(args) -> None:
 # ------------------------------------------------------------------------ GPU arm --
 def _nccl_log_setup(rank: int) -> str | None:
     """Leave NCCL's communicator log on (NVLS / ring / tree choice is the evidence the judge reads)."""
-    if "NCCL_DEBUG" in os.environ:
+    if os.environ.get("QAPB_KEEP_NCCL_DEBUG") == "1":  # the caller's own NCCL_DEBUG settings stay
         return os.environ.get("NCCL_DEBUG_FILE")
     out_dir = os.path.join(ROOT, "gpurun_out")
     if not os.path.isdir(out_dir):
@@ -321,8 +321,14 @@ def run_ours(args) -> None:
     dev = torch.device("cuda", local)
     grouped = "RANK" in os.environ  # under torchrun: NCCL group even for one rank, so the collective really runs
     nccl_log = None
+    saved_stdout = None
     if grouped:
         nccl_log = _nccl_log_setup(rank)
+        # NCCL writes its version banner to stdout when the communicator comes up (first collective): keep
+        # stdout clean for the one JSON line by parking it until the warm-up steps are done
+        sys.stdout.flush()
+        saved_stdout = os.dup(1)
+        os.dup2(os.open(os.devnull, os.O_WRONLY), 1)
         dist.init_process_group("nccl", device_id=dev)
     ten = q.tenure_bounds(n)
     di = device_instance(inst.flow, inst.distance, local)
@@ -349,6 +355,10 @@ def run_ours(args) -> None:
     for w in range(args.warmup):
         step(1000 + w)
     barrier()
+    if saved_stdout is not None:
+        sys.stdout.flush()
+        os.dup2(saved_stdout, 1)
+        os.close(saved_stdout)
     sampler = ClockSampler(local)
     if rank == 0:
         sampler.start()

@@ -89,12 +89,13 @@ def autotune(inst: Instance, *, algorithm: str = "tabu", n_starts: int | None = 
         di.set_plan(plan)
         # fill every SM for two waves under this plan unless the caller fixed the batch
         count = n_starts if n_starts is not None else 2 * sm * max(1, di.info["ctas_per_sm"])
-        best = None
+        best, steps = None, 0
         for rep in range(max(1, repeats)):
             di.multistart(algorithm, rep, 0, count, iters, ten.low, ten.high)
             ms = di.last_kernel_ms()
-            best = ms if best is None else min(best, ms)
-        evals = count * iters * inst.n * (inst.n - 1) // 2
+            if best is None or ms < best:
+                best, steps = ms, di.last_total_steps()  # a tabu start can stop early: count the steps it did
+        evals = steps * inst.n * (inst.n - 1) // 2
         timings.append(PlanTiming(plan, di.info["threads"], di.info["ctas_per_sm"], best, evals / (best * 1e-3)))
     timings.sort(key=lambda t: -t.evals_per_second)
     if not timings:

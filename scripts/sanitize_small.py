@@ -32,10 +32,23 @@ for _n, _which in ((23, "dist"), (40, "flow"), (132, "dist")):
     _inst = Instance(f"onesym{_n}{_which}", _n, _f, _d)
     _res = q.run_multistart(_inst, q.SearchConfig(algorithm="tabu", n_starts=3, iterations=12, master_seed=1))
     print(_inst.name, _res.best.cost, q.backend.device_instance(_f, _d).info["threads"])
-# generic kernel: int64 state (tai*b), forced int32, M in L2, masks in L2
+# every candidate plan of a small and a mid-size instance (paired diagonal blocks, one-warp searches, ...)
+from paper_2307_11248_b200.backend import device_instance as _di
+for name in ("tai30a", "rand23", "tai100a"):
+    inst = shapes.by_name(name)
+    d = _di(inst.flow, inst.distance)
+    for plan in d.plan_candidates():
+        d.set_plan(plan)
+        out = d.multistart("tabu", 1, 0, 3, 10, 1, 3)
+        print(name, plan, out[1], "threads", d.info["threads"])
+    clear_cache()
+# tai*b shapes: unsigned 32-bit state with 64-bit deltas on the hybrid plans (n = 45: registers; n = 150: shared-memory units)
 run("tai45b")
+run("tai150b", starts=2, iters=6)
+# generic kernel: int64 state (tai*b forced off the hybrid plans), forced int32, M in L2, masks in L2
 os.environ["QAPB_FORCE_GENERIC"] = "1"
 clear_cache()
+run("tai45b")
 run("tai30a")
 for st in ("1", "2"):
     os.environ["QAPB_FORCE_STORAGE"] = st
