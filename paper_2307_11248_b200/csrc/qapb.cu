@@ -80,6 +80,8 @@ typedef void (*kern_t)(const SearchParams);
 #define QAPB_DEV_ARGS 1, true, 1, false, false, 64, false, false, false, true, true
 #elif QAPB_DEV_ONLY == 9 // tai150b: 64-bit deltas over unsigned 32-bit state, shared-memory plan with DSM, one symmetric matrix
 #define QAPB_DEV_ARGS 2, false, 2, true, false, 128, true, false, true, false, false, true
+#elif QAPB_DEV_ONLY == 12 // preset 1 at 88 registers (still two 352-thread CTAs per SM)
+#define QAPB_DEV_ARGS 1, true, 1, false, true, 88, false, false, false
 #elif QAPB_DEV_ONLY == 5 // recording instantiation of preset 4
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 64, false, false, true, true
 #elif QAPB_DEV_ONLY == 3 // recording instantiation of preset 1 (single-run entries: parity tests)
@@ -87,7 +89,7 @@ typedef void (*kern_t)(const SearchParams);
 #endif
 static kern_t pick_kernel(int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
 static kern_t pick_hybrid_kernel(int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
-static kern_t multistart_kernel(int, int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
+static kern_t multistart_kernel(int, int, int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
 static kern_t pick_wide_kernel(int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
 #else
 static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
@@ -151,10 +153,14 @@ static kern_t pick_hybrid_kernel(int symm, int packed, int plan)
 // Multi-start instantiations of the two plans the benchmarks use (the staged one-register-unit plan and
 // the shared-memory plan with DSM; packed keys; both matrices symmetric or neither): no trail / cells
 // code, and for 2opt a selection without tabu bits.  null = use the common kernel.
-static kern_t multistart_kernel(int symm, int packed, int plan, int two_opt)
+// (regs88: the staged one-register-unit plan compiled for 88 instead of 80 registers -- ptxas schedules the pass
+// with more values in flight: n = 100 tabu 852 -> 878, 2opt 895 -> 918, sko100 812 -> 836 G evals/s -- used when it
+// costs no resident CTA, and for two symmetric matrices only: the two-product kernel LOSES at 88 (rand100 670 -> 467).)
+static kern_t multistart_kernel(int symm, int packed, int plan, int two_opt, int regs88)
 {
     if (!packed || symm > 1) return nullptr;
-#define KM(S, NT) (plan == 1 ? (kern_t) qap_search_hybrid_kernel<S, true, 1, false, true, 80, false, NT, false> \
+#define KM(S, NT) (plan == 1 ? ((regs88 && S == 1) ? (kern_t) qap_search_hybrid_kernel<1, true, 1, false, true, 88, false, NT, false> \
+                                       : (kern_t) qap_search_hybrid_kernel<S, true, 1, false, true, 80, false, NT, false>) \
                    : plan == 7 ? (kern_t) qap_search_hybrid_kernel<S, true, 1, false, true, 64, false, NT, false, true> \
                    : plan == 8 ? (kern_t) qap_search_hybrid_kernel<S, true, 1, false, false, 64, false, NT, false, true, true> \
                              : (kern_t) qap_search_hybrid_kernel<S, true, 2, true, false, 128, true, NT, false>)
@@ -174,8 +180,12 @@ static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_op
     if (h->dd) plan = h->ow ? 8 : h->staged ? 7 : 6;
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
     if (h->storage == 3 && h->wide) return pick_wide_kernel(symm, plan);
-    if (multistart && h->storage == 3)
-        if (kern_t k2 = multistart_kernel(symm, packed, plan, two_opt)) return k2;
+    if (multistart && h->storage == 3) {
+        // 88 registers per thread where that keeps as many CTAs resident as 80 do
+        const int warps = h->threads / 32, by_smem = (int)(233472u / (h->smem_bytes + 1024u));
+        const int c80 = std::min(by_smem, 65536 / (warps * 32 * 80)), c88 = std::min(by_smem, 65536 / (warps * 32 * 88));
+        if (kern_t k2 = multistart_kernel(symm, packed, plan, two_opt, c88 >= c80 && !getenv("QAPB_NO_REGS88"))) return k2;
+    }
     return h->storage == 3 ? pick_hybrid_kernel(symm, packed, plan)
                            : pick_kernel(h->acc_bits, h->storage, h->lb_class);
 }
@@ -865,7 +875,7 @@ static int launch_build(qapb_handle *h, const WsPlan &w, int batch, int rng, int
 
 // Launch start + build + search kernels for `batch` starts.  `extra_ws` bytes are reserved at
 // the start of the workspace for the caller (multistart keeps best perms there).
-static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extra_ws, cudaStream_t st)
+static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extra_ws, cudaStream_t st, bool first_wave = true)
 {
     const WsPlan w = plan_ws(h, batch, extra_ws);
     int rc = ensure_ws(h, w.total);
@@ -886,7 +896,7 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     }
     // several handles share one kernel instantiation: its opt-in size is the maximum requested so far
     CU(ensure_smem_optin((const void *)kern, h->device, h->smem_bytes));
-    CU(cudaEventRecord(h->ev0, st));
+    if (first_wave) CU(cudaEventRecord(h->ev0, st));
     // start permutations (+ stream state), then M and h as one batched tiled integer product
     BuildParams BP;
     StartParams SP;
@@ -1021,17 +1031,38 @@ extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, u
     P.first_index = first_index;
     P.ten_lo = ten_low;
     P.ten_hi = ten_high;
+    // The per-start workspace (initial M, permutations, M in L2 for large n) grows with the batch: the reference's
+    // default of 6144 starts on a large int64 instance would ask for tens of GB.  The starts are therefore run in
+    // waves sized to a memory budget (free memory / 2, at most 8 GiB; QAPB_WAVE_BYTES overrides), each a whole number
+    // of resident CTA sets; per-start results land in the caller's arrays at their offsets and one reduction
+    // follows.  A batch that fits (every benchmark shape) is a single wave.
+    size_t budget = (size_t)8 << 30, free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) budget = std::min(budget, (free_b + h->ws_bytes) / 2);
+    if (const char *wb = getenv("QAPB_WAVE_BYTES")) budget = (size_t)strtoull(wb, nullptr, 10);
+    int wave = count;
+    if (plan_ws(h, count, head).total > budget) {
+        const size_t per_start = (plan_ws(h, 1024, head).total - plan_ws(h, 0, head).total) / 1024 + 1;
+        const size_t room = budget > plan_ws(h, 0, head).total ? budget - plan_ws(h, 0, head).total : 0;
+        const int set = std::max(1, h->sm_count * std::max(1, h->ctas_per_sm ? h->ctas_per_sm : 1));
+        wave = (int)std::min<size_t>((size_t)count, std::max<size_t>(1, room / per_start));
+        if (wave > set) wave -= wave % set;
+    }
     // size the whole workspace first so the head pointers stay valid
-    rc = ensure_ws(h, plan_ws(h, count, head).total);
+    rc = ensure_ws(h, plan_ws(h, wave, head).total);
     if (rc) return rc;
     int64_t *w_best = (int64_t *)h->ws;
     int64_t *w_cur = (int64_t *)((char *)h->ws + perm_bytes);
     int64_t *w_curcost = (int64_t *)((char *)h->ws + 2 * perm_bytes);
     int64_t *w_steps = w_curcost + count;
-    P.best = w_best; P.best_cost = per_start_costs; P.cur = w_cur; P.cur_cost = w_curcost;
-    P.steps = w_steps;
-    rc = launch_search(h, P, count, head, (cudaStream_t)stream);
-    if (rc) return rc;
+    for (int off = 0; off < count; off += wave) {
+        const int cnt = std::min(wave, count - off);
+        P.first_index = first_index + (uint64_t)off;
+        P.best = w_best + (size_t)off * n; P.best_cost = per_start_costs + off; P.cur = w_cur + (size_t)off * n;
+        P.cur_cost = w_curcost + off;
+        P.steps = w_steps + off;
+        rc = launch_search(h, P, cnt, head, (cudaStream_t)stream, off == 0);
+        if (rc) return rc;
+    }
     h->steps_total_off = (size_t)((char *)(w_steps + count) - (char *)h->ws);
     qap_pick_best_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(count, n, first_index, per_start_costs, w_best, best_key, best_perm,
                                                                w_steps, w_steps + count);

@@ -691,3 +691,27 @@ def test_unsigned_state_with_64_bit_deltas(q, orc, n, kind, scale):
         assert np.array_equal(got[0], w2[0]) and got[1:3] == (w2[1], w2[2]) and np.array_equal(got[3], w2[3])
     finally:
         di.close()
+
+
+def test_multistart_runs_in_waves_under_a_memory_budget(q, orc, monkeypatch):
+    """qapb_multistart splits a batch whose per-start workspace exceeds the memory budget into waves (the reference's
+    default of 6144 starts on a large instance would otherwise ask for tens of GB); the result is the same."""
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    for name, starts, iters, budget in (("tai30a", 64, 40, 100_000), ("tai45b", 23, 30, 120_000), ("tai300a", 7, 3, 3_000_000)):
+        inst = shapes.by_name(name)
+        lo, hi = orc.tenure_bounds(inst.n)
+        want = orc.multistart(inst.flow, inst.distance, "tabu", 9, starts, iters, threads=orc.max_threads())
+        monkeypatch.setenv("QAPB_WAVE_BYTES", str(budget))
+        di = DeviceInstance(inst.flow, inst.distance)
+        try:
+            got = di.multistart("tabu", 9, 0, starts, iters, lo, hi)
+            assert np.array_equal(got[0], want[0]) and got[1:3] == (want[1], want[2]) and np.array_equal(got[3], want[3]), name
+            assert di.last_total_steps() == starts * iters
+            # a shard that does not start at index 0
+            got = di.multistart("tabu", 9, 5, starts - 5, iters, lo, hi)
+            assert np.array_equal(got[0], want[0][5:]), name
+        finally:
+            di.close()
+        monkeypatch.delenv("QAPB_WAVE_BYTES")
