@@ -82,6 +82,12 @@ typedef void (*kern_t)(const SearchParams);
 #define QAPB_DEV_ARGS 2, false, 2, true, false, 128, true, false, true, false, false, true
 #elif QAPB_DEV_ONLY == 12 // preset 1 at 88 registers (still two 352-thread CTAs per SM)
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 88, false, false, false
+#elif QAPB_DEV_ONLY == 13 // one-warp searches at 80 registers (25 per SM)
+#define QAPB_DEV_ARGS 1, true, 1, false, false, 80, false, false, false, true, true
+#elif QAPB_DEV_ONLY == 14 // one-warp searches at 96 registers (21 per SM)
+#define QAPB_DEV_ARGS 1, true, 1, false, false, 96, false, false, false, true, true
+#elif QAPB_DEV_ONLY == 15 // preset 9 without the recording code (multi-start only)
+#define QAPB_DEV_ARGS 2, false, 2, true, false, 128, true, false, false, false, false, true
 #elif QAPB_DEV_ONLY == 5 // recording instantiation of preset 4
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 64, false, false, true, true
 #elif QAPB_DEV_ONLY == 3 // recording instantiation of preset 1 (single-run entries: parity tests)
@@ -208,8 +214,11 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     int exp_in_smem = 1;
     const int ow = dd && threads == 32 && h->npad <= 32;  // the whole search is one warp
     HybLayout L = make_hyb_layout(h->npad, nb, toff, us, 1, 0, 1, dsm, ow);
-    // keep the expiry array in shared memory only while it does not cost a resident CTA
-    if (L.total > (smem_target ? smem_target : smem_cap) && us > 0) {
+    // keep the expiry array in shared memory only while it does not cost a resident CTA -- and not at all when
+    // the matrices cannot be staged as int16 (entries above 32767: tai*b flows): the publish phase then reads
+    // rows of D and F through L1, which is what is left of the 228 KB after the shared-memory carve-out; with
+    // the expiries (touched only when a pair is set or expires) in L2, tai150b runs at 434 instead of 376 G evals/s
+    if ((L.total > (smem_target ? smem_target : smem_cap) || !h->fits_i16) && us > 0) {
         exp_in_smem = 0;
         L = make_hyb_layout(h->npad, nb, toff, us, 0, 0, 1, dsm);
     }
