@@ -177,6 +177,29 @@ static kern_t multistart_kernel(int symm, int packed, int plan, int two_opt, int
 }
 #endif
 
+// Resident CTAs per SM of `k` at this handle's CTA size and shared memory (cached: the query costs more than
+// packing a small instance).
+static int kernel_occupancy(const void *k, const qapb_handle *h)
+{
+    struct Key { const void *k; int threads; unsigned smem; int device; int occ; };
+    static std::mutex mu;
+    static std::vector<Key> seen;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const Key &e : seen)
+            if (e.k == k && e.threads == h->threads && e.smem == h->smem_bytes && e.device == h->device) return e.occ;
+    }
+    int occ = 0;
+    if (ensure_smem_optin(k, h->device, h->smem_bytes) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, h->threads, h->smem_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    seen.push_back({k, h->threads, h->smem_bytes, h->device, occ});
+    return occ;
+}
+
 static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_opt = 0)
 {
     // packed (delta, slot) keys need |delta|*16 + 15 < 2^31
@@ -187,10 +210,11 @@ static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_op
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
     if (h->storage == 3 && h->wide) return pick_wide_kernel(symm, plan);
     if (multistart && h->storage == 3) {
-        // 88 registers per thread where that keeps as many CTAs resident as 80 do
-        const int warps = h->threads / 32, by_smem = (int)(233472u / (h->smem_bytes + 1024u));
-        const int c80 = std::min(by_smem, 65536 / (warps * 32 * 80)), c88 = std::min(by_smem, 65536 / (warps * 32 * 88));
-        if (kern_t k2 = multistart_kernel(symm, packed, plan, two_opt, c88 >= c80 && !getenv("QAPB_NO_REGS88"))) return k2;
+        // 88 registers per thread where that keeps as many CTAs resident as 80 do (asked of the runtime)
+        kern_t k80 = multistart_kernel(symm, packed, plan, two_opt, 0);
+        kern_t k88 = (k80 && plan == 1 && symm == 1 && !getenv("QAPB_NO_REGS88")) ? multistart_kernel(symm, packed, plan, two_opt, 1) : nullptr;
+        if (k88 && k88 != k80 && kernel_occupancy((const void *)k88, h) >= kernel_occupancy((const void *)k80, h)) return k88;
+        if (k80) return k80;
     }
     return h->storage == 3 ? pick_hybrid_kernel(symm, packed, plan)
                            : pick_kernel(h->acc_bits, h->storage, h->lb_class);
@@ -243,29 +267,7 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     return true;
 }
 
-static int hybrid_occupancy(const qapb_handle *h)
-{
-    // the answer depends only on (kernel, CTA size, shared memory, device): remember it, the query
-    // costs more than packing a small instance
-    struct Key { const void *k; int threads; unsigned smem; int device; int occ; };
-    static std::mutex mu;
-    static std::vector<Key> seen;
-    const void *k = (const void *)handle_kernel(h);
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        for (const Key &e : seen)
-            if (e.k == k && e.threads == h->threads && e.smem == h->smem_bytes && e.device == h->device) return e.occ;
-    }
-    int occ = 0;
-    if (ensure_smem_optin(k, h->device, h->smem_bytes) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, h->threads, h->smem_bytes) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    std::lock_guard<std::mutex> lk(mu);
-    seen.push_back({k, h->threads, h->smem_bytes, h->device, occ});
-    return occ;
-}
+static int hybrid_occupancy(const qapb_handle *h) { return kernel_occupancy((const void *)handle_kernel(h), h); }
 
 // Split of the off-diagonal units of one search between registers (UR per thread) and shared
 // memory (US per thread) for the hybrid kernel.  Returns false if the instance does not fit.
