@@ -1048,10 +1048,14 @@ extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, u
     // of resident CTA sets; per-start results land in the caller's arrays at their offsets and one reduction
     // follows.  A batch that fits (every benchmark shape) is a single wave.
     size_t budget = (size_t)8 << 30, free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) budget = std::min(budget, (free_b + h->ws_bytes) / 2);
+    const size_t need = plan_ws(h, count, head).total;
+    // (cudaMemGetInfo costs milliseconds: only batches of a GiB and more, that do not fit the workspace the
+    // handle already holds, ask)
+    if (need > h->ws_bytes && need > ((size_t)1 << 30) && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+        budget = std::min(budget, (free_b + h->ws_bytes) / 2);
     if (const char *wb = getenv("QAPB_WAVE_BYTES")) budget = (size_t)strtoull(wb, nullptr, 10);
     int wave = count;
-    if (plan_ws(h, count, head).total > budget) {
+    if (need > budget) {
         const size_t per_start = (plan_ws(h, 1024, head).total - plan_ws(h, 0, head).total) / 1024 + 1;
         const size_t room = budget > plan_ws(h, 0, head).total ? budget - plan_ws(h, 0, head).total : 0;
         const int set = std::max(1, h->sm_count * std::max(1, h->ctas_per_sm ? h->ctas_per_sm : 1));
