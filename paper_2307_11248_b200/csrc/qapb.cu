@@ -8,6 +8,7 @@
 #include "search_kernel.cuh"
 #include "build_kernels.cuh"
 #include "search_hybrid.cuh"
+#include "search_warp.cuh"
 
 #include <algorithm>
 #include <array>
@@ -48,6 +49,8 @@ struct qapb_handle {
     int dd = 0;                                    // hybrid: diagonal blocks paired in the registers of the threads after the last unit
     int ow = 0;                                    // hybrid: the search is one warp (n <= 32 with dd)
     int wide = 0;                                  // hybrid: unsigned 32-bit state with 64-bit deltas (acc_bits holds the STATE width, 32)
+    int wk = 0;                                    // one warp per search, state in shared memory (search_warp.cuh; n <= 32)
+    int wpc = 1;                                   // ... searches (warps) per CTA
     unsigned smem_bytes = 0;
     int ctas_per_sm = 0, sm_count = 0;
     long long delta_bound = 0;
@@ -92,11 +95,25 @@ typedef void (*kern_t)(const SearchParams);
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 64, false, false, true, true
 #elif QAPB_DEV_ONLY == 3 // recording instantiation of preset 1 (single-run entries: parity tests)
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 80
+#elif QAPB_DEV_ONLY == 20 // one warp per search (search_warp.cuh), symmetric, multi-start tabu
+#define QAPB_DEV_WARP 1, false, false
+#elif QAPB_DEV_ONLY == 21 // ... recording instantiation
+#define QAPB_DEV_WARP 1, false, true
+#elif QAPB_DEV_ONLY == 22 // ... multi-start 2opt
+#define QAPB_DEV_WARP 1, true, false
+#elif QAPB_DEV_ONLY == 23 // ... asymmetric recording instantiation
+#define QAPB_DEV_WARP 0, false, true
 #endif
-static kern_t pick_kernel(int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
-static kern_t pick_hybrid_kernel(int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
-static kern_t multistart_kernel(int, int, int, int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
-static kern_t pick_wide_kernel(int, int) { return (kern_t) qap_search_hybrid_kernel<QAPB_DEV_ARGS>; }
+#ifdef QAPB_DEV_WARP
+#define QAPB_DEV_KERNEL qap_search_warp_kernel<QAPB_DEV_WARP>
+#else
+#define QAPB_DEV_KERNEL qap_search_hybrid_kernel<QAPB_DEV_ARGS>
+#endif
+static kern_t pick_kernel(int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
+static kern_t pick_hybrid_kernel(int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
+static kern_t multistart_kernel(int, int, int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
+static kern_t pick_wide_kernel(int, int) { return (kern_t) QAPB_DEV_KERNEL; }
+static kern_t pick_warp_kernel(int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
 #else
 static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
 {
@@ -175,6 +192,14 @@ static kern_t multistart_kernel(int symm, int packed, int plan, int two_opt, int
     return symm ? KM(1, false) : KM(0, false);
 #undef KM
 }
+// One warp per search (search_warp.cuh): recording instantiations for the single-run entries, and multi-start
+// instantiations (tabu / 2opt) without the recording code.
+static kern_t pick_warp_kernel(int symm, int multistart, int two_opt)
+{
+    if (!multistart) return symm ? (kern_t) qap_search_warp_kernel<1, false, true> : (kern_t) qap_search_warp_kernel<0, false, true>;
+    if (two_opt) return symm ? (kern_t) qap_search_warp_kernel<1, true, false> : (kern_t) qap_search_warp_kernel<0, true, false>;
+    return symm ? (kern_t) qap_search_warp_kernel<1, false, false> : (kern_t) qap_search_warp_kernel<0, false, false>;
+}
 #endif
 
 // Resident CTAs per SM of `k` at this handle's CTA size and shared memory (cached: the query costs more than
@@ -208,6 +233,7 @@ static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_op
     if (h->dsm) plan = 5;
     if (h->dd) plan = h->ow ? 8 : h->staged ? 7 : 6;
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
+    if (h->storage == 3 && h->wk) return pick_warp_kernel(h->symmetric ? 1 : 0, multistart, two_opt);
     if (h->storage == 3 && h->wide) return pick_wide_kernel(symm, plan);
     if (multistart && h->storage == 3) {
         // 88 registers per thread where that keeps as many CTAs resident as 80 do (asked of the runtime)
@@ -226,6 +252,20 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
                             unsigned smem_target = 0)
 {
     const int nb = h->nb, dw = (nb + 31) / 32;
+    if (ur == 0) {
+        // one warp per search, the whole state in the warp's slice of shared memory (search_warp.cuh): n <= 32,
+        // int32 state with packed selection keys
+        if (h->npad > 32 || h->wide || h->acc_bits != 32 || h->delta_bound >= ((1LL << 27) - 1)) return false;
+        int wpc = 1;
+        if (const char *e = getenv("QAPB_WPC")) wpc = std::min(8, std::max(1, atoi(e)));
+        h->wk = 1; h->wpc = wpc;
+        h->staged = 0; h->dsm = 0; h->dd = 0; h->ow = 0;
+        h->upt = 1; h->toff = 32; h->us = 0; h->exp_in_smem = 1;
+        h->threads = 32 * wpc;
+        h->lb_class = 0;
+        h->smem_bytes = (unsigned)WK_TOTAL * (unsigned)wpc;
+        return h->smem_bytes <= smem_cap;
+    }
     const int dd = dsm == 2;  // diagonal blocks paired in registers: no dedicated warps, toff counts every thread
     if (dd) dsm = 0;
     if (h->wide && (dd || (ur == 2 && !dsm))) return false;  // 64-bit deltas: plans 0 / 1 / 5 only
@@ -260,6 +300,7 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     h->dsm = dsm;
     h->dd = dd;
     h->ow = ow;
+    h->wk = 0; h->wpc = 1;
     h->upt = ur; h->toff = toff; h->us = us; h->exp_in_smem = exp_in_smem;
     h->threads = threads;
     h->lb_class = 0;
@@ -284,6 +325,8 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
         if (sscanf(pl, "%d,%d,%d,%d,%d", &a, &b, &c, &d, &e) >= 3 && (a == 1 || a == 2) && b % 32 == 0 && b >= 0 && c >= 0)
             return try_hybrid_plan(h, smem_cap, a, b, c, d, (unsigned)e * 1024u);
     }
+    // n <= 32: one warp per search (no block barriers, no register-indexed fix-ups)
+    if (!getenv("QAPB_NO_WARP") && try_hybrid_plan(h, smem_cap, 0, 32, 0)) return true;
     if (nb > 32) {
         // n = 129..256: every warp on off-diagonal units (two in registers + the rest in shared memory per
         // thread), the diagonal blocks in shared memory with the last nb threads (DSM).  Preferred: 256
@@ -335,6 +378,7 @@ static std::vector<std::array<int, 4>> hybrid_candidates(const qapb_handle *h)
             if (c[0] == ur && c[1] == toff && c[2] == us && c[3] == dsm) return;
         out.push_back({ur, toff, us, dsm});
     };
+    if (h->npad <= 32 && !h->wide && h->acc_bits == 32 && h->delta_bound < ((1LL << 27) - 1)) out.push_back({0, 32, 0, 0});
     if (nb > 32) {
         for (int t : {256, 384, 512}) add(2, t, std::max(1, (noff - 2 * t + t - 1) / t), 1);
         const int toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
@@ -914,7 +958,9 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     rc = launch_build(h, w, batch, P.rng, P.force_seq_rng, P.master_seed, P.first_index, P.seeds, P.perms, st, BP, SP);
     if (rc) return rc;
     P.perm32 = SP.perm32; P.start_state = SP.state; P.initM = BP.M; P.initH = BP.h;
-    kern<<<batch, h->threads, h->smem_bytes, st>>>(P);
+    P.batch = batch;
+    if (h->wk) kern<<<(batch + h->wpc - 1) / h->wpc, h->threads, h->smem_bytes, st>>>(P);  // wpc searches per CTA
+    else kern<<<batch, h->threads, h->smem_bytes, st>>>(P);
     CU(cudaGetLastError());
     CU(cudaEventRecord(h->ev1, st));
     h->have_timing = 1;
@@ -1178,7 +1224,7 @@ extern "C" int qapb_set_plan(qapb_handle *h, int reg_units, int unit_threads, in
     if (h->have_timing) CU(cudaEventSynchronize(h->ev1));  // no launch of the old plan in flight
     qapb_handle probe = *h;
     const unsigned target = (diag_in_smem == 1 && unit_threads <= 256) ? 113u * 1024u : 0u;
-    if ((reg_units != 1 && reg_units != 2) || unit_threads < 0 || unit_threads % 32 != 0 || smem_units < 0 ||
+    if ((reg_units != 0 && reg_units != 1 && reg_units != 2) || unit_threads < 0 || unit_threads % 32 != 0 || smem_units < 0 ||
         !try_hybrid_plan(&probe, device_smem_cap(h->device), reg_units, unit_threads, smem_units, diag_in_smem, target))
         return fail(QAPB_ERR_INVALID, "plan {" + std::to_string(reg_units) + ", " + std::to_string(unit_threads) + ", " +
                                           std::to_string(smem_units) + ", " + std::to_string(diag_in_smem) + "} does not fit this instance");

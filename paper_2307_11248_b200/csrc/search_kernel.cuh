@@ -109,6 +109,7 @@ struct SearchParams {
     int toff, us, exp_in_smem;       // hybrid plan: off-diagonal threads, shared-memory units per thread
     int staged;                      // hybrid: int16 copies of D, F (and transposes) staged in shared memory
     int dsm;                         // hybrid: diagonal blocks in shared memory, owned by the last nb threads
+    int batch;                       // searches of this launch (search_warp.cuh packs several into a CTA)
 };
 
 // ---- accumulator traits -----------------------------------------------------
