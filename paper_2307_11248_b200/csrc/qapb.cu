@@ -49,8 +49,8 @@ struct qapb_handle {
     int dd = 0;                                    // hybrid: diagonal blocks paired in the registers of the threads after the last unit
     int ow = 0;                                    // hybrid: the search is one warp (n <= 32 with dd)
     int wide = 0;                                  // hybrid: unsigned 32-bit state with 64-bit deltas (acc_bits holds the STATE width, 32)
-    int wk = 0;                                    // one warp per search, state in shared memory (search_warp.cuh; n <= 32)
-    int wpc = 1;                                   // ... searches (warps) per CTA
+    int wk = 0;                                    // lanes per search (32, or 16 at n <= 16) of the warp kernel (search_warp.cuh; n <= 32), 0 = other plans
+    int wpc = 1;                                   // ... warps per CTA
     unsigned smem_bytes = 0;
     int ctas_per_sm = 0, sm_count = 0;
     long long delta_bound = 0;
@@ -96,13 +96,19 @@ typedef void (*kern_t)(const SearchParams);
 #elif QAPB_DEV_ONLY == 3 // recording instantiation of preset 1 (single-run entries: parity tests)
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 80
 #elif QAPB_DEV_ONLY == 20 // one warp per search (search_warp.cuh), symmetric, multi-start tabu
-#define QAPB_DEV_WARP 1, false, false
+#define QAPB_DEV_WARP 1, false, false, 32
 #elif QAPB_DEV_ONLY == 21 // ... recording instantiation
-#define QAPB_DEV_WARP 1, false, true
+#define QAPB_DEV_WARP 1, false, true, 32
 #elif QAPB_DEV_ONLY == 22 // ... multi-start 2opt
-#define QAPB_DEV_WARP 1, true, false
+#define QAPB_DEV_WARP 1, true, false, 32
 #elif QAPB_DEV_ONLY == 23 // ... asymmetric recording instantiation
-#define QAPB_DEV_WARP 0, false, true
+#define QAPB_DEV_WARP 0, false, true, 32
+#elif QAPB_DEV_ONLY == 24 // ... two searches per warp (n <= 16), multi-start tabu
+#define QAPB_DEV_WARP 1, false, false, 16
+#elif QAPB_DEV_ONLY == 25 // ... two searches per warp, recording instantiation
+#define QAPB_DEV_WARP 1, false, true, 16
+#elif QAPB_DEV_ONLY == 26 // ... two searches per warp, asymmetric recording instantiation
+#define QAPB_DEV_WARP 0, false, true, 16
 #endif
 #ifdef QAPB_DEV_WARP
 #define QAPB_DEV_KERNEL qap_search_warp_kernel<QAPB_DEV_WARP>
@@ -113,7 +119,7 @@ static kern_t pick_kernel(int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
 static kern_t pick_hybrid_kernel(int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
 static kern_t multistart_kernel(int, int, int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
 static kern_t pick_wide_kernel(int, int) { return (kern_t) QAPB_DEV_KERNEL; }
-static kern_t pick_warp_kernel(int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
+static kern_t pick_warp_kernel(int, int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
 #else
 static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
 {
@@ -194,11 +200,15 @@ static kern_t multistart_kernel(int symm, int packed, int plan, int two_opt, int
 }
 // One warp per search (search_warp.cuh): recording instantiations for the single-run entries, and multi-start
 // instantiations (tabu / 2opt) without the recording code.
-static kern_t pick_warp_kernel(int symm, int multistart, int two_opt)
+static kern_t pick_warp_kernel(int symm, int multistart, int two_opt, int lanes)
 {
-    if (!multistart) return symm ? (kern_t) qap_search_warp_kernel<1, false, true> : (kern_t) qap_search_warp_kernel<0, false, true>;
-    if (two_opt) return symm ? (kern_t) qap_search_warp_kernel<1, true, false> : (kern_t) qap_search_warp_kernel<0, true, false>;
-    return symm ? (kern_t) qap_search_warp_kernel<1, false, false> : (kern_t) qap_search_warp_kernel<0, false, false>;
+#define KW3(G) {{(kern_t) qap_search_warp_kernel<0, false, true, G>, (kern_t) qap_search_warp_kernel<0, false, false, G>, \
+                 (kern_t) qap_search_warp_kernel<0, true, false, G>},                                                     \
+                {(kern_t) qap_search_warp_kernel<1, false, true, G>, (kern_t) qap_search_warp_kernel<1, false, false, G>, \
+                 (kern_t) qap_search_warp_kernel<1, true, false, G>}}
+    static kern_t tab[2][2][3] = {KW3(32), KW3(16)};
+#undef KW3
+    return tab[lanes == 16][symm != 0][!multistart ? 0 : two_opt ? 2 : 1];
 }
 #endif
 
@@ -233,7 +243,7 @@ static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_op
     if (h->dsm) plan = 5;
     if (h->dd) plan = h->ow ? 8 : h->staged ? 7 : 6;
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
-    if (h->storage == 3 && h->wk) return pick_warp_kernel(h->symmetric ? 1 : 0, multistart, two_opt);
+    if (h->storage == 3 && h->wk) return pick_warp_kernel(h->symmetric ? 1 : 0, multistart, two_opt, h->wk);
     if (h->storage == 3 && h->wide) return pick_wide_kernel(symm, plan);
     if (multistart && h->storage == 3) {
         // 88 registers per thread where that keeps as many CTAs resident as 80 do (asked of the runtime)
@@ -256,14 +266,15 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
         // one warp per search, the whole state in the warp's slice of shared memory (search_warp.cuh): n <= 32,
         // int32 state with packed selection keys
         if (h->npad > 32 || h->wide || h->acc_bits != 32 || h->delta_bound >= ((1LL << 27) - 1)) return false;
-        int wpc = 1;
+        int wpc = 4;  // warps per CTA: they share nothing but the address table (launch_search takes fewer for small batches)
         if (const char *e = getenv("QAPB_WPC")) wpc = std::min(8, std::max(1, atoi(e)));
-        h->wk = 1; h->wpc = wpc;
+        const int lanes = (h->npad <= 16 && !getenv("QAPB_NO_HALFWARP")) ? 16 : 32;  // lanes per search
+        h->wk = lanes; h->wpc = wpc;
         h->staged = 0; h->dsm = 0; h->dd = 0; h->ow = 0;
         h->upt = 1; h->toff = 32; h->us = 0; h->exp_in_smem = 1;
         h->threads = 32 * wpc;
         h->lb_class = 0;
-        h->smem_bytes = (unsigned)WK_TOTAL * (unsigned)wpc;
+        h->smem_bytes = wk_smem_bytes(lanes, wpc);
         return h->smem_bytes <= smem_cap;
     }
     const int dd = dsm == 2;  // diagonal blocks paired in registers: no dedicated warps, toff counts every thread
@@ -959,8 +970,16 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     if (rc) return rc;
     P.perm32 = SP.perm32; P.start_state = SP.state; P.initM = BP.M; P.initH = BP.h;
     P.batch = batch;
-    if (h->wk) kern<<<(batch + h->wpc - 1) / h->wpc, h->threads, h->smem_bytes, st>>>(P);  // wpc searches per CTA
-    else kern<<<batch, h->threads, h->smem_bytes, st>>>(P);
+    if (h->wk) {
+        // searches share nothing: pack as many warps into a CTA as still leaves every SM a CTA
+        const int per_warp = 32 / h->wk;
+        int wpc = h->wpc;
+        while (wpc > 1 && (batch + wpc * per_warp - 1) / (wpc * per_warp) < 2 * h->sm_count) wpc >>= 1;
+        const int per_cta = wpc * per_warp;
+        kern<<<(batch + per_cta - 1) / per_cta, 32 * wpc, wk_smem_bytes(h->wk, wpc), st>>>(P);
+    } else {
+        kern<<<batch, h->threads, h->smem_bytes, st>>>(P);
+    }
     CU(cudaGetLastError());
     CU(cudaEventRecord(h->ev1, st));
     h->have_timing = 1;

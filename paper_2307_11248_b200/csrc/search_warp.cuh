@@ -25,87 +25,129 @@
 
 namespace qapb {
 
-enum {
-    WK_M = 0,          // 8 rows x 32 lanes x 16 B: off-diagonal units (rows 0-3: upper block, 4-7: lower block transposed)
-    WK_DG = 4096,      // 8 diagonal blocks x 16 words
-    WK_XP = 4608,      // 32 units x 16 words: tabu expiry per (unit, slot)
-    WK_A = 6656,       // difference vectors of the last move (negated a, c), 32 words each
-    WK_B = 6784,
-    WK_C = 6912,
-    WK_E = 7040,
-    WK_HI = 7168,      // packed-key forms of h (search_hybrid.cuh)
-    WK_HJ = 7296,
-    WK_P = 7424,       // permutation (setup only)
-    WK_TOTAL = 7552
+// Layout of one search's slice of shared memory, in 32-bit words; G = lanes per search (32, or 16 for n <= 16:
+// two searches per warp).  Unit (I,J) sits in chunk slot ((I + J) & 7) + 8 * rank (rank among the units with the
+// same residue) -- the lane with that index owns it -- and element v of row w is stored at position (v + w) & 3 of
+// its 16-byte chunk: the lanes of the fix-ups, which walk a column or a row of M (all block rows X against one
+// block R), then hit 32 different banks, 4 ((X + R) & 7) + ((xu + ru) & 3), while the owner's own accesses stay
+// conflict-free 128-bit ones.
+template <int G> struct WkLay {
+    static constexpr int RSW = G * 4;                // row stride of the unit layout
+    static constexpr int M = 0;                      // 8 rows (0-3: upper block, 4-7: lower block transposed) x G units x 4
+    static constexpr int DG = 8 * RSW;               // diagonal-block pairs: [round q][x | y][lane]
+    static constexpr int XP = DG + 4 * G;            // G units x 16: tabu expiry per (unit, slot)
+    static constexpr int A = XP + 16 * G;            // difference vectors of the last move (negated a, c)
+    static constexpr int B = A + G;
+    static constexpr int C = B + G;
+    static constexpr int E = C + G;
+    static constexpr int HI = E + G;                 // packed-key forms of h (search_hybrid.cuh)
+    static constexpr int HJ = HI + G;
+    static constexpr int P = HJ + G;                 // permutation (setup only)
+    static constexpr int TOTAL = P + G;              // words per search
+    static constexpr int TAB = G * G;                // words of the address table shared by the CTA
 };
-
-// word offset (in the warp's slice) of M[x][y] and M[y][x] for location x = this lane and the moved
-// location y = 4 Y + yu; X == Y is the diagonal block.  One unit holds both entries, 512 words apart.
-__device__ __forceinline__ void wk_pair_words(int X, int xu, int Y, int yu, int nb, int &w_xy, int &w_yx)
+__host__ __device__ inline unsigned wk_smem_bytes(int G, int warps)
 {
-    const bool up = X < Y;
-    const int I = up ? X : Y, J = up ? Y : X;
-    const int uid = I * nb - ((I * (I + 1)) >> 1) + (J - I - 1);
-    // X < Y: M[x][y] = U[xu][yu] (row xu, column yu), M[y][x] = L[yu][xu] (row 4 + xu, column yu)
-    // X > Y: M[y][x] = U[yu][xu] (row yu, column xu), M[x][y] = L[xu][yu] (row 4 + yu, column xu)
-    const int row = up ? xu : yu, col = up ? yu : xu;
-    const int wU = (row * 32 + uid) * 4 + col;
-    w_xy = up ? wU : wU + 512;
-    w_yx = up ? wU + 512 : wU;
-    if (X == Y) {
-        w_xy = WK_DG / 4 + X * 16 + xu * 4 + yu;
-        w_yx = WK_DG / 4 + X * 16 + yu * 4 + xu;
-    }
+    const int total = G == 32 ? WkLay<32>::TOTAL : WkLay<16>::TOTAL;
+    return 4u * (unsigned)(G * G + warps * (32 / G) * total);
 }
 
-// 32 tenures (tabu.py:184-186), one per lane: draw k of the chunk is mix64(state + (k+1)*GAMMA); a draw that
-// randbelow would reject (probability ~ span / 2^64) makes every lane replay the chunk with the exact rule.
-__device__ __forceinline__ int32_t warp_tenure_chunk(unsigned long long &state, unsigned long long span,
-                                                     unsigned long long last_ok, long long lo, int force_seq, int lane)
+// chunk slot of unit (I,J), I < J < nb
+__host__ __device__ inline int wk_unit_slot(int I, int J, int nb)
 {
-    const unsigned long long r = mix64(state + QAPB_GAMMA * ((unsigned long long)lane + 1ULL));
+    const int k = (I + J) & 7;
+    int rank = 0;
+    for (int a = 0; a < nb; ++a)
+        for (int b2 = a + 1; b2 < nb; ++b2) {
+            if (a == I && b2 == J) return k + 8 * rank;
+            if (((a + b2) & 7) == k) ++rank;
+        }
+    return 0;
+}
+
+// Word offsets (in a search's slice) of M[x][y] and M[y][x], x != y.  One off-diagonal unit holds both entries,
+// four rows apart; a pair inside a diagonal block lives in the slot of the lane that owns it.
+template <int G>
+__device__ __forceinline__ unsigned wk_pair_words(int x, int y, int nb)
+{
+    typedef WkLay<G> LY;
+    const int X = x >> 2, xu = x & 3, Y = y >> 2, yu = y & 3;
+    int w_xy, w_yx;
+    if (X == Y) {
+        const int lo = min(xu, yu), hi = max(xu, yu);
+        const int pp = lo == 0 ? hi - 1 : lo == 1 ? hi + 1 : 5;   // (0,1) (0,2) (0,3) (1,2) (1,3) (2,3)
+        const int idx = 6 * X + pp, q = idx / G, l = idx - q * G;
+        const int wx = LY::DG + q * 2 * G + l;                     // M[lo][hi]; M[hi][lo] is G words on
+        w_xy = xu < yu ? wx : wx + G;
+        w_yx = xu < yu ? wx + G : wx;
+    } else {
+        const bool up = X < Y;
+        const int I = up ? X : Y, J = up ? Y : X;
+        const int uid = wk_unit_slot(I, J, nb);
+        // X < Y: M[x][y] = U[xu][yu] (row xu, column yu), M[y][x] = L[yu][xu] (row 4 + xu, column yu)
+        // X > Y: M[y][x] = U[yu][xu] (row yu, column xu), M[x][y] = L[xu][yu] (row 4 + yu, column xu)
+        const int row = up ? xu : yu;
+        const int wU = row * LY::RSW + uid * 4 + ((xu + yu) & 3);
+        w_xy = up ? wU : wU + 4 * LY::RSW;
+        w_yx = up ? wU + 4 * LY::RSW : wU;
+    }
+    return (unsigned)w_xy | ((unsigned)w_yx << 16);
+}
+
+// G tenures (tabu.py:184-186), one per lane: draw k of the chunk is mix64(state + (k+1)*GAMMA); a draw that
+// randbelow would reject (probability ~ span / 2^64) makes every lane replay the chunk with the exact rule.
+template <int G>
+__device__ __forceinline__ int32_t warp_tenure_chunk(unsigned gmask, unsigned long long &state, unsigned long long span,
+                                                     unsigned long long last_ok, long long lo, int force_seq, int gl)
+{
+    const unsigned long long r = mix64(state + QAPB_GAMMA * ((unsigned long long)gl + 1ULL));
     int32_t t = 0;
-    if (__any_sync(0xffffffffu, (r > last_ok) || force_seq)) {
+    if (__any_sync(gmask, (r > last_ok) || force_seq)) {
         unsigned long long st = state;
-        for (int k = 0; k < 32; ++k) {
+        for (int k = 0; k < G; ++k) {
             const int32_t v = (int32_t)(lo + (long long)randbelow_seq(st, span));
-            if (k == lane) t = v;
+            if (k == gl) t = v;
         }
         state = st;
     } else {
         t = (int32_t)(lo + (long long)(r % span));
-        state += QAPB_GAMMA * 32ULL;
+        state += QAPB_GAMMA * (unsigned long long)G;
     }
     return t;
 }
 
 // SYMM: 1 = both matrices symmetric (one product per entry), 0 = the general two-product update.
 // NOTABU: 2opt instantiation (no tabu state at all).  REC: trail / cells / caller-provided tenures.
-template <int SYMM, bool NOTABU, bool REC>
+// G: lanes per search.
+template <int SYMM, bool NOTABU, bool REC, int G>
 __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams P)
 {
+    typedef WkLay<G> LY;
     constexpr bool FULLSYM = SYMM == 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (b >= P.batch) return;  // whole warps only
-    unsigned char *W = smem_raw + (size_t)(threadIdx.x >> 5) * WK_TOTAL;
-    int32_t *sW = reinterpret_cast<int32_t *>(W);
-    int32_t *sM = reinterpret_cast<int32_t *>(W + WK_M);
-    int32_t *sDG = reinterpret_cast<int32_t *>(W + WK_DG);
-    int32_t *xp = reinterpret_cast<int32_t *>(W + WK_XP);
-    int32_t *sP = reinterpret_cast<int32_t *>(W + WK_P);
+    const int lane = threadIdx.x & 31, gl = lane & (G - 1);
+    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const int n = P.n, nb = P.nb, npad = P.npad, noff = P.noff;
+
+    // address table shared by the searches of the CTA: entry [y][x] = words of M[x][y] and M[y][x]
+    unsigned *sTab = reinterpret_cast<unsigned *>(smem_raw);
+    for (int e = threadIdx.x; e < G * G; e += blockDim.x) {
+        const int y = e / G, x = e - y * G;
+        sTab[e] = (x != y && x < npad && y < npad) ? wk_pair_words<G>(x, y, nb) : 0u;
+    }
+    __syncthreads();
+
+    const int b = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / G) + lane / G;
+    if (b >= P.batch) return;  // whole groups only
+    int32_t *sW = reinterpret_cast<int32_t *>(smem_raw) + LY::TAB + ((threadIdx.x >> 5) * (32 / G) + lane / G) * LY::TOTAL;
+    int32_t *sM = sW + LY::M;
+    int32_t *sDG = sW + LY::DG;
+    int32_t *xp = sW + LY::XP;
+    int32_t *sP = sW + LY::P;
     Vecs V;
-    V.A = reinterpret_cast<int32_t *>(W + WK_A);
-    V.B = reinterpret_cast<int32_t *>(W + WK_B);
-    V.C = reinterpret_cast<int32_t *>(W + WK_C);
-    V.E = reinterpret_cast<int32_t *>(W + WK_E);
-    V.HI = reinterpret_cast<int32_t *>(W + WK_HI);
-    V.HJ = reinterpret_cast<int32_t *>(W + WK_HJ);
+    V.A = sW + LY::A; V.B = sW + LY::B; V.C = sW + LY::C; V.E = sW + LY::E; V.HI = sW + LY::HI; V.HJ = sW + LY::HJ;
     V.H = V.ColR = V.ColS = V.TR = V.TS = V.XR = V.XS = nullptr;
 
-    const int n = P.n, nb = P.nb, npad = P.npad, noff = P.noff;
     const int32_t *__restrict__ F = P.F;
     const int32_t *__restrict__ FT = P.FT;
     const int32_t *__restrict__ D = P.D;
@@ -117,32 +159,37 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
     const int iters = P.iterations;
 
     // ---------------------------------------------------------------- setup
-    const bool loc = lane < n;          // this lane is a location
-    const int X = lane >> 2, xu = lane & 3;
-    int my_p = lane < npad ? P.perm32[(size_t)b * npad + lane] : 0;
-    int32_t h = lane < npad ? reinterpret_cast<const int32_t *>(P.initH)[(size_t)b * npad + lane] : 0;
-    V.A[lane] = 0; V.B[lane] = 0; V.C[lane] = 0; V.E[lane] = 0;
-    V.HI[lane] = 4 * xu - 16 * h;
-    V.HJ[lane] = xu - 16 * h;
-    sP[lane] = my_p;
+    const bool loc = gl < n;          // this lane is a location
+    const int xu = gl & 3;
+    int my_p = gl < npad ? P.perm32[(size_t)b * npad + gl] : 0;
+    int32_t h = gl < npad ? reinterpret_cast<const int32_t *>(P.initH)[(size_t)b * npad + gl] : 0;
+    V.A[gl] = 0; V.B[gl] = 0; V.C[gl] = 0; V.E[gl] = 0;
+    V.HI[gl] = 4 * xu - 16 * h;
+    V.HJ[gl] = xu - 16 * h;
+    sP[gl] = my_p;
     if (REC && P.cells) {
         int64_t *cz = P.cells + (size_t)b * n * n;
-        for (int i = lane; i < n * n; i += 32) cz[i] = 0;
+        for (int i = gl; i < n * n; i += G) cz[i] = 0;
     }
     const int32_t *__restrict__ Minit = reinterpret_cast<const int32_t *>(P.initM) + (size_t)b * npad * npad;
 
-    // off-diagonal unit of this lane (lexicographic over I < J)
-    const bool own = lane < noff;
+    // off-diagonal unit of this lane: the one whose chunk slot (wk_unit_slot) is the lane index
+    bool own = false;
     int I = 0, J = 1;
-    if (own) {
-        int rem = lane;
-        while (rem >= nb - 1 - I) { rem -= nb - 1 - I; ++I; }
-        J = I + 1 + rem;
-    }
-    unsigned tb = 0xffffu;
-    int32_t mexp = MAXV;
     {
-        int32_t U[4][4], L[4][4];
+        int rank = gl >> 3;
+        for (int a = 0; a < nb && !own; ++a)
+            for (int b2 = a + 1; b2 < nb && !own; ++b2)
+                if (((a + b2) & 7) == (gl & 7) && rank-- == 0) { I = a; J = b2; own = true; }
+    }
+    unsigned tb = 0xffffu, deadm = 0xffffu;  // pairs that are tabu now (pad slots permanently set: deadm)
+    int32_t mexp = MAXV;                     // earliest expiry among the clearable bits
+    int4 *myM = reinterpret_cast<int4 *>(sM) + gl;   // row w of this lane's unit: myM[w * G], rotated by w
+    // The unit stays in REGISTERS across iterations; it passes through its shared-memory slot only when it touches
+    // block row / column R or S of a move (flushed before the fix-ups, reloaded after them): half the shared-memory
+    // traffic of streaming every unit through the pass.
+    int32_t U[4][4], L[4][4];
+    {
         unsigned dead = 0xffffu;
         if (own) load_unit(Minit, npad, n, I, J, U, L, dead, PADV);
         else {
@@ -152,37 +199,31 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
                 for (int v = 0; v < 4; ++v) { U[u][v] = PADV; L[u][v] = PADV; }
         }
         tb = dead;
+        deadm = dead;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            reinterpret_cast<int4 *>(sM)[u * 32 + lane] = make_int4(U[u][0], U[u][1], U[u][2], U[u][3]);
-            reinterpret_cast<int4 *>(sM)[(4 + u) * 32 + lane] = make_int4(L[0][u], L[1][u], L[2][u], L[3][u]);
-        }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) xp[lane * 16 + q] = ((dead >> q) & 1u) ? MAXV : 0;
+        for (int q = 0; q < 16; ++q) xp[gl * 16 + q] = ((dead >> q) & 1u) ? MAXV : 0;
     }
-    if (lane < nb) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) sDG[lane * 16 + u * 4 + v] = Minit[(size_t)(4 * lane + u) * npad + 4 * lane + v];
-    }
-    // diagonal-block pairs lane and lane + 32 (pair pp of block Bk: (0,1) (0,2) (0,3) (1,2) (1,3) (2,3))
-    int di[2], dj[2], dwx[2], dwy[2];
+    bool touched = false;  // the unit was flushed for the fix-ups of the last move
+    // diagonal-block pairs gl and gl + G (pair pp of block Bk: (0,1) (0,2) (0,3) (1,2) (1,3) (2,3)), state in
+    // this lane's slots sDG[q*2G + gl] = M[i][j], sDG[q*2G + G + gl] = M[j][i]
+    int di[2], dj[2];
     bool dalive[2];
     int32_t dexp[2] = {0, 0};  // expiry iteration of the pair (cells[i][j]); 0 = never tabu
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-        const int idx = lane + 32 * q;
+        const int idx = gl + G * q;
         const int Bk = idx / 6, pp = idx - 6 * Bk;
         const int u = pp < 3 ? 0 : pp < 5 ? 1 : 2;
         const int v = pp < 3 ? pp + 1 : pp < 5 ? pp - 1 : 3;
         di[q] = 4 * Bk + u; dj[q] = 4 * Bk + v;
         dalive[q] = idx < 6 * nb && dj[q] < n;
-        if (!dalive[q]) { di[q] = 0; dj[q] = 1; }
-        dwx[q] = (di[q] >> 2) * 16 + (di[q] & 3) * 4 + (dj[q] & 3);
-        dwy[q] = (di[q] >> 2) * 16 + (dj[q] & 3) * 4 + (di[q] & 3);
+        int32_t x = PADV, y = PADV;
+        if (dalive[q]) { x = Minit[(size_t)di[q] * npad + dj[q]]; y = Minit[(size_t)dj[q] * npad + di[q]]; }
+        else { di[q] = 0; dj[q] = 1; }
+        sDG[q * 2 * G + gl] = x;
+        sDG[q * 2 * G + G + gl] = y;
     }
-    __syncwarp();
+    __syncwarp(gmask);
 
     long long cost;  // _kernels.pyx:18-24, int64, including the diagonal products
     {
@@ -190,11 +231,11 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
         if (loc) {
             for (int j = 0; j < n; ++j) {
                 const int pj = sP[j];
-                part += (j == lane) ? (long long)P.fd[my_p] * P.dd[lane] : (long long)F[my_p * npad + pj] * D[lane * npad + j];
+                part += (j == gl) ? (long long)P.fd[my_p] * P.dd[gl] : (long long)F[my_p * npad + pj] * D[gl * npad + j];
             }
         }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(FULL, part, off);
+        for (int off = G / 2; off > 0; off >>= 1) part += __shfl_xor_sync(gmask, part, off, G);
         cost = part;
     }
     long long best_cost = cost;
@@ -205,11 +246,12 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
     const unsigned long long span = (unsigned long long)(P.ten_hi - P.ten_lo + 1);
     const unsigned long long last_ok = (tabu && P.rng) ? ~0ULL - (0ULL - span) % span : 0ULL;
     int32_t my_ten = 0;
+    const unsigned *myTab = sTab + gl;  // entry of moved location y: myTab[y * G]
 
     for (int c = 1; c <= iters; ++c) {
-        if (tabu && ((c - 1) & 31) == 0) {
-            if (P.rng) my_ten = warp_tenure_chunk(rstate, span, last_ok, P.ten_lo, P.force_seq_rng, lane);
-            else if (REC) my_ten = (c - 1 + lane < iters) ? (int32_t)P.tenures[(size_t)b * iters + (c - 1 + lane)] : 0;
+        if (tabu && ((c - 1) & (G - 1)) == 0) {
+            if (P.rng) my_ten = warp_tenure_chunk<G>(gmask, rstate, span, last_ok, P.ten_lo, P.force_seq_rng, gl);
+            else if (REC) my_ten = (c - 1 + gl < iters) ? (int32_t)P.tenures[(size_t)b * iters + (c - 1 + gl)] : 0;
         }
         // ---------------- pass: rank-2 update of the previous move (the difference vectors are zero at its
         // two locations and before the first move), delta, admissibility, first minimum
@@ -217,13 +259,15 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
         unsigned my_key;
         int my_which = 0, my_slot = 0;  // 0: the off-diagonal unit, 1 / 2: diagonal pair q = 0 / 1
         {
-            int32_t U[4][4], L[4][4];
+            if (touched) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int4 a = reinterpret_cast<const int4 *>(sM)[u * 32 + lane];
-                const int4 l = reinterpret_cast<const int4 *>(sM)[(4 + u) * 32 + lane];
-                U[u][0] = a.x; U[u][1] = a.y; U[u][2] = a.z; U[u][3] = a.w;
-                L[0][u] = l.x; L[1][u] = l.y; L[2][u] = l.z; L[3][u] = l.w;
+                for (int u = 0; u < 4; ++u) {
+                    const int4 a = myM[u * G];
+                    const int4 l = myM[(4 + u) * G];
+                    const int32_t av[4] = {a.x, a.y, a.z, a.w}, lv[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) { U[u][v] = av[(v + u) & 3]; L[v][u] = lv[(v + u) & 3]; }
+                }
             }
             int32_t aI[4], bI[4], aJ[4], bJ[4];
             ld_vec4(V.A, I, aI); ld_vec4(V.B, I, bI); ld_vec4(V.A, J, aJ); ld_vec4(V.B, J, bJ);
@@ -246,11 +290,6 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
                         L[v][u] += aJ[v] * bI[u] + cJ[v] * eI[u];
                     }
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                reinterpret_cast<int4 *>(sM)[u * 32 + lane] = make_int4(U[u][0], U[u][1], U[u][2], U[u][3]);
-                reinterpret_cast<int4 *>(sM)[(4 + u) * 32 + lane] = make_int4(L[0][u], L[1][u], L[2][u], L[3][u]);
-            }
             int32_t dk;
             int sk;
             // (2opt: pad pairs carry 2^25 in both entries, so their keys lose against every real pair)
@@ -262,7 +301,7 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-            int32_t x = sDG[dwx[q]], y = sDG[dwy[q]];
+            int32_t x = sDG[q * 2 * G + gl], y = sDG[q * 2 * G + G + gl];
             const int32_t ai = V.A[di[q]], bj = V.B[dj[q]], aj = V.A[dj[q]], bi = V.B[di[q]];
             x += ai * bj;
             y += aj * bi;
@@ -271,16 +310,17 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
                 x += ci * ej;
                 y += cj * ei;
             }
-            const int32_t hi = __shfl_sync(FULL, h, di[q]), hj = __shfl_sync(FULL, h, dj[q]);
-            if (dalive[q]) { sDG[dwx[q]] = x; sDG[dwy[q]] = y; }
+            const int32_t hi = __shfl_sync(gmask, h, di[q], G), hj = __shfl_sync(gmask, h, dj[q], G);
+            sDG[q * 2 * G + gl] = x;
+            sDG[q * 2 * G + G + gl] = y;
             const int32_t d = x + y - hi - hj;
             const bool adm = dalive[q] && (NOTABU || dexp[q] <= c || d < thr);
             const unsigned key = pair_key(di[q], dj[q], 0);
             if (adm && (d < my_d || (d == my_d && key < my_key))) { my_d = d; my_key = key; my_which = 1 + q; }
         }
-        int32_t bd = my_d;
-        unsigned bkey = my_key;
-        warp_argmin(bd, bkey);
+        // lexicographic minimum of (delta, key) over the search's lanes
+        const int32_t bd = __reduce_min_sync(gmask, my_d);
+        const unsigned bkey = __reduce_min_sync(gmask, my_d == bd ? my_key : 0xffffffffu);
         if (bd == MAXV) {  // no admissible move: premature stop (_kernels.pyx:168-170)
             stopped = 1;
             break;
@@ -292,24 +332,33 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
         thr = Acc<int32_t>::clamp_thr(best_cost - cost);
         steps_done = c;
         const bool is_winner = my_key == bkey;
-        const int pr = __shfl_sync(FULL, my_p, r), ps = __shfl_sync(FULL, my_p, s);
-        const int32_t hr = __shfl_sync(FULL, h, r), hs = __shfl_sync(FULL, h, s);
-        const int32_t ten = tabu ? __shfl_sync(FULL, my_ten, (c - 1) & 31) : 0;
-        __syncwarp();  // ------------------------------------------------ sync #1: the pass has stored M
+        const int pr = __shfl_sync(gmask, my_p, r, G), ps = __shfl_sync(gmask, my_p, s, G);
+        const int32_t hr = __shfl_sync(gmask, h, r, G), hs = __shfl_sync(gmask, h, s, G);
+        const int32_t ten = tabu ? __shfl_sync(gmask, my_ten, (c - 1) & (G - 1), G) : 0;
+        {
+            const int R = r >> 2, S = s >> 2;
+            touched = own && (I == R || J == R || I == S || J == S);
+            if (touched) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {  // position k of a chunk holds element (k - u) & 3 of its row
+                    myM[u * G] = make_int4(U[u][(0 - u) & 3], U[u][(1 - u) & 3], U[u][(2 - u) & 3], U[u][(3 - u) & 3]);
+                    myM[(4 + u) * G] = make_int4(L[(0 - u) & 3][u], L[(1 - u) & 3][u], L[(2 - u) & 3][u], L[(3 - u) & 3][u]);
+                }
+            }
+        }
+        __syncwarp(gmask);  // -------------------------------------------- sync #1: the touched units are in shared memory
 
         // ---------------- publish: difference vectors of the move (old permutation), h', and the entries on
         // rows / columns r,s of M fixed in place by the lane of their location
-        const int R = r >> 2, S = s >> 2, ru = r & 3, su = s & 3;
-        const int i = loc ? lane : 0;
+        const int i = loc ? gl : 0;
         const int pi = loc ? my_p : 0;
-        const bool mid = loc && (lane != r) && (lane != s);
-        int w_ir, w_ri, w_is, w_si;
-        wk_pair_words(X, xu, R, ru, nb, w_ir, w_ri);
-        wk_pair_words(X, xu, S, su, nb, w_is, w_si);
+        const bool mid = loc && (gl != r) && (gl != s);
+        const unsigned tr = myTab[r * G], ts = myTab[s * G];
+        int32_t *p_ir = sW + (tr & 0xffffu), *p_ri = sW + (tr >> 16);
+        int32_t *p_is = sW + (ts & 0xffffu), *p_si = sW + (ts >> 16);
         int32_t m_ir = 0, m_ri = 0, m_is = 0, m_si = 0;
-        if (mid) { m_ir = sW[w_ir]; m_ri = sW[w_ri]; m_is = sW[w_is]; m_si = sW[w_si]; }
-        if (loc && lane == r) m_is = sW[w_is];  // M[r][s]
-        if (loc && lane == s) m_ir = sW[w_ir];  // M[s][r]
+        if (loc && gl != r) { m_ir = *p_ir; m_ri = *p_ri; }   // (lane s: M[s][r])
+        if (loc && gl != s) { m_is = *p_is; m_si = *p_si; }   // (lane r: M[r][s])
         int32_t kr = 0, ks = 0;  // corner terms, zero when both matrices are symmetric
         if (FULLSYM) {
             const int32_t Drs = D[r * npad + s], Fpspr = F[ps * npad + pr];
@@ -317,14 +366,14 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
             const int32_t Fpspi = F[ps * npad + pi], Fprpi = F[pr * npad + pi];
             const int32_t a = mid ? Dsi - Dri : 0, bb = mid ? Fpspi - Fprpi : 0;
             const int32_t a2 = 2 * a, b2 = 2 * bb;
-            V.A[lane] = -a2;
-            V.B[lane] = bb;
+            V.A[gl] = -a2;
+            V.B[gl] = bb;
             if (mid) {
                 h -= a2 * bb;
-                sW[w_ir] = m_is + a2 * (Fpspr - Fpspi);        // M'[i][r] = M[i][s] + tR[i]
-                sW[w_is] = m_ir + a2 * (Fprpi - Fpspr);        // M'[i][s] = M[i][r] + tS[i]
-                sW[w_ri] = m_ri + b2 * (Dri - Drs);            // M'[r][i] = M[r][i] + xR[i]
-                sW[w_si] = m_si + b2 * (Drs - Dsi);            // M'[s][i] = M[s][i] + xS[i]
+                *p_ir = m_is + a2 * (Fpspr - Fpspi);        // M'[i][r] = M[i][s] + tR[i]
+                *p_is = m_ir + a2 * (Fprpi - Fpspr);        // M'[i][s] = M[i][r] + tS[i]
+                *p_ri = m_ri + b2 * (Dri - Drs);            // M'[r][i] = M[r][i] + xR[i]
+                *p_si = m_si + b2 * (Drs - Dsi);            // M'[s][i] = M[s][i] + xS[i]
             }
         } else {
             const int32_t Drs = D[r * npad + s], Dsr = D[s * npad + r];
@@ -336,26 +385,26 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
             const int32_t a = mid ? Dis - Dir : 0, cc = mid ? Dsi - Dri : 0;
             const int32_t bb = mid ? Fpips - Fpipr : 0, e = mid ? Fpspi - Fprpi : 0;
             const int32_t be = bb + e;
-            V.A[lane] = -a;
-            V.B[lane] = bb;
-            V.C[lane] = -cc;
-            V.E[lane] = e;
+            V.A[gl] = -a;
+            V.B[gl] = bb;
+            V.C[gl] = -cc;
+            V.E[gl] = e;
             kr = (Drs - Dsr) * Fpspr;
             ks = (Dsr - Drs) * Fprps;
             if (mid) {
                 h -= a * bb + cc * e;
-                sW[w_ir] = m_is + a * (Fpspr - (Fpips + Fpspi)) + cc * Fprps;
-                sW[w_is] = m_ir + a * ((Fpipr + Fprpi) - Fprps) - cc * Fpspr;
-                sW[w_ri] = m_ri - Drs * bb - Dsr * e + Dri * be;
-                sW[w_si] = m_si + Dsr * bb + Drs * e - Dsi * be;
+                *p_ir = m_is + a * (Fpspr - (Fpips + Fpspi)) + cc * Fprps;
+                *p_is = m_ir + a * ((Fpipr + Fprpi) - Fprps) - cc * Fpspr;
+                *p_ri = m_ri - Drs * bb - Dsr * e + Dri * be;
+                *p_si = m_si + Dsr * bb + Drs * e - Dsi * be;
             }
         }
         // corners: M'[r][s] = h[r] + kr, h'[r] = M[r][s] + ks;  M'[s][r] = h[s] + ks, h'[s] = M[s][r] + kr
-        if (loc && lane == r) { sW[w_is] = hr + kr; h = m_is + ks; }
-        if (loc && lane == s) { sW[w_ir] = hs + ks; h = m_ir + kr; }
-        V.HI[lane] = 4 * xu - 16 * h;
-        V.HJ[lane] = xu - 16 * h;
-        my_p = (lane == r) ? ps : (lane == s) ? pr : my_p;
+        if (loc && gl == r) { *p_is = hr + kr; h = m_is + ks; }
+        if (loc && gl == s) { *p_ir = hs + ks; h = m_ir + kr; }
+        V.HI[gl] = 4 * xu - 16 * h;
+        V.HJ[gl] = xu - 16 * h;
+        my_p = (gl == r) ? ps : (gl == s) ? pr : my_p;
         if (improved) best_p = my_p;
 
         // ---- the lane owning the winning pair: tabu memory, trail
@@ -367,7 +416,7 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
                 if (tabu) {
                     tb |= 1u << my_slot;
                     mexp = min(mexp, new_exp);
-                    xp[lane * 16 + my_slot] = new_exp;
+                    xp[gl * 16 + my_slot] = new_exp;
                 }
             } else {
 #pragma unroll
@@ -389,15 +438,23 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
             }
         }
         // ---- tabu bits that expire at the next iteration are cleared here
-        if (!NOTABU && own && c + 1 >= mexp) expire_bits(tb, mexp, c + 1, xp + lane * 16);
-        __syncwarp();  // ------------------------------------------------ sync #2
+        if (!NOTABU && own && c + 1 >= mexp) {
+            const unsigned live = tb & ~deadm;
+            if ((live & (live - 1u)) == 0u) {  // one tabu pair in this unit (the usual case): one load
+                const int32_t e = xp[gl * 16 + (__ffs(live) - 1)];
+                if (e <= c + 1) { tb &= ~live; mexp = MAXV; } else mexp = e;
+            } else {
+                expire_bits(tb, mexp, c + 1, xp + gl * 16);
+            }
+        }
+        __syncwarp(gmask);  // -------------------------------------------- sync #2
     }
 
     if (loc) {
-        P.best[(size_t)b * n + lane] = best_p;
-        P.cur[(size_t)b * n + lane] = my_p;
+        P.best[(size_t)b * n + gl] = best_p;
+        P.cur[(size_t)b * n + gl] = my_p;
     }
-    if (lane == 0) {
+    if (gl == 0) {
         P.best_cost[b] = best_cost;
         P.cur_cost[b] = cost;
         if (P.stopped) P.stopped[b] = stopped;

@@ -10,7 +10,9 @@ from paper_2307_11248_b200.backend import device_instance
 
 kind = sys.argv[1] if len(sys.argv) > 1 else "sym"
 bad = 0
-for n in (2, 3, 4, 5, 8, 9, 12, 13, 16, 17, 21, 24, 25, 28, 29, 30, 31, 32):
+import os
+NS = [int(x) for x in os.environ.get("WARP_NS", "2,3,4,5,8,9,12,13,16,17,21,24,25,28,29,30,31,32").split(",")]
+for n in NS:
     inst = shapes.tai_a(n, seed=n) if kind == "sym" else shapes.rand(n, seed=n)
     di = device_instance(inst.flow, inst.distance)
     lo, hi = oracle.tenure_bounds(n)
@@ -40,7 +42,10 @@ for n in (2, 3, 4, 5, 8, 9, 12, 13, 16, 17, 21, 24, 25, 28, 29, 30, 31, 32):
             print("multistart MISMATCH n", n, algo)
 print("warp_check", kind, "mismatches:", bad, "threads", di.info["threads"], "smem", di.info["smem_bytes"], "ctas/SM", di.info["ctas_per_sm"])
 if len(sys.argv) > 2:
-    for name, starts, iters in (("tai30a", 1, 1000), ("tai30a", 1776, 240), ("tai30a", 4736, 240), ("nug12", 1776, 96), ("nug12", 4736, 96)):
+    cases = (("tai30a", 1, 1000), ("tai30a", 1776, 240), ("tai30a", 4736, 240), ("nug12", 1776, 96), ("nug12", 4736, 96))
+    if os.environ.get("WARP_TIME") == "small":
+        cases = (("nug12", 1, 1000), ("nug12", 1776, 96), ("nug12", 4736, 96), ("nug12", 9472, 96), ("tai16a", 4736, 128))
+    for name, starts, iters in cases:
         inst = shapes.by_name(name)
         di = device_instance(inst.flow, inst.distance)
         t = q.tenure_bounds(inst.n)
