@@ -277,7 +277,7 @@ def _shape_runs(q, device_instance, local: int, table) -> list:
             ev = steps * si.n * (si.n - 1) // 2
             out.append({"shape": name, "n": si.n, "algo": algo, "starts": starts, "iterations": its,
                         "ms": ms, "evals_per_s": ev / (ms * 1e-3), "acc_bits": sd.info["acc_bits"],
-                        "kernel": "hybrid" if sd.info["storage"] == 3 else "generic",
+                        "kernel": {3: "hybrid", 4: "warp"}.get(sd.info["storage"], "generic"),
                         "threads": sd.info["threads"], "ctas_per_sm": sd.info["ctas_per_sm"]})
         except Exception as exc:  # pragma: no cover
             out.append({"shape": name, "error": repr(exc)})
@@ -505,7 +505,8 @@ def run_ours(args) -> None:
         shapes_tbl = None
         if not args.no_shapes:
             shapes_tbl = _shape_runs(q, device_instance, local, (
-                ("nug12", "2opt", 1776, 48), ("tai30a", "tabu", 1, 1000), ("tai30a", "tabu", 1776, 240),
+                ("nug12", "2opt", 1776, 48), ("nug12", "tabu", 4736, 96), ("tai30a", "tabu", 1, 1000),
+                ("tai30a", "tabu", 1776, 240), ("tai30a", "tabu", 4736, 240),
                 ("tai64c", "tabu", 1184, 512), ("tai100a", "2opt", 1184, 400), ("sko100", "tabu", 1184, 800),
                 ("rand100", "tabu", 1184, 800), ("tai150b", "tabu", 296, 1200), ("tai256c", "2opt", 148, 1024),
                 ("tai256c", "tabu", 148, 2048)))

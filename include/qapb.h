@@ -61,7 +61,9 @@ typedef struct qapb_info {
     int32_t units_per_thread;
     int32_t storage;        /* 0: placement matrix in shared memory, 1: in L2/global,
                                2: placement matrix and tabu masks in L2/global,
-                               3: hybrid kernel (registers + shared memory)           */
+                               3: hybrid kernel (registers + shared memory),
+                               4: one warp per search (n <= 32; `threads` / 32 searches per
+                                  CTA, twice that at n <= 16)                            */
     int32_t smem_bytes;     /* dynamic shared memory per CTA                          */
     int32_t ctas_per_sm;    /* resident searches per SM (occupancy query)             */
     int32_t sm_count;
@@ -173,7 +175,7 @@ int qapb_multistart_trace_host(qapb_handle *h, int algo, const uint64_t *seeds, 
  * configuration is how one search is laid out on an SM).  `qapb_plan_candidates` lists the plans of
  * the register/shared-memory kernel that fit this instance as rows {register units per thread,
  * threads carrying off-diagonal units, shared-memory units per thread, diagonal blocks in shared
- * memory (0/1)}; `qapb_set_plan` re-plans the handle with one of them (results are identical under
+ * memory (0/1)} -- register units 0 names the one-warp-per-search kernel (n <= 32, the default there); `qapb_set_plan` re-plans the handle with one of them (results are identical under
  * every plan; only the speed differs).  Instances served by the generic kernel have no candidates. */
 int qapb_plan_candidates(qapb_handle *h, int32_t *plans /* [cap][4] */, int cap, int *count);
 int qapb_set_plan(qapb_handle *h, int reg_units, int unit_threads, int smem_units, int diag_in_smem);

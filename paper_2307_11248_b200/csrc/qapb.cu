@@ -819,7 +819,7 @@ extern "C" int qapb_get_info(const qapb_handle *h, qapb_info *info)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hm->ctas_per_sm, (const void *)handle_kernel(h), h->threads, h->smem_bytes);
     }
     info->n = h->n; info->device = h->device; info->acc_bits = h->wide ? 64 : h->acc_bits; info->symmetric = h->symmetric;
-    info->threads = h->threads; info->units_per_thread = h->upt; info->storage = h->storage;
+    info->threads = h->threads; info->units_per_thread = h->upt; info->storage = h->wk ? 4 : h->storage;
     info->smem_bytes = (int32_t)h->smem_bytes; info->ctas_per_sm = h->ctas_per_sm; info->sm_count = h->sm_count;
     info->delta_bound = h->delta_bound;
     return QAPB_OK;
@@ -966,9 +966,11 @@ static int launch_search(qapb_handle *h, SearchParams &P, int batch, size_t extr
     // start permutations (+ stream state), then M and h as one batched tiled integer product
     BuildParams BP;
     StartParams SP;
-    rc = launch_build(h, w, batch, P.rng, P.force_seq_rng, P.master_seed, P.first_index, P.seeds, P.perms, st, BP, SP);
-    if (rc) return rc;
-    P.perm32 = SP.perm32; P.start_state = SP.state; P.initM = BP.M; P.initH = BP.h;
+    if (!h->wk) {  // (the warp kernel draws its start and builds its placement matrix itself)
+        rc = launch_build(h, w, batch, P.rng, P.force_seq_rng, P.master_seed, P.first_index, P.seeds, P.perms, st, BP, SP);
+        if (rc) return rc;
+        P.perm32 = SP.perm32; P.start_state = SP.state; P.initM = BP.M; P.initH = BP.h;
+    }
     P.batch = batch;
     if (h->wk) {
         // searches share nothing: pack as many warps into a CTA as still leaves every SM a CTA

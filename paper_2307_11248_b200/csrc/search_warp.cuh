@@ -44,12 +44,12 @@ template <int G> struct WkLay {
     static constexpr int HJ = HI + G;
     static constexpr int P = HJ + G;                 // permutation (setup only)
     static constexpr int TOTAL = P + G;              // words per search
-    static constexpr int TAB = G * G;                // words of the address table shared by the CTA
+    static constexpr int TAB = G * G + 32;           // words shared by the CTA: address table, then slot / unit maps (64 + 64 bytes)
 };
 __host__ __device__ inline unsigned wk_smem_bytes(int G, int warps)
 {
     const int total = G == 32 ? WkLay<32>::TOTAL : WkLay<16>::TOTAL;
-    return 4u * (unsigned)(G * G + warps * (32 / G) * total);
+    return 4u * (unsigned)(G * G + 32 + warps * (32 / G) * total);
 }
 
 // chunk slot of unit (I,J), I < J < nb
@@ -68,7 +68,7 @@ __host__ __device__ inline int wk_unit_slot(int I, int J, int nb)
 // Word offsets (in a search's slice) of M[x][y] and M[y][x], x != y.  One off-diagonal unit holds both entries,
 // four rows apart; a pair inside a diagonal block lives in the slot of the lane that owns it.
 template <int G>
-__device__ __forceinline__ unsigned wk_pair_words(int x, int y, int nb)
+__device__ __forceinline__ unsigned wk_pair_words(int x, int y, const unsigned char *slot_of)
 {
     typedef WkLay<G> LY;
     const int X = x >> 2, xu = x & 3, Y = y >> 2, yu = y & 3;
@@ -83,7 +83,7 @@ __device__ __forceinline__ unsigned wk_pair_words(int x, int y, int nb)
     } else {
         const bool up = X < Y;
         const int I = up ? X : Y, J = up ? Y : X;
-        const int uid = wk_unit_slot(I, J, nb);
+        const int uid = slot_of[I * 8 + J];
         // X < Y: M[x][y] = U[xu][yu] (row xu, column yu), M[y][x] = L[yu][xu] (row 4 + xu, column yu)
         // X > Y: M[y][x] = U[yu][xu] (row yu, column xu), M[x][y] = L[xu][yu] (row 4 + yu, column xu)
         const int row = up ? xu : yu;
@@ -120,7 +120,10 @@ __device__ __forceinline__ int32_t warp_tenure_chunk(unsigned gmask, unsigned lo
 // NOTABU: 2opt instantiation (no tabu state at all).  REC: trail / cells / caller-provided tenures.
 // G: lanes per search.
 template <int SYMM, bool NOTABU, bool REC, int G>
-__global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams P)
+#ifndef QAPB_WARP_MINB
+#define QAPB_WARP_MINB 1
+#endif
+__global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(const SearchParams P)
 {
     typedef WkLay<G> LY;
     constexpr bool FULLSYM = SYMM == 1;
@@ -129,11 +132,24 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
     const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const int n = P.n, nb = P.nb, npad = P.npad, noff = P.noff;
 
-    // address table shared by the searches of the CTA: entry [y][x] = words of M[x][y] and M[y][x]
+    // shared by the searches of the CTA: chunk slot of every unit and its inverse, then the address table:
+    // entry [y][x] = words of M[x][y] and M[y][x]
     unsigned *sTab = reinterpret_cast<unsigned *>(smem_raw);
+    unsigned char *sSlot = reinterpret_cast<unsigned char *>(sTab + G * G);  // [I * 8 + J] -> slot
+    unsigned char *sUnit = sSlot + 64;                                        // [slot] -> I | J << 4, 0xff = none
+    for (int t = threadIdx.x; t < 64; t += blockDim.x) {
+        const int a = t >> 3, b2 = t & 7;
+        sUnit[t] = 0xff;
+        sSlot[t] = (a < b2 && b2 < nb) ? (unsigned char)wk_unit_slot(a, b2, nb) : 0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 64; t += blockDim.x) {
+        const int a = t >> 3, b2 = t & 7;
+        if (a < b2 && b2 < nb) sUnit[sSlot[t]] = (unsigned char)(a | (b2 << 4));
+    }
     for (int e = threadIdx.x; e < G * G; e += blockDim.x) {
         const int y = e / G, x = e - y * G;
-        sTab[e] = (x != y && x < npad && y < npad) ? wk_pair_words<G>(x, y, nb) : 0u;
+        sTab[e] = (x != y && x < npad && y < npad) ? wk_pair_words<G>(x, y, sSlot) : 0u;
     }
     __syncthreads();
 
@@ -161,49 +177,44 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
     // ---------------------------------------------------------------- setup
     const bool loc = gl < n;          // this lane is a location
     const int xu = gl & 3;
-    int my_p = gl < npad ? P.perm32[(size_t)b * npad + gl] : 0;
-    int32_t h = gl < npad ? reinterpret_cast<const int32_t *>(P.initH)[(size_t)b * npad + gl] : 0;
+    // ---- start permutation and stream state (rng.py:62-70, core.py:81-87; what qap_start_kernel does for the
+    // CTA-wide kernels): the n - 1 shuffle draws one per lane, the swaps through shuffles; a draw that randbelow
+    // would reject makes every lane replay the exact sequential rule
+    int my_p = 0;
+    unsigned long long rstate = 0ULL;
+    if (P.rng) {
+        const unsigned long long seed =
+            P.seeds ? P.seeds[b] : mix64(P.master_seed + QAPB_GAMMA * (P.first_index + (unsigned long long)b + 1ULL));
+        int reject = P.force_seq_rng;
+        unsigned jv = 0;  // lane k: the draw for position i = n - 1 - k
+        if (gl < n - 1) {
+            const unsigned long long bound = (unsigned long long)(n - gl);
+            const unsigned long long r = mix64(seed + QAPB_GAMMA * ((unsigned long long)gl + 1ULL));
+            if (r > ~0ULL - (0ULL - bound) % bound) reject = 1;
+            jv = (unsigned)(r % bound);
+        }
+        reject = __any_sync(gmask, reject);
+        my_p = loc ? gl : 0;
+        unsigned long long st = seed;
+        for (int i = n - 1; i >= 1; --i) {
+            const int j = reject ? (int)randbelow_seq(st, (unsigned long long)i + 1ULL) : (int)__shfl_sync(gmask, jv, n - 1 - i, G);
+            const int vi = __shfl_sync(gmask, my_p, i, G), vj = __shfl_sync(gmask, my_p, j, G);
+            my_p = gl == i ? vj : gl == j ? vi : my_p;
+        }
+        rstate = reject ? st : seed + QAPB_GAMMA * (unsigned long long)(n - 1);
+    } else {
+        my_p = loc ? (int)P.perms[(size_t)b * n + gl] : 0;
+    }
     V.A[gl] = 0; V.B[gl] = 0; V.C[gl] = 0; V.E[gl] = 0;
-    V.HI[gl] = 4 * xu - 16 * h;
-    V.HJ[gl] = xu - 16 * h;
     sP[gl] = my_p;
     if (REC && P.cells) {
         int64_t *cz = P.cells + (size_t)b * n * n;
         for (int i = gl; i < n * n; i += G) cz[i] = 0;
     }
-    const int32_t *__restrict__ Minit = reinterpret_cast<const int32_t *>(P.initM) + (size_t)b * npad * npad;
 
     // off-diagonal unit of this lane: the one whose chunk slot (wk_unit_slot) is the lane index
-    bool own = false;
-    int I = 0, J = 1;
-    {
-        int rank = gl >> 3;
-        for (int a = 0; a < nb && !own; ++a)
-            for (int b2 = a + 1; b2 < nb && !own; ++b2)
-                if (((a + b2) & 7) == (gl & 7) && rank-- == 0) { I = a; J = b2; own = true; }
-    }
-    unsigned tb = 0xffffu, deadm = 0xffffu;  // pairs that are tabu now (pad slots permanently set: deadm)
-    int32_t mexp = MAXV;                     // earliest expiry among the clearable bits
-    int4 *myM = reinterpret_cast<int4 *>(sM) + gl;   // row w of this lane's unit: myM[w * G], rotated by w
-    // The unit stays in REGISTERS across iterations; it passes through its shared-memory slot only when it touches
-    // block row / column R or S of a move (flushed before the fix-ups, reloaded after them): half the shared-memory
-    // traffic of streaming every unit through the pass.
-    int32_t U[4][4], L[4][4];
-    {
-        unsigned dead = 0xffffu;
-        if (own) load_unit(Minit, npad, n, I, J, U, L, dead, PADV);
-        else {
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) { U[u][v] = PADV; L[u][v] = PADV; }
-        }
-        tb = dead;
-        deadm = dead;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) xp[gl * 16 + q] = ((dead >> q) & 1u) ? MAXV : 0;
-    }
-    bool touched = false;  // the unit was flushed for the fix-ups of the last move
+    const bool own = sUnit[gl] != 0xff;
+    const int I = own ? (sUnit[gl] & 15) : 0, J = own ? (sUnit[gl] >> 4) : 1;
     // diagonal-block pairs gl and gl + G (pair pp of block Bk: (0,1) (0,2) (0,3) (1,2) (1,3) (2,3)), state in
     // this lane's slots sDG[q*2G + gl] = M[i][j], sDG[q*2G + G + gl] = M[j][i]
     int di[2], dj[2];
@@ -217,12 +228,100 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
         const int v = pp < 3 ? pp + 1 : pp < 5 ? pp - 1 : 3;
         di[q] = 4 * Bk + u; dj[q] = 4 * Bk + v;
         dalive[q] = idx < 6 * nb && dj[q] < n;
-        int32_t x = PADV, y = PADV;
-        if (dalive[q]) { x = Minit[(size_t)di[q] * npad + dj[q]]; y = Minit[(size_t)dj[q] * npad + di[q]]; }
-        else { di[q] = 0; dj[q] = 1; }
-        sDG[q * 2 * G + gl] = x;
-        sDG[q * 2 * G + G + gl] = y;
+        if (!dalive[q]) { di[q] = 0; dj[q] = 1; }
     }
+
+    // ---- the placement matrix of the start (what qap_build_m_whole_kernel does for the CTA-wide kernels):
+    //   S[a][b] = sum_k D0[a][k] F0[p_b][p_k] + D0[k][a] F0[p_k][p_b]
+    //   M[i][j] = S[i][j] + D0[i][j] (F0[p_i][p_j] + F0[p_j][p_i]) + dd[i] fd[p_j],   h[i] = S[i][i] + dd[i] fd[p_i]
+    // with the gathered flow matrix staged in the (still unused) unit slots: first Gm[k][j] = F0[p_j][p_k] for the
+    // first sum, then its transpose for the second (both matrices symmetric: twice the first sum).
+    unsigned tb = 0xffffu, deadm = 0xffffu;  // pairs that are tabu now (pad slots permanently set: deadm)
+    int32_t mexp = MAXV;                     // earliest expiry among the clearable bits
+    int4 *myM = reinterpret_cast<int4 *>(sM) + gl;   // row w of this lane's unit: myM[w * G], rotated by w
+    // The unit stays in REGISTERS across iterations; it passes through its shared-memory slot only when it touches
+    // block row / column R or S of a move (flushed before the fix-ups, reloaded after them): half the shared-memory
+    // traffic of streaming every unit through the pass.
+    int32_t U[4][4], L[4][4];
+    int32_t h = 0;
+    {
+        int32_t *sG = sM;  // G x G words
+        int32_t dx[2] = {0, 0}, dy[2] = {0, 0};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) { U[u][v] = 0; L[u][v] = 0; }
+        __syncwarp(gmask);
+#pragma unroll 1
+        for (int phase = 0; phase < (FULLSYM ? 1 : 2); ++phase) {
+            // phase 0: buffer[k][j] = F0[p_j][p_k], left factor D0[a][k] (rows of D^T); phase 1: the transposes
+            const int32_t *__restrict__ lhs = phase == 0 ? DT : D;
+            if (phase == 1) __syncwarp(gmask);
+            for (int k = 0; k < G; ++k) {
+                int32_t g = 0;
+                if (loc && k < n) g = phase == 0 ? F[my_p * npad + sP[k]] : F[sP[k] * npad + my_p];
+                sG[k * G + gl] = g;
+            }
+            __syncwarp(gmask);
+            for (int k = 0; k < n; ++k) {
+                int32_t aI[4], aJ[4], gI[4], gJ[4];
+                ld_vec4(lhs + k * npad, I, aI); ld_vec4(lhs + k * npad, J, aJ);
+                ld_vec4(sG + k * G, I, gI); ld_vec4(sG + k * G, J, gJ);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        U[u][v] += aI[u] * gJ[v];
+                        L[v][u] += aJ[v] * gI[u];
+                    }
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int32_t li = lhs[k * npad + di[q]], lj = lhs[k * npad + dj[q]];
+                    dx[q] += li * sG[k * G + dj[q]];
+                    dy[q] += lj * sG[k * G + di[q]];
+                }
+                h += lhs[k * npad + (loc ? gl : 0)] * sG[k * G + gl];
+            }
+        }
+        // direct and diagonal terms (the buffer holds F0[p_k][p_j] at [k][j], or its transpose: the sum of
+        // the two orientations is the same), pads
+        const int32_t two = FULLSYM ? 2 : 1;
+        unsigned dead = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int i = 4 * I + u, j = 4 * J + v;
+                if (i >= n || j >= n || !own) {
+                    dead |= 1u << (u * 4 + v);
+                    U[u][v] = PADV; L[v][u] = PADV;
+                } else {
+                    const int32_t fs = sG[i * G + j] + sG[j * G + i];
+                    U[u][v] = two * U[u][v] + D[i * npad + j] * fs + P.dd[i] * P.fd[sP[j]];
+                    L[v][u] = two * L[v][u] + D[j * npad + i] * fs + P.dd[j] * P.fd[sP[i]];
+                }
+            }
+        tb = dead;
+        deadm = dead;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) xp[gl * 16 + q] = ((dead >> q) & 1u) ? MAXV : 0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            int32_t x = PADV, y = PADV;
+            if (dalive[q]) {
+                const int i = di[q], j = dj[q];
+                const int32_t fs = sG[i * G + j] + sG[j * G + i];
+                x = two * dx[q] + D[i * npad + j] * fs + P.dd[i] * P.fd[sP[j]];
+                y = two * dy[q] + D[j * npad + i] * fs + P.dd[j] * P.fd[sP[i]];
+            }
+            sDG[q * 2 * G + gl] = x;
+            sDG[q * 2 * G + G + gl] = y;
+        }
+        h = loc ? two * h + P.dd[gl] * P.fd[my_p] : 0;
+    }
+    V.HI[gl] = 4 * xu - 16 * h;
+    V.HJ[gl] = xu - 16 * h;
+    bool touched = false;  // the unit was flushed for the fix-ups of the last move
     __syncwarp(gmask);
 
     long long cost;  // _kernels.pyx:18-24, int64, including the diagonal products
@@ -242,11 +341,13 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
     int32_t thr = 0;  // best_cost - cost, clamped; aspiration <=> delta < thr  (_kernels.pyx:162)
     int best_p = my_p;
     int steps_done = 0, stopped = 0;
-    unsigned long long rstate = (tabu && P.rng) ? P.start_state[b] : 0ULL;
     const unsigned long long span = (unsigned long long)(P.ten_hi - P.ten_lo + 1);
     const unsigned long long last_ok = (tabu && P.rng) ? ~0ULL - (0ULL - span) % span : 0ULL;
     int32_t my_ten = 0;
-    const unsigned *myTab = sTab + gl;  // entry of moved location y: myTab[y * G]
+    // entry of moved location y: table word y * G + gl.  (A 32-bit shared-window address kept in a register: from
+    // the pointer the compiler re-derives the window base with S2UR SR_CgaCtaId in every iteration.)
+    unsigned tab_sa = (unsigned)__cvta_generic_to_shared(sTab + gl);
+    asm volatile("" : "+r"(tab_sa));
 
     for (int c = 1; c <= iters; ++c) {
         if (tabu && ((c - 1) & (G - 1)) == 0) {
@@ -353,7 +454,9 @@ __global__ void __launch_bounds__(256) qap_search_warp_kernel(const SearchParams
         const int i = loc ? gl : 0;
         const int pi = loc ? my_p : 0;
         const bool mid = loc && (gl != r) && (gl != s);
-        const unsigned tr = myTab[r * G], ts = myTab[s * G];
+        unsigned tr, ts;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tr) : "r"(tab_sa + (unsigned)r * (G * 4)));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ts) : "r"(tab_sa + (unsigned)s * (G * 4)));
         int32_t *p_ir = sW + (tr & 0xffffu), *p_ri = sW + (tr >> 16);
         int32_t *p_is = sW + (ts & 0xffffu), *p_si = sW + (ts >> 16);
         int32_t m_ir = 0, m_ri = 0, m_is = 0, m_si = 0;

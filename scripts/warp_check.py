@@ -42,7 +42,7 @@ for n in NS:
             print("multistart MISMATCH n", n, algo)
 print("warp_check", kind, "mismatches:", bad, "threads", di.info["threads"], "smem", di.info["smem_bytes"], "ctas/SM", di.info["ctas_per_sm"])
 if len(sys.argv) > 2:
-    cases = (("tai30a", 1, 1000), ("tai30a", 1776, 240), ("tai30a", 4736, 240), ("nug12", 1776, 96), ("nug12", 4736, 96))
+    cases = (("tai30a", 1, 1000), ("tai30a", 1776, 240), ("tai30a", 4736, 240), ("tai30a", 9472, 240), ("nug12", 1776, 96), ("nug12", 4736, 96))
     if os.environ.get("WARP_TIME") == "small":
         cases = (("nug12", 1, 1000), ("nug12", 1776, 96), ("nug12", 4736, 96), ("nug12", 9472, 96), ("tai16a", 4736, 128))
     for name, starts, iters in cases:

@@ -490,7 +490,7 @@ def test_every_launch_plan_gives_identical_results(q, orc, shape, iters):
     di = DeviceInstance(inst.flow, inst.distance)
     try:
         plans = di.plan_candidates()
-        assert len(plans) >= 2 and di.info["storage"] == 3
+        assert len(plans) >= 2 and di.info["storage"] in (3, 4)
         for plan in plans:
             di.set_plan(plan)
             costs, bc, bi, bp = di.multistart("tabu", 13, 0, 5, iters, lo, hi)
