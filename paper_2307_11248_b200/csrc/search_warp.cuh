@@ -434,7 +434,6 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
         steps_done = c;
         const bool is_winner = my_key == bkey;
         const int pr = __shfl_sync(gmask, my_p, r, G), ps = __shfl_sync(gmask, my_p, s, G);
-        const int32_t hr = __shfl_sync(gmask, h, r, G), hs = __shfl_sync(gmask, h, s, G);
         const int32_t ten = tabu ? __shfl_sync(gmask, my_ten, (c - 1) & (G - 1), G) : 0;
         {
             const int R = r >> 2, S = s >> 2;
@@ -460,8 +459,9 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
         int32_t *p_ir = sW + (tr & 0xffffu), *p_ri = sW + (tr >> 16);
         int32_t *p_is = sW + (ts & 0xffffu), *p_si = sW + (ts >> 16);
         int32_t m_ir = 0, m_ri = 0, m_is = 0, m_si = 0;
-        if (loc && gl != r) { m_ir = *p_ir; m_ri = *p_ri; }   // (lane s: M[s][r])
-        if (loc && gl != s) { m_is = *p_is; m_si = *p_si; }   // (lane r: M[r][s])
+        if (loc && gl != r) m_ir = *p_ir;   // (lane s: M[s][r])
+        if (loc && gl != s) m_is = *p_is;   // (lane r: M[r][s])
+        if (mid) { m_ri = *p_ri; m_si = *p_si; }
         int32_t kr = 0, ks = 0;  // corner terms, zero when both matrices are symmetric
         if (FULLSYM) {
             const int32_t Drs = D[r * npad + s], Fpspr = F[ps * npad + pr];
@@ -503,8 +503,8 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
             }
         }
         // corners: M'[r][s] = h[r] + kr, h'[r] = M[r][s] + ks;  M'[s][r] = h[s] + ks, h'[s] = M[s][r] + kr
-        if (loc && gl == r) { *p_is = hr + kr; h = m_is + ks; }
-        if (loc && gl == s) { *p_ir = hs + ks; h = m_ir + kr; }
+        if (loc && gl == r) { *p_is = h + kr; h = m_is + ks; }
+        if (loc && gl == s) { *p_ir = h + ks; h = m_ir + kr; }
         V.HI[gl] = 4 * xu - 16 * h;
         V.HJ[gl] = xu - 16 * h;
         my_p = (gl == r) ? ps : (gl == s) ? pr : my_p;

@@ -16,6 +16,9 @@ prof r2_ncu_full_search_hybrid_tai256c_148x1024 qap_search_hybrid tai256c 148 10
 prof r2_ncu_full_search_hybrid_tai160a_296x640 qap_search_hybrid tai160a 296 640
 prof r2_ncu_full_search_hybrid_wide_tai150b_296x1200 qap_search_hybrid tai150b 296 1200
 prof r2_ncu_full_build_m_whole_tai100a qap_build_m tai100a 1024 800
+prof r2_ncu_full_search_warp_tai30a_1776x240 qap_search_warp tai30a 1776 240
+prof r2_ncu_full_search_warp_nug12_4736x96 qap_search_warp nug12 4736 96
+python scripts/single_start_time.py > gpurun_out/r2_single_start_latency.txt 2>&1
 compute-sanitizer --tool memcheck python scripts/sanitize_small.py > gpurun_out/r2_sanitizer_memcheck.log 2>&1
 compute-sanitizer --tool racecheck python scripts/sanitize_small.py > gpurun_out/r2_sanitizer_racecheck.log 2>&1
 tail -3 gpurun_out/r2_sanitizer_memcheck.log gpurun_out/r2_sanitizer_racecheck.log
