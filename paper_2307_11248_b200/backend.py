@@ -179,8 +179,9 @@ class DeviceInstance:
 
     def plan_candidates(self) -> list[tuple[int, int, int, int]]:
         """Launch configurations that fit this instance: (register units per thread, threads carrying
-        off-diagonal units, shared-memory units per thread, diagonal blocks in shared memory); the
-        library's default choice first.  Empty for instances served by the generic kernel."""
+        off-diagonal units, shared-memory units per thread, diagonal blocks in shared memory); register
+        units 0 is the one-warp-per-search kernel (n <= 32), listed first where it applies.  Empty for
+        instances served by the generic kernel."""
         buf = np.zeros((16, 4), np.int32)
         count = ctypes.c_int(0)
         _lib.check(_lib.lib().qapb_plan_candidates(self._h, _addr(buf), 16, ctypes.byref(count)))
