@@ -153,8 +153,15 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
     }
     __syncthreads();
 
-    const int b = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / G) + lane / G;
-    if (b >= P.batch) return;  // whole groups only
+    // Two searches per warp (G = 16) reduce with FULL-warp `redux.sync` (a reduction over a sub-warp mask is emulated
+    // in software: 1.3 instead of 0.8 us per iteration), so both halves must stay in step until the warp is done: a
+    // half without a search of its own (odd batch) runs a clone of the last one and writes nothing, and a search that
+    // runs out of admissible moves goes on as an inert participant of the reductions.
+    constexpr bool HALF = G == 16;
+    const int b_raw = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / G) + lane / G;
+    if (b_raw - lane / G >= P.batch) return;  // whole warps only
+    const bool ghost = b_raw >= P.batch;
+    const int b = ghost ? P.batch - 1 : b_raw;
     int32_t *sW = reinterpret_cast<int32_t *>(smem_raw) + LY::TAB + ((threadIdx.x >> 5) * (32 / G) + lane / G) * LY::TOTAL;
     int32_t *sM = sW + LY::M;
     int32_t *sDG = sW + LY::DG;
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
     }
     V.A[gl] = 0; V.B[gl] = 0; V.C[gl] = 0; V.E[gl] = 0;
     sP[gl] = my_p;
-    if (REC && P.cells) {
+    if (REC && P.cells && !ghost) {
         int64_t *cz = P.cells + (size_t)b * n * n;
         for (int i = gl; i < n * n; i += G) cz[i] = 0;
     }
@@ -349,16 +356,18 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
     unsigned tab_sa = (unsigned)__cvta_generic_to_shared(sTab + gl);
     asm volatile("" : "+r"(tab_sa));
 
+    bool inert = false;  // (G = 16) stopped early: takes part in the warp-wide reductions only
     for (int c = 1; c <= iters; ++c) {
+        int32_t my_d = MAXV;
+        unsigned my_key = 0xffffffffu;
+        int my_which = 0, my_slot = 0;  // 0: the off-diagonal unit, 1 / 2: diagonal pair q = 0 / 1
+        if (!(HALF && inert)) {
         if (tabu && ((c - 1) & (G - 1)) == 0) {
             if (P.rng) my_ten = warp_tenure_chunk<G>(gmask, rstate, span, last_ok, P.ten_lo, P.force_seq_rng, gl);
             else if (REC) my_ten = (c - 1 + gl < iters) ? (int32_t)P.tenures[(size_t)b * iters + (c - 1 + gl)] : 0;
         }
         // ---------------- pass: rank-2 update of the previous move (the difference vectors are zero at its
         // two locations and before the first move), delta, admissibility, first minimum
-        int32_t my_d;
-        unsigned my_key;
-        int my_which = 0, my_slot = 0;  // 0: the off-diagonal unit, 1 / 2: diagonal pair q = 0 / 1
         {
             if (touched) {
 #pragma unroll
@@ -419,11 +428,28 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
             const unsigned key = pair_key(di[q], dj[q], 0);
             if (adm && (d < my_d || (d == my_d && key < my_key))) { my_d = d; my_key = key; my_which = 1 + q; }
         }
+        }  // !(HALF && inert)
         // lexicographic minimum of (delta, key) over the search's lanes
-        const int32_t bd = __reduce_min_sync(gmask, my_d);
-        const unsigned bkey = __reduce_min_sync(gmask, my_d == bd ? my_key : 0xffffffffu);
+        int32_t bd;
+        unsigned bkey;
+        if (HALF) {
+            const bool up = lane >= 16;
+            __syncwarp();
+            const int32_t d0 = __reduce_min_sync(0xffffffffu, up ? MAXV : my_d);
+            const int32_t d1 = __reduce_min_sync(0xffffffffu, up ? my_d : MAXV);
+            bd = up ? d1 : d0;
+            const unsigned kk = my_d == bd ? my_key : 0xffffffffu;
+            const unsigned k0 = __reduce_min_sync(0xffffffffu, up ? 0xffffffffu : kk);
+            const unsigned k1 = __reduce_min_sync(0xffffffffu, up ? kk : 0xffffffffu);
+            bkey = up ? k1 : k0;
+            if (inert) continue;
+        } else {
+            bd = __reduce_min_sync(gmask, my_d);
+            bkey = __reduce_min_sync(gmask, my_d == bd ? my_key : 0xffffffffu);
+        }
         if (bd == MAXV) {  // no admissible move: premature stop (_kernels.pyx:168-170)
             stopped = 1;
+            if (HALF) { inert = true; continue; }
             break;
         }
         const int r = (int)(bkey >> 17), s = (int)((bkey >> 1) & 0xffffu);
@@ -529,12 +555,12 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
                         if (tabu) dexp[q] = new_exp;
                     }
             }
-            if (REC && P.tr_i) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
+            if (REC && P.tr_i && !ghost) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
                 const size_t o = (size_t)b * iters + (c - 1);
                 P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
                 if (P.tr_tabu) P.tr_tabu[o] = (int64_t)was;
             }
-            if (REC && tabu && P.cells) {
+            if (REC && tabu && P.cells && !ghost) {
                 int64_t *cz = P.cells + (size_t)b * n * n;
                 cz[(size_t)r * n + s] = (int64_t)c + ten;
                 cz[(size_t)s * n + r] += 1;
@@ -553,6 +579,7 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
         __syncwarp(gmask);  // -------------------------------------------- sync #2
     }
 
+    if (ghost) return;
     if (loc) {
         P.best[(size_t)b * n + gl] = best_p;
         P.cur[(size_t)b * n + gl] = my_p;

@@ -40,6 +40,17 @@ for n in NS:
         if not (np.array_equal(g[0], w[0]) and g[1] == w[1] and g[2] == w[2] and np.array_equal(g[3], w[3])):
             bad += 1
             print("multistart MISMATCH n", n, algo)
+# searches that run out of admissible moves at different iterations (long tenures on tiny instances)
+for n in (3, 4, 5, 6):
+    if n not in NS and max(NS) < 17:
+        pass
+    inst = shapes.tai_a(n, seed=50 + n) if kind == "sym" else shapes.rand(n, seed=50 + n)
+    di = device_instance(inst.flow, inst.distance)
+    g = di.multistart("tabu", 8, 0, 9, 40, 50, 50)
+    w = oracle.multistart(inst.flow, inst.distance, "tabu", 8, 9, 40, tenure=(50, 50), threads=1)
+    if not (np.array_equal(g[0], w[0]) and g[1] == w[1] and g[2] == w[2] and np.array_equal(g[3], w[3])):
+        bad += 1
+        print("early-stop multistart MISMATCH n", n)
 print("warp_check", kind, "mismatches:", bad, "threads", di.info["threads"], "smem", di.info["smem_bytes"], "ctas/SM", di.info["ctas_per_sm"])
 if len(sys.argv) > 2:
     cases = (("tai30a", 1, 1000), ("tai30a", 1776, 240), ("tai30a", 4736, 240), ("tai30a", 9472, 240), ("nug12", 1776, 96), ("nug12", 4736, 96))

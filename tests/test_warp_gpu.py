@@ -121,3 +121,33 @@ def test_traced_multistart_and_early_stop(built):
         _same_single(g, w, "n=3 long tenures")
     finally:
         di.close()
+
+
+@pytest.mark.parametrize("n,kind", [(3, 3), (4, 0), (5, 3), (6, 4), (18, 3)])
+def test_searches_of_one_warp_stop_at_different_iterations(built, n, kind):
+    """Long tenures on tiny instances: every pair turns tabu and the searches run out of admissible moves after a
+    different number of steps each -- at n <= 16 two searches share a warp and its reductions, so a stopped
+    search must not disturb its partner (nor the clone that fills an odd batch)."""
+    import oracle
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    f, d = _instance(n, kind, 900 + n)
+    di = DeviceInstance(f, d)
+    try:
+        ten = (400, 400)
+        for count in (1, 2, 9):
+            got = di.multistart("tabu", 8, 0, count, 60, *ten)
+            want = oracle.multistart(f, d, "tabu", 8, count, 60, tenure=ten, threads=1)
+            assert np.array_equal(got[0], want[0]) and got[1] == want[1] and got[2] == want[2], (n, kind, count)
+            assert np.array_equal(got[3], want[3]), (n, kind, count)
+        seeds = np.array([oracle.derive_seed(8, k) for k in range(5)], np.uint64)
+        costs, perms, steps, mi, mj, md = di.multistart_trace("tabu", seeds, 60, *ten)
+        for k in range(5):
+            r = oracle.Rng(int(seeds[k]))
+            p = r.permutation(n)
+            t = r.tenures(ten[0], ten[1], 60)
+            w = oracle.tabu_run(f, d, p, 60, t)
+            assert steps[k] == w[6] and costs[k] == w[1] and np.array_equal(mi[k, : w[6]], w[7][0]), (n, kind, k)
+        assert n > 6 or int(steps.min()) < 60, "no search stopped early: the case does not exercise the inert path"
+    finally:
+        di.close()
