@@ -84,7 +84,10 @@ typedef void (*kern_t)(const SearchParams);
 #elif QAPB_DEV_ONLY == 9 // tai150b: 64-bit deltas over unsigned 32-bit state, shared-memory plan with DSM, one symmetric matrix
 #define QAPB_DEV_ARGS 2, false, 2, true, false, 128, true, false, true, false, false, true
 #elif QAPB_DEV_ONLY == 12 // preset 1 at 88 registers (still two 352-thread CTAs per SM)
-#define QAPB_DEV_ARGS 1, true, 1, false, true, 88, false, false, false
+#ifndef QAPB_DEV_REGS
+#define QAPB_DEV_REGS 88
+#endif
+#define QAPB_DEV_ARGS 1, true, 1, false, true, QAPB_DEV_REGS, false, false, false
 #elif QAPB_DEV_ONLY == 13 // one-warp searches at 80 registers (25 per SM)
 #define QAPB_DEV_ARGS 1, true, 1, false, false, 80, false, false, false, true, true
 #elif QAPB_DEV_ONLY == 14 // one-warp searches at 96 registers (21 per SM)

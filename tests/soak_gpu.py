@@ -1,7 +1,8 @@
 """Randomised differential soak: GPU multistart / tabu_run / two_opt_run vs the C oracle on random
 instances (sizes, value ranges, symmetry, diagonals), every launch plan of each instance.
-Usage: python tests/soak_gpu.py [seconds] [seed]   (development aid; the oracle is the checker)"""
-import sys, time
+Usage: python tests/soak_gpu.py [seconds] [seed]   (development aid; the oracle is the checker)
+SOAK_SMALL=1 restricts the sizes to n = 2 .. 32 (the one-warp-per-search kernel) with batches of up to 70 starts."""
+import os, sys, time
 sys.path.insert(0, ".")
 import numpy as np
 import __graft_entry__ as e
@@ -15,6 +16,9 @@ rs = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 t0 = time.time(); cases = 0; plans_run = 0
 while time.time() - t0 < budget:
     n = int(rs.choice([2, 3, 4, 5, 7, 8, 9, 12, 16, 17, 23, 31, 32, 33, 40, 48, 63, 64, 65, 80, 100, 129, 140]))
+    small = os.environ.get("SOAK_SMALL") == "1"
+    if small:
+        n = int(rs.integers(2, 33))
     hi = int(rs.choice([2, 10, 100, 1000, 40000, 3000000]))
     lo = -hi if rs.random() < 0.2 else 0
     f = rs.integers(lo, hi + 1, (n, n)).astype(np.int64)
@@ -29,7 +33,7 @@ while time.time() - t0 < budget:
     iters = int(rs.integers(1, 3 * n + 8)) if n <= 64 else int(rs.integers(1, 40))
     if n <= 33 and rs.random() < 0.08:
         iters = int(rs.integers(250, 700))  # across the 256-iteration tenure chunk boundaries
-    starts = int(rs.integers(1, 7))
+    starts = int(rs.integers(1, 71 if small else 7))
     algo = "tabu" if rs.random() < 0.7 else "2opt"
     master = int(rs.integers(0, 2**62))
     lo_t, hi_t = oracle.tenure_bounds(n)
