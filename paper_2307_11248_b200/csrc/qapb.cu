@@ -67,6 +67,9 @@ struct qapb_handle {
 };
 
 typedef void (*kern_t)(const SearchParams);
+#ifndef QAPB_DEV_REGS
+#define QAPB_DEV_REGS 88
+#endif
 #ifdef QAPB_DEV_ONLY
 // development build (seconds instead of minutes): only one instantiation, -DQAPB_DEV_ONLY=<preset>
 #if QAPB_DEV_ONLY == 1   // tai100a / sko100 multi-start tabu (staged one-register-unit plan)
@@ -98,6 +101,10 @@ typedef void (*kern_t)(const SearchParams);
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 64, false, false, true, true
 #elif QAPB_DEV_ONLY == 3 // recording instantiation of preset 1 (single-run entries: parity tests)
 #define QAPB_DEV_ARGS 1, true, 1, false, true, 80
+#elif QAPB_DEV_ONLY == 40 // ONE register unit + shared-memory units, DSM, multi-start tabu (n = 129..256: QAPB_PLAN=1,512,3,1 + QAPB_UR1_SMEM=1)
+#define QAPB_DEV_ARGS 1, true, 1, true, false, QAPB_DEV_REGS, true, false, false
+#elif QAPB_DEV_ONLY == 41 // ... with 64-bit deltas, one symmetric matrix (tai150b: QAPB_PLAN=1,256,2,1)
+#define QAPB_DEV_ARGS 2, false, 1, true, false, QAPB_DEV_REGS, true, false, false, false, false, true
 #elif QAPB_DEV_ONLY == 20 // one warp per search (search_warp.cuh), symmetric, multi-start tabu
 #define QAPB_DEV_WARP 1, false, false, 32
 #elif QAPB_DEV_ONLY == 21 // ... recording instantiation
@@ -143,10 +150,11 @@ static kern_t pick_wide_kernel(int symm, int plan)
 {
 #define KW(S) {(kern_t) qap_search_hybrid_kernel<S, false, 1, false, false, 80, false, false, true, false, false, true>, \
                (kern_t) qap_search_hybrid_kernel<S, false, 1, false, true, 80, false, false, true, false, false, true>,  \
-               (kern_t) qap_search_hybrid_kernel<S, false, 2, true, false, 128, true, false, true, false, false, true>}
-    static kern_t tab[3][3] = {KW(0), KW(1), KW(2)};
+               (kern_t) qap_search_hybrid_kernel<S, false, 2, true, false, 128, true, false, true, false, false, true>,  \
+               (kern_t) qap_search_hybrid_kernel<S, false, 1, true, false, 128, true, false, true, false, false, true>}
+    static kern_t tab[3][4] = {KW(0), KW(1), KW(2)};
 #undef KW
-    return tab[symm][plan == 5 ? 2 : plan];
+    return tab[symm][plan == 9 ? 3 : plan == 5 ? 2 : plan];
 }
 
 static kern_t pick_hybrid_kernel(int symm, int packed, int plan)
@@ -160,6 +168,9 @@ static kern_t pick_hybrid_kernel(int symm, int packed, int plan)
     // plan 5: plan 2 with the diagonal blocks in shared memory (no dedicated diagonal warps)
     // plan 6/7: plan 0/1 with the diagonal blocks paired in the threads after the last unit (DD), 64 registers
     // plan 8: plan 6 as ONE warp (n <= 32): warp barriers, 32 searches per SM
+    // plan 9: plan 5 with ONE register unit per thread (the rest in shared memory): no spills at 128 registers --
+    //         instantiated for two symmetric matrices with packed keys (tai256c: 846 -> 887 G evals/s) and for 64-bit deltas
+    if (plan == 9) return (kern_t) qap_search_hybrid_kernel<1, true, 1, true, false, 128, true>;
 #define KH(S, PK) {(kern_t) qap_search_hybrid_kernel<S, PK, 1, false, false, 80>, \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 1, false, true, 80>,  \
                    (kern_t) qap_search_hybrid_kernel<S, PK, 2, true, false, 128>,  \
@@ -191,6 +202,9 @@ static kern_t pick_hybrid_kernel(int symm, int packed, int plan)
 static kern_t multistart_kernel(int symm, int packed, int plan, int two_opt, int regs88)
 {
     if (!packed || symm > 1) return nullptr;
+    if (plan == 9)
+        return two_opt ? (kern_t) qap_search_hybrid_kernel<1, true, 1, true, false, 128, true, true, false>
+                       : (kern_t) qap_search_hybrid_kernel<1, true, 1, true, false, 128, true, false, false>;
 #define KM(S, NT) (plan == 1 ? ((regs88 && S == 1) ? (kern_t) qap_search_hybrid_kernel<1, true, 1, false, true, 88, false, NT, false> \
                                        : (kern_t) qap_search_hybrid_kernel<S, true, 1, false, true, 80, false, NT, false>) \
                    : plan == 7 ? (kern_t) qap_search_hybrid_kernel<S, true, 1, false, true, 64, false, NT, false, true> \
@@ -243,7 +257,7 @@ static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_op
     // packed (delta, slot) keys need |delta|*16 + 15 < 2^31
     const int packed = h->delta_bound < ((1LL << 27) - 1);
     int plan = h->us > 0 ? 2 : (h->upt == 2 ? (h->staged ? 4 : 3) : (h->staged ? 1 : 0));
-    if (h->dsm) plan = 5;
+    if (h->dsm) plan = h->upt == 1 ? 9 : 5;
     if (h->dd) plan = h->ow ? 8 : h->staged ? 7 : 6;
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
     if (h->storage == 3 && h->wk) return pick_warp_kernel(h->symmetric ? 1 : 0, multistart, two_opt, h->wk);
@@ -285,7 +299,9 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     if (h->wide && (dd || (ur == 2 && !dsm))) return false;  // 64-bit deltas: plans 0 / 1 / 5 only
     if (dd && !(ur == 1 && us == 0 && toff >= h->noff + (nb + 1) / 2)) return false;
     const int threads = (dsm || dd) ? toff : toff + 32 * dw;
-    if (dsm && !(ur == 2 && us > 0)) return false;  // the instantiated shape
+    // the instantiated shapes: two register units, or one for 64-bit deltas / two symmetric matrices with packed keys
+    const bool ur1_smem = ur == 1 && (h->wide || (h->symmetric && h->delta_bound < ((1LL << 27) - 1)));
+    if (dsm && !((ur == 2 || ur1_smem) && us > 0)) return false;
     if (dsm && threads < nb) return false;
     if ((long long)(ur + us) * toff < h->noff) return false;
     if (threads > 1024 || (us > 0 && threads > 512) || (us == 0 && ur == 2 && threads > 608)) return false;
@@ -302,7 +318,7 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     }
     if (L.total > smem_cap) return false;
     if (threads < h->n) return false;  // the publish phase maps one location per thread
-    if (h->npad > 128 && !(us > 0 && ur == 2)) return false;  // layout size class 256 is tied to the (2 + smem) shape
+    if (h->npad > 128 && !(us > 0 && (ur == 2 || (ur == 1 && dsm)))) return false;  // layout size class 256 goes with shared-memory units
     if (h->npad <= 128 && us > 0) return false;
     int staged = 0;
     if (us == 0 && h->fits_i16 && !ow && !getenv("QAPB_NO_STAGE")) {
@@ -349,8 +365,17 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
         // diagonal-warp plan); else all 512 threads on one search (4 units per thread at n = 256
         // instead of 4 or 5 on 14 of 16 warps: 710 -> 750 G evals/s).
         if (!getenv("QAPB_NO_DSM") || h->wide) {
+            const bool ur1 = !getenv("QAPB_NO_UR1");
+            // 64-bit deltas: ONE register unit per thread keeps the 128-register kernel free of spills (tai150b:
+            // 428 -> 484 G evals/s with two searches per SM)
+            if (h->wide && ur1 && try_hybrid_plan(h, smem_cap, 1, 256, std::max(1, (noff - 256 + 255) / 256), 1, 113u * 1024u) &&
+                hybrid_occupancy(h) >= 2)
+                return true;
             const int us2 = std::max(1, (noff - 2 * 256 + 255) / 256);
             if (try_hybrid_plan(h, smem_cap, 2, 256, us2, 1, 113u * 1024u) && hybrid_occupancy(h) >= 2) return true;
+            // one search per SM: one register unit per thread where that shape is instantiated and fits (n = 200:
+            // 678 -> 701, n = 256: 846 -> 887 G evals/s), else two
+            if (!h->wide && ur1 && try_hybrid_plan(h, smem_cap, 1, 512, std::max(1, (noff - 512 + 511) / 512), 1)) return true;
             const int us1 = std::max(1, (noff - 2 * 512 + 511) / 512);
             if (try_hybrid_plan(h, smem_cap, 2, 512, us1, 1)) return true;
         }
@@ -395,6 +420,7 @@ static std::vector<std::array<int, 4>> hybrid_candidates(const qapb_handle *h)
     if (h->npad <= 32 && !h->wide && h->acc_bits == 32 && h->delta_bound < ((1LL << 27) - 1)) out.push_back({0, 32, 0, 0});
     if (nb > 32) {
         for (int t : {256, 384, 512}) add(2, t, std::max(1, (noff - 2 * t + t - 1) / t), 1);
+        for (int t : {256, 512}) add(1, t, std::max(1, (noff - t + t - 1) / t), 1);  // (kept if the shape is instantiated for the instance)
         const int toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
         if (!h->wide) add(2, toff, std::max(0, (noff - 2 * toff + toff - 1) / toff), 0);
     } else {

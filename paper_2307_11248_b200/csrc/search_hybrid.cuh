@@ -480,7 +480,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     int32_t *sM = reinterpret_cast<int32_t *>(smem_raw + lay.offM);
     unsigned *sTB = reinterpret_cast<unsigned *>(smem_raw + lay.offTB);
     int32_t *sMX = reinterpret_cast<int32_t *>(smem_raw + lay.offMX);
-    constexpr int NPM = OW ? 32 : (SMEMU && UR == 2) ? 256 : 128;  // size class of the plan (host: make_hyb_layout)
+    constexpr int NPM = OW ? 32 : SMEMU ? 256 : 128;  // size class of the plan (host: make_hyb_layout; shared-memory units <=> n > 128)
     Vecs V;
     V.A = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(0, NPM));
     V.C = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(1, NPM));
