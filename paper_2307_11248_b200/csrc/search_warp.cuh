@@ -4,19 +4,22 @@
 // two-level argmin and register-indexed fix-up regions per iteration; at n <= 32 a whole search is 28
 // off-diagonal units, so that machinery is all that is left of the iteration.  Here a search is one warp
 // and nothing but warp-synchronous code:
-//   * lane l is LOCATION l for the publish phase (p[l], h[l] live in its registers), off-diagonal UNIT l
-//     (block pair {(I,J),(J,I)}, lexicographic over I < J, 16 pairs) for the pass, and the owner of the
-//     diagonal-block pairs l and l + 32 (of 6 per diagonal block), one scalar pair at a time -- every lane
-//     runs the same instruction stream, there is no diagonal warp or diagonal path to diverge into;
-//   * the placement matrix lives in the warp's slice of shared memory: off-diagonal units in the private
-//     layout of the generic kernel (row w of unit l at (w*32 + l)*16 bytes: conflict-free 128-bit LDS/STS),
-//     diagonal blocks as plain 4x4 tiles.  Addresses are free to index at run time, so the 4n entries on
-//     rows/columns r,s are fixed in place by the lane of their location -- four loads, four stores -- with no
-//     column dump, no fix-up vectors and no register-indexed switch;
+//   * lane l is LOCATION l for the publish phase (p[l], h[l] live in its registers), the owner of one
+//     off-diagonal UNIT (block pair {(I,J),(J,I)}, 16 pairs; the unit whose chunk slot is l) for the pass, and
+//     the owner of the diagonal-block pairs l and l + 32 (of 6 per diagonal block), one scalar pair at a
+//     time -- every lane runs the same instruction stream, there is no diagonal warp or diagonal path to
+//     diverge into;
+//   * the unit stays in the lane's REGISTERS; the 4n entries on rows/columns r,s of a move are fixed in place
+//     in the warp's slice of shared memory: the lanes whose unit touches block R or S flush it to its slot
+//     (conflict-free 128-bit stores), the lane of location i patches M[i][r], M[r][i], M[i][s], M[s][i]
+//     there -- four loads, four stores, addresses from a table shared by the CTA -- and the touched units
+//     reload at the start of the next pass: no column dump, no fix-up vectors, no register-indexed switch;
 //   * the argmin is two `redux.sync`; the two barriers of an iteration are `__syncwarp()`;
-//   * tenures are drawn 32 at a time, one per lane (exact sequential replay on a rejected draw), and the
-//     tenure of an iteration comes out of its lane by shuffle;
-//   * searches share nothing, so any number of them can be packed into a CTA (blockDim.x / 32).
+//   * the start permutation, the tenure stream (32 draws at a time, one per lane, exact sequential replay on
+//     a rejected draw; the tenure of an iteration comes out of its lane by shuffle) and the initial
+//     placement matrix are produced in this kernel: a small-n multistart is two launches (search, pick);
+//   * searches share nothing but the address table, so a CTA holds 1-4 warps; at n <= 16 a search is a
+//     half-warp (G = 16) and a warp runs two.
 // Same integers as every other plan: the formulas of the publish phase are the ones of search_hybrid.cuh.
 // int32 state with packed selection keys only (|delta| < 2^27, host-proven); other instances of this size
 // keep the hybrid plans.
