@@ -132,7 +132,10 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
     constexpr bool FULLSYM = SYMM == 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, gl = lane & (G - 1);
-    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    // Every warp collective names the FULL warp (a run-time sub-warp mask makes the compiler guard each shuffle with
+    // MATCH / VOTE convergence checks); with G = 16 the two searches of a warp therefore run in lockstep, shuffles
+    // and votes segmented by their width argument.
+    constexpr unsigned gmask = 0xffffffffu;
     const int n = P.n, nb = P.nb, npad = P.npad, noff = P.noff;
 
     // shared by the searches of the CTA: chunk slot of every unit and its inverse, then the address table:
@@ -156,10 +159,10 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
     }
     __syncthreads();
 
-    // Two searches per warp (G = 16) reduce with FULL-warp `redux.sync` (a reduction over a sub-warp mask is emulated
-    // in software: 1.3 instead of 0.8 us per iteration), so both halves must stay in step until the warp is done: a
-    // half without a search of its own (odd batch) runs a clone of the last one and writes nothing, and a search that
-    // runs out of admissible moves goes on as an inert participant of the reductions.
+    // Two searches per warp (G = 16): both halves must stay in step until the warp is done.  A half without a search
+    // of its own (odd batch) runs a clone of the last one and writes nothing, and a search that runs out of
+    // admissible moves goes on INERT: it keeps executing the iteration on a dummy move (0, 1) -- every address stays
+    // valid, its matrix is garbage from then on -- while its results (costs, permutations, step count) are frozen.
     constexpr bool HALF = G == 16;
     const int b_raw = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / G) + lane / G;
     if (b_raw - lane / G >= P.batch) return;  // whole warps only
@@ -364,7 +367,6 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
         int32_t my_d = MAXV;
         unsigned my_key = 0xffffffffu;
         int my_which = 0, my_slot = 0;  // 0: the off-diagonal unit, 1 / 2: diagonal pair q = 0 / 1
-        if (!(HALF && inert)) {
         if (tabu && ((c - 1) & (G - 1)) == 0) {
             if (P.rng) my_ten = warp_tenure_chunk<G>(gmask, rstate, span, last_ok, P.ten_lo, P.force_seq_rng, gl);
             else if (REC) my_ten = (c - 1 + gl < iters) ? (int32_t)P.tenures[(size_t)b * iters + (c - 1 + gl)] : 0;
@@ -431,7 +433,6 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
             const unsigned key = pair_key(di[q], dj[q], 0);
             if (adm && (d < my_d || (d == my_d && key < my_key))) { my_d = d; my_key = key; my_which = 1 + q; }
         }
-        }  // !(HALF && inert)
         // lexicographic minimum of (delta, key) over the search's lanes
         int32_t bd;
         unsigned bkey;
@@ -445,23 +446,25 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
             const unsigned k0 = __reduce_min_sync(0xffffffffu, up ? 0xffffffffu : kk);
             const unsigned k1 = __reduce_min_sync(0xffffffffu, up ? kk : 0xffffffffu);
             bkey = up ? k1 : k0;
-            if (inert) continue;
         } else {
             bd = __reduce_min_sync(gmask, my_d);
             bkey = __reduce_min_sync(gmask, my_d == bd ? my_key : 0xffffffffu);
         }
-        if (bd == MAXV) {  // no admissible move: premature stop (_kernels.pyx:168-170)
+        if (bd == MAXV && !inert) {  // no admissible move: premature stop (_kernels.pyx:168-170)
             stopped = 1;
-            if (HALF) { inert = true; continue; }
-            break;
+            if (!HALF) break;
+            inert = true;
         }
-        const int r = (int)(bkey >> 17), s = (int)((bkey >> 1) & 0xffffu);
-        cost += (long long)bd;
-        const bool improved = cost < best_cost;
+        const bool live = !(HALF && inert);
+        const int r = live ? (int)(bkey >> 17) : 0, s = live ? (int)((bkey >> 1) & 0xffffu) : 1;
+        if (live) cost += (long long)bd;
+        const bool improved = live && cost < best_cost;
         if (improved) best_cost = cost;
-        thr = Acc<int32_t>::clamp_thr(best_cost - cost);
-        steps_done = c;
-        const bool is_winner = my_key == bkey;
+        if (live) {
+            thr = Acc<int32_t>::clamp_thr(best_cost - cost);
+            steps_done = c;
+        }
+        const bool is_winner = live && my_key == bkey;
         const int pr = __shfl_sync(gmask, my_p, r, G), ps = __shfl_sync(gmask, my_p, s, G);
         const int32_t ten = tabu ? __shfl_sync(gmask, my_ten, (c - 1) & (G - 1), G) : 0;
         {
@@ -536,7 +539,7 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
         if (loc && gl == s) { *p_ir = h + ks; h = m_ir + kr; }
         V.HI[gl] = 4 * xu - 16 * h;
         V.HJ[gl] = xu - 16 * h;
-        my_p = (gl == r) ? ps : (gl == s) ? pr : my_p;
+        if (live) my_p = (gl == r) ? ps : (gl == s) ? pr : my_p;
         if (improved) best_p = my_p;
 
         // ---- the lane owning the winning pair: tabu memory, trail
