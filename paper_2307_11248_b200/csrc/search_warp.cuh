@@ -9,11 +9,11 @@
 //     the owner of the diagonal-block pairs l and l + 32 (of 6 per diagonal block), one scalar pair at a
 //     time -- every lane runs the same instruction stream, there is no diagonal warp or diagonal path to
 //     diverge into;
-//   * the unit stays in the lane's REGISTERS; the 4n entries on rows/columns r,s of a move are fixed in place
-//     in the warp's slice of shared memory: the lanes whose unit touches block R or S flush it to its slot
-//     (conflict-free 128-bit stores), the lane of location i patches M[i][r], M[r][i], M[i][s], M[s][i]
-//     there -- four loads, four stores, addresses from a table shared by the CTA -- and the touched units
-//     reload at the start of the next pass: no column dump, no fix-up vectors, no register-indexed switch;
+//   * the units live in the warp's slice of shared memory and stream through registers once per pass
+//     (conflict-free 128-bit loads and stores of the owner lane); the 4n entries on rows/columns r,s of a move
+//     are fixed in place there: the lane of location i patches M[i][r], M[r][i], M[i][s], M[s][i] -- four
+//     loads, four stores, addresses from a table shared by the CTA -- no column dump, no fix-up vectors, no
+//     register-indexed switch, and no divergent region on the serial path behind the argmin;
 //   * the argmin is two `redux.sync`; the two barriers of an iteration are `__syncwarp()`;
 //   * the start permutation, the tenure stream (32 draws at a time, one per lane, exact sequential replay on
 //     a rejected draw; the tenure of an iteration comes out of its lane by shuffle) and the initial
@@ -95,6 +95,22 @@ __device__ __forceinline__ unsigned wk_pair_words(int x, int y, const unsigned c
         w_yx = up ? wU + 4 * LY::RSW : wU;
     }
     return (unsigned)w_xy | ((unsigned)w_yx << 16);
+}
+
+// Predicated shared-memory accesses as single instructions: small `if` bodies on the serial path compile to
+// divergent regions, and waiting for their reconvergence (stall "branch resolving" at the BSYNC) was 7 % of an
+// iteration with the flush of the touched units alone.
+__device__ __forceinline__ int32_t lds32_if(bool p, const int32_t *ptr, int32_t otherwise)
+{
+    int32_t v = otherwise;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.s32 %0, [%1];\n\t}"
+                 : "+r"(v) : "r"((unsigned)__cvta_generic_to_shared(ptr)), "r"((unsigned)p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts32_if(bool p, int32_t *ptr, int32_t v)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.s32 [%0], %1;\n\t}"
+                 :: "r"((unsigned)__cvta_generic_to_shared(ptr)), "r"(v), "r"((unsigned)p) : "memory");
 }
 
 // G tenures (tabu.py:184-186), one per lane: draw k of the chunk is mix64(state + (k+1)*GAMMA); a draw that
@@ -252,9 +268,10 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
     unsigned tb = 0xffffu, deadm = 0xffffu;  // pairs that are tabu now (pad slots permanently set: deadm)
     int32_t mexp = MAXV;                     // earliest expiry among the clearable bits
     int4 *myM = reinterpret_cast<int4 *>(sM) + gl;   // row w of this lane's unit: myM[w * G], rotated by w
-    // The unit stays in REGISTERS across iterations; it passes through its shared-memory slot only when it touches
-    // block row / column R or S of a move (flushed before the fix-ups, reloaded after them): half the shared-memory
-    // traffic of streaming every unit through the pass.
+    // The unit streams from its shared-memory slot through these registers once per pass.  (Keeping it in registers
+    // and moving only the ~13 units that touch block R or S of a move saves nothing: a predicated 128-bit access of
+    // 13 scattered lanes costs 3.4 of the 4 wavefronts of a full-warp one, and as `if` bodies the flush and the
+    // reload are divergent regions on the serial path.)
     int32_t U[4][4], L[4][4];
     int32_t h = 0;
     {
@@ -334,7 +351,12 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
     }
     V.HI[gl] = 4 * xu - 16 * h;
     V.HJ[gl] = xu - 16 * h;
-    bool touched = false;  // the unit was flushed for the fix-ups of the last move
+    __syncwarp(gmask);  // (the staged flow matrix has been read: its region now takes the unit slots)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // position k of a chunk holds element (k - u) & 3 of its row
+        myM[u * G] = make_int4(U[u][(0 - u) & 3], U[u][(1 - u) & 3], U[u][(2 - u) & 3], U[u][(3 - u) & 3]);
+        myM[(4 + u) * G] = make_int4(L[(0 - u) & 3][u], L[(1 - u) & 3][u], L[(2 - u) & 3][u], L[(3 - u) & 3][u]);
+    }
     __syncwarp(gmask);
 
     long long cost;  // _kernels.pyx:18-24, int64, including the diagonal products
@@ -374,15 +396,13 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
         // ---------------- pass: rank-2 update of the previous move (the difference vectors are zero at its
         // two locations and before the first move), delta, admissibility, first minimum
         {
-            if (touched) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int4 a = myM[u * G];
-                    const int4 l = myM[(4 + u) * G];
-                    const int32_t av[4] = {a.x, a.y, a.z, a.w}, lv[4] = {l.x, l.y, l.z, l.w};
+            for (int u = 0; u < 4; ++u) {  // position k of a chunk holds element (k - u) & 3 of its row
+                const int4 a = myM[u * G];
+                const int4 l = myM[(4 + u) * G];
+                const int32_t av[4] = {a.x, a.y, a.z, a.w}, lv[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) { U[u][v] = av[(v + u) & 3]; L[v][u] = lv[(v + u) & 3]; }
-                }
+                for (int v = 0; v < 4; ++v) { U[u][v] = av[(v + u) & 3]; L[v][u] = lv[(v + u) & 3]; }
             }
             int32_t aI[4], bI[4], aJ[4], bJ[4];
             ld_vec4(V.A, I, aI); ld_vec4(V.B, I, bI); ld_vec4(V.A, J, aJ); ld_vec4(V.B, J, bJ);
@@ -404,6 +424,13 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
                         U[u][v] += aI[u] * bJ[v] + cI[u] * eJ[v];
                         L[v][u] += aJ[v] * bI[u] + cJ[v] * eI[u];
                     }
+            }
+            // back to the slot (the lanes of the fix-ups read the entries on rows / columns r,s of the coming move
+            // there): stored here, the unit is off the serial path behind the argmin
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // position k of a chunk holds element (k - u) & 3 of its row
+                myM[u * G] = make_int4(U[u][(0 - u) & 3], U[u][(1 - u) & 3], U[u][(2 - u) & 3], U[u][(3 - u) & 3]);
+                myM[(4 + u) * G] = make_int4(L[(0 - u) & 3][u], L[(1 - u) & 3][u], L[(2 - u) & 3][u], L[(3 - u) & 3][u]);
             }
             int32_t dk;
             int sk;
@@ -429,9 +456,12 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
             sDG[q * 2 * G + gl] = x;
             sDG[q * 2 * G + G + gl] = y;
             const int32_t d = x + y - hi - hj;
-            const bool adm = dalive[q] && (NOTABU || dexp[q] <= c || d < thr);
+            const bool adm = dalive[q] & (NOTABU | (dexp[q] <= c) | (d < thr));
             const unsigned key = pair_key(di[q], dj[q], 0);
-            if (adm && (d < my_d || (d == my_d && key < my_key))) { my_d = d; my_key = key; my_which = 1 + q; }
+            const bool take = adm & ((d < my_d) | ((d == my_d) & (key < my_key)));  // (no short-circuit branches)
+            my_d = take ? d : my_d;
+            my_key = take ? key : my_key;
+            my_which = take ? 1 + q : my_which;
         }
         // lexicographic minimum of (delta, key) over the search's lanes
         int32_t bd;
@@ -467,18 +497,7 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
         const bool is_winner = live && my_key == bkey;
         const int pr = __shfl_sync(gmask, my_p, r, G), ps = __shfl_sync(gmask, my_p, s, G);
         const int32_t ten = tabu ? __shfl_sync(gmask, my_ten, (c - 1) & (G - 1), G) : 0;
-        {
-            const int R = r >> 2, S = s >> 2;
-            touched = own && (I == R || J == R || I == S || J == S);
-            if (touched) {
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {  // position k of a chunk holds element (k - u) & 3 of its row
-                    myM[u * G] = make_int4(U[u][(0 - u) & 3], U[u][(1 - u) & 3], U[u][(2 - u) & 3], U[u][(3 - u) & 3]);
-                    myM[(4 + u) * G] = make_int4(L[(0 - u) & 3][u], L[(1 - u) & 3][u], L[(2 - u) & 3][u], L[(3 - u) & 3][u]);
-                }
-            }
-        }
-        __syncwarp(gmask);  // -------------------------------------------- sync #1: the touched units are in shared memory
+        __syncwarp(gmask);  // -------------------------------------------- sync #1: every unit is in its slot
 
         // ---------------- publish: difference vectors of the move (old permutation), h', and the entries on
         // rows / columns r,s of M fixed in place by the lane of their location
@@ -542,45 +561,45 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
         if (live) my_p = (gl == r) ? ps : (gl == s) ? pr : my_p;
         if (improved) best_p = my_p;
 
-        // ---- the lane owning the winning pair: tabu memory, trail
-        if (is_winner) {
+        // ---- the lane owning the winning pair: tabu memory (branch-free: a divergent region costs its reconvergence),
+        // trail
+        {
             const int32_t new_exp = (int32_t)(c + ten);
-            unsigned was = 0;
-            if (my_which == 0) {
-                was = (tb >> my_slot) & 1u;
-                if (tabu) {
-                    tb |= 1u << my_slot;
-                    mexp = min(mexp, new_exp);
-                    xp[gl * 16 + my_slot] = new_exp;
-                }
-            } else {
+            const bool wu = is_winner && my_which == 0;   // the pair is in this lane's off-diagonal unit
+            unsigned was = wu ? (tb >> my_slot) & 1u : 0u;
 #pragma unroll
-                for (int q = 0; q < 2; ++q)
-                    if (my_which == 1 + q) {
-                        was = dexp[q] > c ? 1u : 0u;
-                        if (tabu) dexp[q] = new_exp;
-                    }
+            for (int q = 0; q < 2; ++q) {
+                const bool wq = is_winner && my_which == 1 + q;
+                was = (wq && dexp[q] > c) ? 1u : was;
+                dexp[q] = (wq && tabu) ? new_exp : dexp[q];
             }
-            if (REC && P.tr_i && !ghost) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
-                const size_t o = (size_t)b * iters + (c - 1);
-                P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
-                if (P.tr_tabu) P.tr_tabu[o] = (int64_t)was;
-            }
-            if (REC && tabu && P.cells && !ghost) {
-                int64_t *cz = P.cells + (size_t)b * n * n;
-                cz[(size_t)r * n + s] = (int64_t)c + ten;
-                cz[(size_t)s * n + r] += 1;
+            const bool wt = wu && tabu;
+            tb |= wt ? 1u << my_slot : 0u;
+            mexp = wt ? min(mexp, new_exp) : mexp;
+            sts32_if(wt, xp + gl * 16 + my_slot, new_exp);
+            if (REC && is_winner) {
+                if (P.tr_i && !ghost) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
+                    const size_t o = (size_t)b * iters + (c - 1);
+                    P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
+                    if (P.tr_tabu) P.tr_tabu[o] = (int64_t)was;
+                }
+                if (tabu && P.cells && !ghost) {
+                    int64_t *cz = P.cells + (size_t)b * n * n;
+                    cz[(size_t)r * n + s] = (int64_t)c + ten;
+                    cz[(size_t)s * n + r] += 1;
+                }
             }
         }
         // ---- tabu bits that expire at the next iteration are cleared here
-        if (!NOTABU && own && c + 1 >= mexp) {
+        if (!NOTABU) {
+            const bool due = own && c + 1 >= mexp;
             const unsigned live = tb & ~deadm;
-            if ((live & (live - 1u)) == 0u) {  // one tabu pair in this unit (the usual case): one load
-                const int32_t e = xp[gl * 16 + (__ffs(live) - 1)];
-                if (e <= c + 1) { tb &= ~live; mexp = MAXV; } else mexp = e;
-            } else {
-                expire_bits(tb, mexp, c + 1, xp + gl * 16);
-            }
+            const bool one = (live & (live - 1u)) == 0u;  // one tabu pair in this unit (the usual case): one predicated load
+            const int32_t e = lds32_if(due && one, xp + gl * 16 + (__ffs(live | 0x10000u) - 1), MAXV);
+            const bool clr = due && one && e <= c + 1;
+            tb = clr ? tb & ~live : tb;
+            mexp = (due && one) ? (clr ? MAXV : e) : mexp;
+            if (due && !one) expire_bits(tb, mexp, c + 1, xp + gl * 16);
         }
         __syncwarp(gmask);  // -------------------------------------------- sync #2
     }
