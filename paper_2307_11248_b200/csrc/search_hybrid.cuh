@@ -995,7 +995,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             if (REC && tabu && P.cells) {
                 int64_t *cz = P.cells + (size_t)b * n * n;
                 cz[(size_t)r * n + s] = (int64_t)c + ten;
-                cz[(size_t)s * n + r] += 1;
+                atomicAdd(reinterpret_cast<unsigned long long *>(cz + (size_t)s * n + r), 1ULL);  // (a reduction without return: the load-add-store would wait for L2)
             }
         }
         if (timing) tE = clock64();

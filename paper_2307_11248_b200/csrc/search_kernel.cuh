@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(MAXT, MINB) qap_search_kernel(const SearchPara
                         if (P.cells) {
                             int64_t *cz = P.cells + (size_t)b * n * n;
                             cz[(size_t)r * n + s] = (int64_t)c + ten;
-                            cz[(size_t)s * n + r] += 1;
+                            atomicAdd(reinterpret_cast<unsigned long long *>(cz + (size_t)s * n + r), 1ULL);  // (a reduction without return: the load-add-store would wait for L2)
                         }
                     }
                     a = 0; cc = 0; bb = 0; e = 0;

@@ -107,6 +107,14 @@ __device__ __forceinline__ int32_t lds32_if(bool p, const int32_t *ptr, int32_t 
                  : "+r"(v) : "r"((unsigned)__cvta_generic_to_shared(ptr)), "r"((unsigned)p) : "memory");
     return v;
 }
+__device__ __forceinline__ void stg64_if(bool p, int64_t *ptr, int64_t v)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.s64 [%0], %1;\n\t}" :: "l"(ptr), "l"(v), "r"((unsigned)p) : "memory");
+}
+__device__ __forceinline__ void redg64_inc_if(bool p, int64_t *ptr)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.global.add.u64 [%0], 1;\n\t}" :: "l"(ptr), "r"((unsigned)p) : "memory");
+}
 __device__ __forceinline__ void sts32_if(bool p, int32_t *ptr, int32_t v)
 {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.s32 [%0], %1;\n\t}"
@@ -577,17 +585,17 @@ __global__ void __launch_bounds__(256, QAPB_WARP_MINB) qap_search_warp_kernel(co
             tb |= wt ? 1u << my_slot : 0u;
             mexp = wt ? min(mexp, new_exp) : mexp;
             sts32_if(wt, xp + gl * 16 + my_slot, new_exp);
-            if (REC && is_winner) {
-                if (P.tr_i && !ghost) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
-                    const size_t o = (size_t)b * iters + (c - 1);
-                    P.tr_i[o] = r; P.tr_j[o] = s; P.tr_d[o] = (int64_t)bd;
-                    if (P.tr_tabu) P.tr_tabu[o] = (int64_t)was;
-                }
-                if (tabu && P.cells && !ghost) {
-                    int64_t *cz = P.cells + (size_t)b * n * n;
-                    cz[(size_t)r * n + s] = (int64_t)c + ten;
-                    cz[(size_t)s * n + r] += 1;
-                }
+            if (REC && P.tr_i && !ghost) {  // trail row (_kernels.pyx:182-187); was_tabu = cells[bi][bj] > c (:171)
+                const size_t o = (size_t)b * iters + (c - 1);
+                stg64_if(is_winner, P.tr_i + o, r);
+                stg64_if(is_winner, P.tr_j + o, s);
+                stg64_if(is_winner, P.tr_d + o, (int64_t)bd);
+                if (P.tr_tabu) stg64_if(is_winner, P.tr_tabu + o, (int64_t)was);
+            }
+            if (REC && tabu && P.cells && !ghost) {  // cells[r][s] = c + t, cells[s][r] += 1 (_kernels.pyx:176-178)
+                int64_t *cz = P.cells + (size_t)b * n * n;
+                stg64_if(is_winner, cz + (size_t)r * n + s, (int64_t)c + ten);
+                redg64_inc_if(is_winner, cz + (size_t)s * n + r);  // (a reduction without return: the load-add-store would wait for L2)
             }
         }
         // ---- tabu bits that expire at the next iteration are cleared here
