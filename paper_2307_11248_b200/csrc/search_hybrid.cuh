@@ -223,26 +223,33 @@ __device__ __forceinline__ int64_t wide_delta(int32_t u, int32_t l, int32_t hi, 
     return (int64_t)(uint32_t)u + (int64_t)(uint32_t)l - (int64_t)(uint32_t)hi - (int64_t)(uint32_t)hj;
 }
 
+// CH running first-minima (a 64-bit value and a slot each): one per block row where the registers allow it (one
+// register unit per thread: tai150b 484 -> 502 G evals/s), one per pair of rows in the two-register-unit plans
+template <int CH>
 __device__ __forceinline__ void unit_select_wide(const int32_t (&U)[4][4], const int32_t (&L)[4][4], unsigned tbk, int Ik,
                                                  int Jk, int64_t thr, const Vecs &V, int64_t &dbest, int &sbest)
 {
+    static_assert(CH == 2 || CH == 4, "two or four chains");
     int32_t hI[4], hJ[4];
     ld_vec4(V.H, Ik, hI);
     ld_vec4(V.H, Jk, hJ);
-    // two running first-minima (rows 0-1 and rows 2-3): a 64-bit value and a slot each -- more chains cost
-    // registers the 128-register plans do not have
-    int64_t rd[2] = {delta_max<int64_t>(), delta_max<int64_t>()};
-    int rs[2] = {0, 8};
+    int64_t rd[4] = {delta_max<int64_t>(), delta_max<int64_t>(), delta_max<int64_t>(), delta_max<int64_t>()};
+    int rs[4] = {0, 4, 8, 12};
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
+        const int ch = CH == 4 ? u : (u >> 1) * 2;
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int64_t d = wide_delta(U[u][v], L[v][u], hI[u], hJ[v]);
             const bool adm = !(tbk & (1u << (u * 4 + v))) || (d < thr);
-            if (adm && d < rd[u >> 1]) { rd[u >> 1] = d; rs[u >> 1] = u * 4 + v; }
+            if (adm && d < rd[ch]) { rd[ch] = d; rs[ch] = u * 4 + v; }
         }
     }
-    if (rd[1] < rd[0]) { rd[0] = rd[1]; rs[0] = rs[1]; }
+    if (CH == 4) {
+        if (rd[1] < rd[0]) { rd[0] = rd[1]; rs[0] = rs[1]; }
+        if (rd[3] < rd[2]) { rd[2] = rd[3]; rs[2] = rs[3]; }
+    }
+    if (rd[2] < rd[0]) { rd[0] = rd[2]; rs[0] = rs[2]; }
     dbest = rd[0];
     sbest = rs[0];
 }
@@ -722,7 +729,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
             }
             if (DD || I[k] != J[k]) {
                 if (R >= 0) unit_update<SYM>(U[k], L[k], I[k], J[k], R, S, ru, su, V);
-                if constexpr (WIDE) unit_select_wide(U[k], L[k], tb[k], I[k], J[k], thr, V, dk, sk); else unit_select<PACKED, NOTABU>(U[k], L[k], tb[k], I[k], J[k], thr, V, one, sixteen, dk, sk);
+                if constexpr (WIDE) unit_select_wide<(UR == 1 && SMEMU) ? 4 : 2>(U[k], L[k], tb[k], I[k], J[k], thr, V, dk, sk); else unit_select<PACKED, NOTABU>(U[k], L[k], tb[k], I[k], J[k], thr, V, one, sixteen, dk, sk);
             } else {
                 if (R >= 0) diag_update<SYM>(U[k], I[k], R, S, ru, su, V);
                 if constexpr (WIDE) diag_select_wide(U[k], tb[k], I[k], thr, V, dk, sk); else diag_select<PACKED>(U[k], tb[k], I[k], thr, V, dk, sk);
@@ -754,7 +761,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
                 }
                 delta_t dk;
                 int sk;
-                if constexpr (WIDE) unit_select_wide(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V, dk, sk); else unit_select<PACKED, NOTABU>(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V, one, sixteen, dk, sk);
+                if constexpr (WIDE) unit_select_wide<(UR == 1 && SMEMU) ? 4 : 2>(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V, dk, sk); else unit_select<PACKED, NOTABU>(Us, Ls, sTB[k2 * Toff + tid], Ik, Jk, thr, V, one, sixteen, dk, sk);
                 if (dk != MAXD) {
                     const unsigned key = pair_key(4 * Ik + (sk >> 2), 4 * Jk + (sk & 3), 0);
                     if (dk < my_d || (dk == my_d && key < my_key)) { my_d = dk; my_key = key; my_which = UR + k2; my_slot = sk; }
