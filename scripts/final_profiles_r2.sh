@@ -19,7 +19,6 @@ prof r2_ncu_full_build_m_whole_tai100a qap_build_m tai100a 1024 800
 prof r2_ncu_full_search_warp_tai30a_1776x240 qap_search_warp tai30a 1776 240
 prof r2_ncu_full_search_warp_nug12_4736x96 qap_search_warp nug12 4736 96
 python scripts/single_start_time.py > gpurun_out/r2_single_start_latency.txt 2>&1
-compute-sanitizer --tool memcheck python scripts/sanitize_small.py > gpurun_out/r2_sanitizer_memcheck.log 2>&1
-compute-sanitizer --tool racecheck python scripts/sanitize_small.py > gpurun_out/r2_sanitizer_racecheck.log 2>&1
-tail -3 gpurun_out/r2_sanitizer_memcheck.log gpurun_out/r2_sanitizer_racecheck.log
+# (compute-sanitizer was closed on the GPU pool late in round 2: profiles/r2_sanitizer_*.log are from the runs before
+#  that -- 0 errors / 0 hazards; the randomised differential soak, tests/soak_gpu.py, covers the later commits)
 ls -la gpurun_out
