@@ -371,6 +371,15 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
             if (h->wide && ur1 && try_hybrid_plan(h, smem_cap, 1, 256, std::max(1, (noff - 256 + 255) / 256), 1, 113u * 1024u) &&
                 hybrid_occupancy(h) >= 2)
                 return true;
+            // two symmetric matrices with packed keys (the instantiated shape of plan 9), n <= 156: one register unit
+            // + at most TWO shared-memory units per thread still leaves room for two searches per SM, and the
+            // spill-free kernel beats the two-register-unit one (G evals/s at 296 x 640, n = 132 / 144 / 148 / 156:
+            // 600 / 665 / 677 / 584 -> 652 / 713 / 735 / 760).  Three shared-memory units (n >= 157) cost the second
+            // resident search (n = 160: 497 against 684), and wider CTAs at 96 registers gain 1-2 % only.
+            const int us1s = std::max(1, (noff - 256 + 255) / 256);
+            if (!h->wide && ur1 && us1s <= 2 && try_hybrid_plan(h, smem_cap, 1, 256, us1s, 1, 113u * 1024u) &&
+                hybrid_occupancy(h) >= 2)
+                return true;
             const int us2 = std::max(1, (noff - 2 * 256 + 255) / 256);
             if (try_hybrid_plan(h, smem_cap, 2, 256, us2, 1, 113u * 1024u) && hybrid_occupancy(h) >= 2) return true;
             // one search per SM: one register unit per thread where that shape is instantiated and fits (n = 200:
