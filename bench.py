@@ -508,7 +508,8 @@ def run_ours(args) -> None:
                 ("nug12", "2opt", 1776, 48), ("nug12", "tabu", 4736, 96), ("tai30a", "tabu", 1, 1000),
                 ("tai30a", "tabu", 1776, 240), ("tai30a", "tabu", 4736, 240),
                 ("tai64c", "tabu", 1184, 512), ("tai100a", "2opt", 1184, 400), ("sko100", "tabu", 1184, 800),
-                ("rand100", "tabu", 1184, 800), ("tai150b", "tabu", 296, 1200), ("tai256c", "2opt", 148, 1024),
+                ("rand100", "tabu", 1184, 800), ("tai150b", "tabu", 296, 1200), ("tai160a", "tabu", 296, 640),
+                ("tai256c", "2opt", 148, 1024),
                 ("tai256c", "tabu", 148, 2048)))
         print(json.dumps({
             "metric": "swap_move_evals_per_sec", "value": value, "unit": "evals/s", "n_gpus": world,

@@ -105,6 +105,10 @@ typedef void (*kern_t)(const SearchParams);
 #define QAPB_DEV_ARGS 1, true, 1, true, false, QAPB_DEV_REGS, true, false, false
 #elif QAPB_DEV_ONLY == 41 // ... with 64-bit deltas, one symmetric matrix (tai150b: QAPB_PLAN=1,256,2,1)
 #define QAPB_DEV_ARGS 2, false, 1, true, false, QAPB_DEV_REGS, true, false, false, false, false, true
+#elif QAPB_DEV_ONLY == 42 // register-only plan at n = 129..180 (size class 256), one search per SM, multi-start tabu
+#define QAPB_DEV_ARGS 1, true, 1, false, false, QAPB_DEV_REGS, false, false, false, false, false, false, true
+#elif QAPB_DEV_ONLY == 43 // ... with 64-bit deltas, one symmetric matrix (tai150b)
+#define QAPB_DEV_ARGS 2, false, 1, false, false, 80, false, false, false, false, false, true, true
 #elif QAPB_DEV_ONLY == 20 // one warp per search (search_warp.cuh), symmetric, multi-start tabu
 #define QAPB_DEV_WARP 1, false, false, 32
 #elif QAPB_DEV_ONLY == 21 // ... recording instantiation
@@ -130,6 +134,7 @@ static kern_t pick_hybrid_kernel(int, int, int) { return (kern_t) QAPB_DEV_KERNE
 static kern_t multistart_kernel(int, int, int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
 static kern_t pick_wide_kernel(int, int) { return (kern_t) QAPB_DEV_KERNEL; }
 static kern_t pick_warp_kernel(int, int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
+static kern_t pick_np256_kernel(int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
 #else
 static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
 {
@@ -227,6 +232,18 @@ static kern_t pick_warp_kernel(int symm, int multistart, int two_opt, int lanes)
 #undef KW3
     return tab[lanes == 16][symm != 0][!multistart ? 0 : two_opt ? 2 : 1];
 }
+// Register-only plan at n = 129..176 (NP256: the n <= 128 kernel in layout size class 256), ONE search per SM on
+// noff + 64 threads: 72 registers up to 896 threads (n <= 164), 64 up to 1024 (n <= 176).  Two symmetric matrices
+// with packed keys; recording / multi-start tabu / multi-start 2opt instantiations.
+static kern_t pick_np256_kernel(int multistart, int two_opt, int regs)
+{
+#define KN(R) {(kern_t) qap_search_hybrid_kernel<1, true, 1, false, false, R, false, false, true, false, false, false, true>,  \
+               (kern_t) qap_search_hybrid_kernel<1, true, 1, false, false, R, false, false, false, false, false, false, true>, \
+               (kern_t) qap_search_hybrid_kernel<1, true, 1, false, false, R, false, true, false, false, false, false, true>}
+    static kern_t tab[2][3] = {KN(72), KN(64)};
+#undef KN
+    return tab[regs == 64][!multistart ? 0 : two_opt ? 2 : 1];
+}
 #endif
 
 // Resident CTAs per SM of `k` at this handle's CTA size and shared memory (cached: the query costs more than
@@ -261,6 +278,7 @@ static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_op
     if (h->dd) plan = h->ow ? 8 : h->staged ? 7 : 6;
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
     if (h->storage == 3 && h->wk) return pick_warp_kernel(h->symmetric ? 1 : 0, multistart, two_opt, h->wk);
+    if (h->storage == 3 && h->npad > 128 && h->us == 0) return pick_np256_kernel(multistart, two_opt, h->threads <= 896 ? 72 : 64);
     if (h->storage == 3 && h->wide) return pick_wide_kernel(symm, plan);
     if (multistart && h->storage == 3) {
         // 88 registers per thread where that keeps as many CTAs resident as 80 do (asked of the runtime)
@@ -318,10 +336,13 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     }
     if (L.total > smem_cap) return false;
     if (threads < h->n) return false;  // the publish phase maps one location per thread
-    if (h->npad > 128 && !(us > 0 && (ur == 2 || (ur == 1 && dsm)))) return false;  // layout size class 256 goes with shared-memory units
+    // layout size class 256 goes with shared-memory units -- or with the register-only plan of one search per SM (NP256)
+    const bool reg_only_256 = h->npad > 128 && us == 0 && ur == 1 && !dsm && !dd;
+    if (reg_only_256 && !(!h->wide && h->symmetric && h->delta_bound < ((1LL << 27) - 1) && toff >= h->noff)) return false;  // the instantiated shape
+    if (h->npad > 128 && !reg_only_256 && !(us > 0 && (ur == 2 || (ur == 1 && dsm)))) return false;
     if (h->npad <= 128 && us > 0) return false;
     int staged = 0;
-    if (us == 0 && h->fits_i16 && !ow && !getenv("QAPB_NO_STAGE")) {
+    if (us == 0 && h->fits_i16 && !ow && !reg_only_256 && !getenv("QAPB_NO_STAGE")) {
         // stage while two CTAs per SM still fit
         HybLayout Ls = make_hyb_layout(h->npad, nb, toff, us, exp_in_smem, 1, h->symmetric, dsm);
         if (Ls.total <= std::min(smem_cap, ((dsm || dd) ? 74u : 110u) * 1024u)) { staged = 1; L = Ls; }
@@ -357,6 +378,14 @@ static bool plan_hybrid(qapb_handle *h, unsigned smem_cap)
     }
     // n <= 32: one warp per search (no block barriers, no register-indexed fix-ups)
     if (!getenv("QAPB_NO_WARP") && try_hybrid_plan(h, smem_cap, 0, 32, 0)) return true;
+    if (nb > 32 && !h->wide && !getenv("QAPB_NO_REGONLY256")) {
+        // n = 129..176, two symmetric matrices, packed keys: the register-only kernel of n <= 128 on ONE search per SM
+        // (noff + 64 threads, 72 / 64 registers, no spills, no shared-memory units): tabu 296 x 640 at n = 132 / 144 /
+        // 148 / 152 / 156 / 160 / 164 / 176: 736 / 811 / 835 / 842 / 832 / 854 / 873 / 898 G evals/s against 653 / 714 /
+        // 736 / 762 / 759 / 684 / 683 / 732 for the shared-memory plans with two searches per SM
+        const int tro = (noff + 31) / 32 * 32;
+        if (tro + 64 <= 1024 && try_hybrid_plan(h, smem_cap, 1, tro, 0) && hybrid_occupancy(h) >= 1) return true;
+    }
     if (nb > 32) {
         // n = 129..256: every warp on off-diagonal units (two in registers + the rest in shared memory per
         // thread), the diagonal blocks in shared memory with the last nb threads (DSM).  Preferred: 256
@@ -430,6 +459,7 @@ static std::vector<std::array<int, 4>> hybrid_candidates(const qapb_handle *h)
     if (nb > 32) {
         for (int t : {256, 384, 512}) add(2, t, std::max(1, (noff - 2 * t + t - 1) / t), 1);
         for (int t : {256, 512}) add(1, t, std::max(1, (noff - t + t - 1) / t), 1);  // (kept if the shape is instantiated for the instance)
+        if (!h->wide && (noff + 31) / 32 * 32 + 64 <= 1024) add(1, (noff + 31) / 32 * 32, 0, 0);  // register-only, one search per SM (likewise)
         const int toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
         if (!h->wide) add(2, toff, std::max(0, (noff - 2 * toff + toff - 1) / toff), 0);
     } else {

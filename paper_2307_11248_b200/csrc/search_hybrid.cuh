@@ -467,7 +467,7 @@ __device__ __forceinline__ void expire_bits(unsigned &tb, int32_t &mexp, int c, 
 // argmin is already the result, and 32 independent searches share an SM (size class 32 of the shared-memory
 // layout: 5.6 KB per search).
 template <int SYMM, bool PACKED, int UR, bool SMEMU, bool STG, int MAXREG, bool DSM = false, bool NOTABU = false,
-          bool REC = true, bool DD = false, bool OW = false, bool WIDE = false>
+          bool REC = true, bool DD = false, bool OW = false, bool WIDE = false, bool NP256 = false>
 __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams P)
 {
     static_assert(!OW || (DD && !STG), "one-warp searches: paired diagonal blocks, no staged matrices");
@@ -487,7 +487,7 @@ __global__ void __maxnreg__(MAXREG) qap_search_hybrid_kernel(const SearchParams 
     int32_t *sM = reinterpret_cast<int32_t *>(smem_raw + lay.offM);
     unsigned *sTB = reinterpret_cast<unsigned *>(smem_raw + lay.offTB);
     int32_t *sMX = reinterpret_cast<int32_t *>(smem_raw + lay.offMX);
-    constexpr int NPM = OW ? 32 : SMEMU ? 256 : 128;  // size class of the plan (host: make_hyb_layout; shared-memory units <=> n > 128)
+    constexpr int NPM = OW ? 32 : (SMEMU || NP256) ? 256 : 128;  // size class of the plan (host: make_hyb_layout: n > 128 <=> shared-memory units or NP256)
     Vecs V;
     V.A = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(0, NPM));
     V.C = reinterpret_cast<int32_t *>(smem_raw + HYB_VEC(1, NPM));

@@ -36,7 +36,7 @@ def _check_single(di, oracle, f, d, perm, iters, ten, tag):
 
 
 @pytest.mark.parametrize("n,kind,hi", [(129, 3, 60), (160, 3, 99), (160, 1, 30), (200, 3, 99), (200, 0, 20),
-                                       (256, 3, 99), (256, 2, 12), (144, 3, 3000), (100, 3, 99), (100, 0, 99),
+                                       (256, 3, 99), (256, 2, 12), (144, 3, 3000), (164, 3, 50), (176, 3, 99), (100, 3, 99), (100, 0, 99),
                                        (64, 3, 99), (33, 1, 1000), (30, 3, 99), (12, 0, 50)])
 def test_short_tenures_every_plan(built, n, kind, hi):
     import oracle
@@ -91,5 +91,36 @@ def test_two_opt_every_plan(built, n, hi):
                 di.set_plan(plan)
             g = di.two_opt(perm, 48)
             assert all(np.array_equal(a[0], b) for a, b in zip(g, w)), (n, plan)
+    finally:
+        di.close()
+
+
+@pytest.mark.parametrize("n,hi", [(130, 99), (152, 60), (164, 99), (176, 40)])
+def test_register_only_plan_above_128(built, n, hi):
+    """n = 129..176 with two symmetric matrices and packed keys run by default on the register-only kernel of
+    n <= 128 in layout size class 256 (one search per SM on noff + 64 threads; 72 registers up to n = 164, 64 above):
+    the recording, the multi-start tabu and the multi-start 2opt instantiations against the oracle."""
+    import oracle
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    rs = np.random.default_rng(7 * n)
+    f, d = _instance(rs, n, 3, hi)
+    nb = (n + 3) // 4
+    noff = nb * (nb - 1) // 2
+    di = DeviceInstance(f, d)
+    try:
+        info = di.info
+        assert info["storage"] == 3 and info["units_per_thread"] == 1 and info["ctas_per_sm"] == 1, info
+        assert info["threads"] == (noff + 31) // 32 * 32 + 64, info
+        iters = 80
+        rng = oracle.Rng(oracle.derive_seed(n, 1))
+        perm = di.two_opt(rng.permutation(n), 3 * n, moves=False)[2][0]
+        _check_single(di, oracle, f, d, perm, iters, rng.tenures(1, 3, iters), (n, "short tenures"))
+        lo, hi_t = oracle.tenure_bounds(n)
+        for algo in ("tabu", "2opt"):
+            got = di.multistart(algo, 11, 0, 5, iters, lo, hi_t)
+            want = oracle.multistart(f, d, algo, 11, 5, iters, threads=oracle.max_threads())
+            assert np.array_equal(got[0], want[0]) and got[1:3] == (want[1], want[2]), (n, algo)
+            assert np.array_equal(got[3], want[3]), (n, algo)
     finally:
         di.close()
