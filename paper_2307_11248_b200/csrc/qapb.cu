@@ -233,16 +233,16 @@ static kern_t pick_warp_kernel(int symm, int multistart, int two_opt, int lanes)
     return tab[lanes == 16][symm != 0][!multistart ? 0 : two_opt ? 2 : 1];
 }
 // Register-only plan at n = 129..176 (NP256: the n <= 128 kernel in layout size class 256), ONE search per SM on
-// noff + 64 threads: 72 registers up to 896 threads (n <= 164), 64 up to 1024 (n <= 176).  Two symmetric matrices
+// noff + 64 threads: 80 registers up to 800 threads (n <= 152; +3 % over 72), 72 up to 896 (n <= 164), 64 up to 1024 (n <= 176).  Two symmetric matrices
 // with packed keys; recording / multi-start tabu / multi-start 2opt instantiations.
 static kern_t pick_np256_kernel(int multistart, int two_opt, int regs)
 {
 #define KN(R) {(kern_t) qap_search_hybrid_kernel<1, true, 1, false, false, R, false, false, true, false, false, false, true>,  \
                (kern_t) qap_search_hybrid_kernel<1, true, 1, false, false, R, false, false, false, false, false, false, true>, \
                (kern_t) qap_search_hybrid_kernel<1, true, 1, false, false, R, false, true, false, false, false, false, true>}
-    static kern_t tab[2][3] = {KN(72), KN(64)};
+    static kern_t tab[3][3] = {KN(80), KN(72), KN(64)};
 #undef KN
-    return tab[regs == 64][!multistart ? 0 : two_opt ? 2 : 1];
+    return tab[regs == 64 ? 2 : regs == 72 ? 1 : 0][!multistart ? 0 : two_opt ? 2 : 1];
 }
 #endif
 
@@ -278,7 +278,7 @@ static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_op
     if (h->dd) plan = h->ow ? 8 : h->staged ? 7 : 6;
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
     if (h->storage == 3 && h->wk) return pick_warp_kernel(h->symmetric ? 1 : 0, multistart, two_opt, h->wk);
-    if (h->storage == 3 && h->npad > 128 && h->us == 0) return pick_np256_kernel(multistart, two_opt, h->threads <= 896 ? 72 : 64);
+    if (h->storage == 3 && h->npad > 128 && h->us == 0) return pick_np256_kernel(multistart, two_opt, h->threads <= 800 ? 80 : h->threads <= 896 ? 72 : 64);
     if (h->storage == 3 && h->wide) return pick_wide_kernel(symm, plan);
     if (multistart && h->storage == 3) {
         // 88 registers per thread where that keeps as many CTAs resident as 80 do (asked of the runtime)
