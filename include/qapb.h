@@ -177,7 +177,9 @@ int qapb_multistart_trace_host(qapb_handle *h, int algo, const uint64_t *seeds, 
  * threads carrying off-diagonal units, shared-memory units per thread, diagonal blocks in shared
  * memory (0/1)} -- register units 0 names the one-warp-per-search kernel (n <= 32, the default there); {1, T, 0, 0} at
  * n > 128 is the register-only plan with one search per SM (n <= 176, two symmetric matrices; the default there); `qapb_set_plan` re-plans the handle with one of them (results are identical under
- * every plan; only the speed differs).  Instances served by the generic kernel have no candidates. */
+ * every plan; only the speed differs).  Instances served by the generic kernel have no candidates.
+ * Instances with 64-bit deltas at n = 129..152 are re-planned by `qapb_multistart` itself according to the batch
+ * size (at most one search per SM: register-only) until `qapb_set_plan` names a plan. */
 int qapb_plan_candidates(qapb_handle *h, int32_t *plans /* [cap][4] */, int cap, int *count);
 int qapb_set_plan(qapb_handle *h, int reg_units, int unit_threads, int smem_units, int diag_in_smem);
 

@@ -51,6 +51,11 @@ struct qapb_handle {
     int wide = 0;                                  // hybrid: unsigned 32-bit state with 64-bit deltas (acc_bits holds the STATE width, 32)
     int wk = 0;                                    // lanes per search (32, or 16 at n <= 16) of the warp kernel (search_warp.cuh; n <= 32), 0 = other plans
     int wpc = 1;                                   // ... warps per CTA
+    // 64-bit deltas at n > 128: the default plan (two searches per SM, part of the state in shared memory) wins when both
+    // slots of every SM are taken; a batch of at most one search per SM runs faster on the register-only plan (tai150b,
+    // 148 starts: 477 against 356 G evals/s).  qapb_multistart switches between the two by batch size unless the caller
+    // chose a plan itself (qapb_set_plan) -- results are identical under every plan.
+    int have_alt = 0, user_plan = 0, def_plan[4] = {0, 0, 0, 0}, alt_plan[4] = {0, 0, 0, 0};
     unsigned smem_bytes = 0;
     int ctas_per_sm = 0, sm_count = 0;
     long long delta_bound = 0;
@@ -135,6 +140,7 @@ static kern_t multistart_kernel(int, int, int, int, int) { return (kern_t) QAPB_
 static kern_t pick_wide_kernel(int, int) { return (kern_t) QAPB_DEV_KERNEL; }
 static kern_t pick_warp_kernel(int, int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
 static kern_t pick_np256_kernel(int, int, int) { return (kern_t) QAPB_DEV_KERNEL; }
+static kern_t pick_wide_np256_kernel(int) { return (kern_t) QAPB_DEV_KERNEL; }
 #else
 static kern_t pick_kernel(int acc_bits, int storage, int lb_class)
 {
@@ -244,6 +250,14 @@ static kern_t pick_np256_kernel(int multistart, int two_opt, int regs)
 #undef KN
     return tab[regs == 64 ? 2 : regs == 72 ? 1 : 0][!multistart ? 0 : two_opt ? 2 : 1];
 }
+// ... with 64-bit deltas (80 registers, at most 800 threads: n <= 152), per symmetry class
+static kern_t pick_wide_np256_kernel(int symm)
+{
+#define KWN(S) (kern_t) qap_search_hybrid_kernel<S, false, 1, false, false, 80, false, false, true, false, false, true, true>
+    static kern_t tab[3] = {KWN(0), KWN(1), KWN(2)};
+#undef KWN
+    return tab[symm];
+}
 #endif
 
 // Resident CTAs per SM of `k` at this handle's CTA size and shared memory (cached: the query costs more than
@@ -278,6 +292,7 @@ static kern_t handle_kernel(const qapb_handle *h, int multistart = 0, int two_op
     if (h->dd) plan = h->ow ? 8 : h->staged ? 7 : 6;
     const int symm = h->symmetric ? 1 : (h->sym_mode >= 2 ? 2 : 0);
     if (h->storage == 3 && h->wk) return pick_warp_kernel(h->symmetric ? 1 : 0, multistart, two_opt, h->wk);
+    if (h->storage == 3 && h->npad > 128 && h->us == 0 && h->wide) return pick_wide_np256_kernel(symm);
     if (h->storage == 3 && h->npad > 128 && h->us == 0) return pick_np256_kernel(multistart, two_opt, h->threads <= 800 ? 80 : h->threads <= 896 ? 72 : 64);
     if (h->storage == 3 && h->wide) return pick_wide_kernel(symm, plan);
     if (multistart && h->storage == 3) {
@@ -338,7 +353,8 @@ static bool try_hybrid_plan(qapb_handle *h, unsigned smem_cap, int ur, int toff,
     if (threads < h->n) return false;  // the publish phase maps one location per thread
     // layout size class 256 goes with shared-memory units -- or with the register-only plan of one search per SM (NP256)
     const bool reg_only_256 = h->npad > 128 && us == 0 && ur == 1 && !dsm && !dd;
-    if (reg_only_256 && !(!h->wide && h->symmetric && h->delta_bound < ((1LL << 27) - 1) && toff >= h->noff)) return false;  // the instantiated shape
+    // the instantiated shapes: two symmetric matrices with packed keys, or 64-bit deltas on at most 800 threads
+    if (reg_only_256 && !(toff >= h->noff && (h->wide ? toff + 32 * dw <= 800 : (h->symmetric && h->delta_bound < ((1LL << 27) - 1))))) return false;
     if (h->npad > 128 && !reg_only_256 && !(us > 0 && (ur == 2 || (ur == 1 && dsm)))) return false;
     if (h->npad <= 128 && us > 0) return false;
     int staged = 0;
@@ -459,7 +475,7 @@ static std::vector<std::array<int, 4>> hybrid_candidates(const qapb_handle *h)
     if (nb > 32) {
         for (int t : {256, 384, 512}) add(2, t, std::max(1, (noff - 2 * t + t - 1) / t), 1);
         for (int t : {256, 512}) add(1, t, std::max(1, (noff - t + t - 1) / t), 1);  // (kept if the shape is instantiated for the instance)
-        if (!h->wide && (noff + 31) / 32 * 32 + 64 <= 1024) add(1, (noff + 31) / 32 * 32, 0, 0);  // register-only, one search per SM (likewise)
+        if ((noff + 31) / 32 * 32 + 64 <= 1024) add(1, (noff + 31) / 32 * 32, 0, 0);  // register-only, one search per SM (likewise)
         const int toff = std::min(448, ((noff + 3) / 4 + 31) / 32 * 32);
         if (!h->wide) add(2, toff, std::max(0, (noff - 2 * toff + toff - 1) / toff), 0);
     } else {
@@ -803,6 +819,15 @@ extern "C" int qapb_create(int n, const int64_t *flow, const int64_t *dist, int 
         }
     }
     h->storage = storage;
+    if (storage == 3 && h->wide && h->npad > 128 && !h->dd && !getenv("QAPB_NO_AUTOPLAN")) {
+        qapb_handle probe = *h;
+        const int tro = (h->noff + 31) / 32 * 32;
+        if (h->us > 0 && try_hybrid_plan(&probe, smem_cap, 1, tro, 0, 0) && hybrid_occupancy(&probe) >= 1) {
+            h->have_alt = 1;
+            h->def_plan[0] = h->upt; h->def_plan[1] = h->toff; h->def_plan[2] = h->us; h->def_plan[3] = h->dsm;
+            h->alt_plan[0] = 1; h->alt_plan[1] = tro; h->alt_plan[2] = 0; h->alt_plan[3] = 0;
+        }
+    }
 
     // device copies: one arena, filled in a pinned staging buffer and uploaded with one copy
     const size_t mb = (size_t)npad * npad * sizeof(int32_t), vb = (size_t)npad * sizeof(int32_t);
@@ -1151,6 +1176,8 @@ extern "C" int qapb_tabu(qapb_handle *h, const int64_t *perms, int batch, int it
     return launch_search(h, P, batch, 0, (cudaStream_t)stream);
 }
 
+static int apply_plan(qapb_handle *h, int reg_units, int unit_threads, int smem_units, int diag_in_smem);
+
 extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, uint64_t first_index, int count,
                                int iterations, int64_t ten_low, int64_t ten_high, int64_t *per_start_costs,
                                int64_t *best_key, int64_t *best_perm, void *stream)
@@ -1164,6 +1191,14 @@ extern "C" int qapb_multistart(qapb_handle *h, int algo, uint64_t master_seed, u
     if (algo == QAPB_ALGO_TABU && (double)iterations + (double)ten_high >= 2147483647.0)
         return fail(QAPB_ERR_UNSUPPORTED, "iterations + tenure must fit int32");
     if (!per_start_costs || !best_key || !best_perm) return fail(QAPB_ERR_INVALID, "NULL buffer");
+    if (h->have_alt && !h->user_plan) {
+        // at most one search per SM: the register-only plan; more: the default (see qapb_handle::have_alt)
+        const int *want = count <= h->sm_count ? h->alt_plan : h->def_plan;
+        if (want[0] != h->upt || want[1] != h->toff || want[2] != h->us || want[3] != h->dsm) {
+            rc = apply_plan(h, want[0], want[1], want[2], want[3]);
+            if (rc) return rc;
+        }
+    }
     const int n = h->n;
     // workspace head: best perms [count,n], cur perms [count,n], cur costs [count], steps [count], total steps [1]
     const size_t perm_bytes = (size_t)count * n * sizeof(int64_t);
@@ -1305,10 +1340,9 @@ extern "C" int qapb_plan_candidates(qapb_handle *h, int32_t *plans, int cap, int
     return QAPB_OK;
 }
 
-extern "C" int qapb_set_plan(qapb_handle *h, int reg_units, int unit_threads, int smem_units, int diag_in_smem)
+// Re-plan a handle (qapb_set_plan, and the batch-size switch of qapb_multistart).
+static int apply_plan(qapb_handle *h, int reg_units, int unit_threads, int smem_units, int diag_in_smem)
 {
-    if (!h) return fail(QAPB_ERR_INVALID, "NULL handle");
-    if (h->storage != 3) return fail(QAPB_ERR_UNSUPPORTED, "this instance runs in the generic kernel: no alternative plans");
     CU(cudaSetDevice(h->device));
     if (h->have_timing) CU(cudaEventSynchronize(h->ev1));  // no launch of the old plan in flight
     qapb_handle probe = *h;
@@ -1323,6 +1357,15 @@ extern "C" int qapb_set_plan(qapb_handle *h, int reg_units, int unit_threads, in
     fill_unit_table(h, units.data());
     CU(cudaMemcpy(h->dunit, units.data(), units.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
     return QAPB_OK;
+}
+
+extern "C" int qapb_set_plan(qapb_handle *h, int reg_units, int unit_threads, int smem_units, int diag_in_smem)
+{
+    if (!h) return fail(QAPB_ERR_INVALID, "NULL handle");
+    if (h->storage != 3) return fail(QAPB_ERR_UNSUPPORTED, "this instance runs in the generic kernel: no alternative plans");
+    const int rc = apply_plan(h, reg_units, unit_threads, smem_units, diag_in_smem);
+    if (rc == QAPB_OK) h->user_plan = 1;  // the caller's choice stands: no switching by batch size
+    return rc;
 }
 
 extern "C" int qapb_last_total_steps(qapb_handle *h, int64_t *steps)

@@ -124,3 +124,43 @@ def test_register_only_plan_above_128(built, n, hi):
             assert np.array_equal(got[3], want[3]), (n, algo)
     finally:
         di.close()
+
+
+def test_wide_plan_follows_the_batch_size(built):
+    """64-bit deltas at n > 128 (the tai150b shape): a batch of at most one search per SM runs on the register-only
+    plan, a larger one on the default plan with two searches per SM (qapb_handle::have_alt); qapb_set_plan pins the
+    plan.  Results equal the oracle's either way."""
+    import oracle
+    from paper_2307_11248_b200 import shapes
+    from paper_2307_11248_b200.backend import DeviceInstance
+
+    inst = shapes.by_name("tai150b")
+    f, d = np.asarray(inst.flow), np.asarray(inst.distance)
+    n = inst.n
+    nb = (n + 3) // 4
+    tro = (nb * (nb - 1) // 2 + 31) // 32 * 32
+    lo, hi = oracle.tenure_bounds(n)
+    di = DeviceInstance(f, d)
+    try:
+        assert di.info["acc_bits"] == 64 and di.info["storage"] == 3
+        default_threads = di.info["threads"]
+        sm = di.info["sm_count"]
+        got = di.multistart("tabu", 3, 0, 6, 48, lo, hi)
+        di._refresh_info()  # (the cached dict is refreshed by set_plan only)
+        assert di.info["threads"] == tro + 64 and di.info["ctas_per_sm"] == 1, di.info
+        want = oracle.multistart(f, d, "tabu", 3, 6, 48, threads=oracle.max_threads())
+        assert np.array_equal(got[0], want[0]) and got[1:3] == (want[1], want[2]) and np.array_equal(got[3], want[3])
+        big = di.multistart("tabu", 3, 0, sm + 8, 6, lo, hi)
+        di._refresh_info()
+        assert di.info["threads"] == default_threads, di.info
+        want_big = oracle.multistart(f, d, "tabu", 3, sm + 8, 6, threads=oracle.max_threads())
+        assert np.array_equal(big[0], want_big[0]) and big[1:3] == (want_big[1], want_big[2])
+        # a caller's own choice stands
+        plan = [p for p in di.plan_candidates() if p[2] > 0][0]
+        di.set_plan(plan)
+        pinned = di.info["threads"]
+        again = di.multistart("tabu", 3, 0, 6, 48, lo, hi)
+        di._refresh_info()
+        assert di.info["threads"] == pinned and np.array_equal(again[0], want[0])
+    finally:
+        di.close()
